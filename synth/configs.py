@@ -1,0 +1,211 @@
+"""Seeded problem builders for BASELINE.json configs[0..4] (and custom sizes).
+
+Everything here is INPUT DATA. Readings:
+  A1  SOAR distance is chordal: d = (C/pi)|sin(pi*(x_i-x_j)/C)|, C = domain
+      length (1 for the heat grid on [0,1), s index units for Lorenz-96).
+  A2  SOAR(d) = var * (1 + d/L) * exp(-d/L)   (BJ.c0 writes "(1+d/0.2)exp(-d/0.2)").
+  A3  RHS by linearising about the background forecast x^(0):
+      x^(0)_0 = x_b, x^(0)_w = M_w(x^(0)_{w-1}); b = 0 (b_0 = x_b - x^(0)_0 = 0,
+      b_w = M_w(x^(0)_{w-1}) - x^(0)_w = 0), d_w = y_w - H x^(0)_w.
+  A14 H_w selects every q-th state point starting at 0 (idx_j = q*j), same for all w.
+  A15 numpy Generator(PCG64(seed)); RHS/problem column j uses seed (seed0 + j);
+      draw order: x_0^t, model noise w=1..N, observation noise w=0..N, background.
+The truth/background model propagation below is workload synthesis (it builds
+y and x_b); the operator M_w used by the METHOD is implemented separately by
+oracle/ and by the CUDA library.
+"""
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+import scipy.linalg as sla
+
+from .layout import pack
+
+# (length, variance) pairs; heat grids live on [0,1) with spacing 1/s.
+CONFIGS = {
+    0: dict(model="heat", s=50, N=4, q=2, m=1, B=(0.2, 1.0), Q=(0.2, 0.1),
+            R=(0.1, 0.05), heat_r=0.25,
+            desc="BJ.c0 heat s=50 N=4 p=25 single RHS"),
+    1: dict(model="heat", s=1000, N=20, q=2, m=16, B=(0.05, 1.0), Q=(0.05, 0.1),
+            R=(0.02, 0.05), heat_r=0.25,
+            desc="BJ.c1 heat s=1000 N=20 p=500, 16 RHS"),
+    2: dict(model="l96", s=40, N=50, q=2, m=1024, B=(2.0, 1.0), Q=(2.0, 0.1),
+            R=(1.0, 0.1), F=8.0, dt=0.025, nsub=5, spinup=1000,
+            desc="BJ.c2 Lorenz-96 TLM s=40 N=50 p=20, 1024 problems"),
+    3: dict(model="heat", s=4096, N=127, q=4, m=64, B=(0.01, 1.0), Q=(0.01, 0.1),
+            R=(0.005, 0.05), heat_r=0.25,
+            desc="BJ.c3 heat s=4096 N=127 p=1024, 64 RHS"),
+    4: dict(model="heat", s=2048, N=31, q=1, m=256, B=(0.02, 1.0), Q=(0.02, 0.1),
+            R=(0.1, 0.01), heat_r=0.25,
+            desc="BJ.c4 heat s=2048 N=31 p=2048, 256 RHS"),
+}
+
+
+@dataclass
+class Problem:
+    name: str
+    model: str              # "heat" | "l96" | "dense"
+    s: int
+    p: int
+    N: int
+    m: int
+    B: np.ndarray           # [s,s]
+    Q: np.ndarray           # [s,s] shared by windows 1..N
+    R: np.ndarray           # [p,p] shared by windows 0..N
+    H_idx: np.ndarray       # [p] int32, strictly increasing
+    heat_r: float = 0.0
+    F: float = 8.0
+    dt: float = 0.0
+    nsub: int = 0
+    traj: Optional[np.ndarray] = None     # l96: [N][s][m] start state of window w-1 for M_w
+    M_dense: Optional[np.ndarray] = None  # dense model: [N][s][s] (M_w for w=1..N)
+    rhs: Optional[np.ndarray] = None      # flat library layout, (2s+p)*W*m
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def W(self):
+        return self.N + 1
+
+    @property
+    def n(self):
+        return (2 * self.s + self.p) * self.W * self.m
+
+
+def chordal_distance(lag, C):
+    """Chordal distance on a circle of circumference C for a lag in the same units."""
+    return (C / np.pi) * np.abs(np.sin(np.pi * np.asarray(lag, dtype=np.float64) / C))
+
+
+def soar(d, L, var):
+    d = np.asarray(d, dtype=np.float64)
+    return var * (1.0 + d / L) * np.exp(-d / L)
+
+
+def soar_matrix(positions, C, L, var):
+    """Dense SOAR covariance between points at `positions` on a circle of length C."""
+    pos = np.asarray(positions, dtype=np.float64)
+    lag = pos[:, None] - pos[None, :]
+    return soar(chordal_distance(lag, C), L, var)
+
+
+def heat_lap(s):
+    """Periodic second-difference matrix (diag -2, off-diagonals +1), unscaled."""
+    Lap = -2.0 * np.eye(s)
+    i = np.arange(s)
+    Lap[i, (i + 1) % s] += 1.0
+    Lap[i, (i - 1) % s] += 1.0
+    return Lap
+
+
+def _l96_rhs(x, F):
+    # dx_i/dt = (x_{i+1} - x_{i-2}) x_{i-1} - x_i + F, axis 0 = state
+    return (np.roll(x, -1, 0) - np.roll(x, 2, 0)) * np.roll(x, 1, 0) - x + F
+
+
+def _l96_rk4(x, dt, F):
+    k1 = _l96_rhs(x, F)
+    k2 = _l96_rhs(x + 0.5 * dt * k1, F)
+    k3 = _l96_rhs(x + 0.5 * dt * k2, F)
+    k4 = _l96_rhs(x + dt * k3, F)
+    return x + dt / 6.0 * (k1 + 2 * k2 + 2 * k3 + k4)
+
+
+def _gaussian(rng_list, chol, shape_first):
+    """Draw one N(0, C) sample per column generator: returns [n, m]."""
+    z = np.stack([g.standard_normal(shape_first) for g in rng_list], axis=1)
+    return chol @ z
+
+
+def _build(name, model, s, N, q, m, Bp, Qp, Rp, seed0, heat_r=0.25, F=8.0, dt=0.025,
+           nsub=5, spinup=1000, with_rhs=True, domain=None):
+    W = N + 1
+    H_idx = (np.arange(0, s, q)).astype(np.int32)
+    p = H_idx.size
+    if model == "heat":
+        C = 1.0
+        pos_state = np.arange(s) / s
+    else:
+        C = float(s)
+        pos_state = np.arange(s, dtype=np.float64)
+    pos_obs = pos_state[H_idx]
+    B = soar_matrix(pos_state, C, *Bp)
+    Q = soar_matrix(pos_state, C, *Qp)
+    R = soar_matrix(pos_obs, C, *Rp)
+    prob = Problem(name=name, model=model, s=s, p=p, N=N, m=m, B=B, Q=Q, R=R,
+                   H_idx=H_idx, heat_r=heat_r, F=F, dt=dt, nsub=nsub)
+    if not with_rhs:
+        return prob
+    rngs = [np.random.Generator(np.random.PCG64(seed0 + j)) for j in range(m)]
+    cB = np.linalg.cholesky(B)
+    cQ = np.linalg.cholesky(Q)
+    cR = np.linalg.cholesky(R)
+    if model == "heat":
+        lu = sla.lu_factor(np.eye(s) - heat_r * heat_lap(s))
+        step = lambda x: sla.lu_solve(lu, x)  # truth/forecast model (synthesis only)
+        x0t = _gaussian(rngs, cB, s)
+    else:
+        def step(x):
+            for _ in range(nsub):
+                x = _l96_rk4(x, dt, F)
+            return x
+        spin = F + 0.01 * np.stack([g.standard_normal(s) for g in rngs], axis=1)
+        for _ in range(spinup):
+            spin = _l96_rk4(spin, dt, F)
+        x0t = spin
+    truth = [x0t]
+    for w in range(1, W):
+        truth.append(step(truth[-1]) + _gaussian(rngs, cQ, s))
+    y = [truth[w][H_idx] + _gaussian(rngs, cR, p) for w in range(W)]
+    xb = x0t + _gaussian(rngs, cB, s)
+    guess = [xb]
+    for w in range(1, W):
+        guess.append(step(guess[-1]))
+    eta = np.zeros((s, W, m))            # b = 0 (reading A3)
+    nu = np.stack([y[w] - guess[w][H_idx] for w in range(W)], axis=1)   # [p][W][m]
+    xx = np.zeros((s, W, m))
+    prob.rhs = pack(eta, nu, xx)
+    if model == "l96":
+        prob.traj = np.ascontiguousarray(np.stack(guess[:N], axis=0))  # [N][s][m]
+    prob.extra = dict(truth=np.stack(truth, 1), xb=xb, guess=np.stack(guess, 1), y=np.stack(y, 1))
+    return prob
+
+
+def make_problem(cfg, seed0=0, m=None, N=None, with_rhs=True):
+    """Build BASELINE.json configs[cfg]; optionally override batch width m or N."""
+    c = dict(CONFIGS[cfg])
+    mm = c["m"] if m is None else m
+    NN = c["N"] if N is None else N
+    kw = {}
+    if c["model"] == "l96":
+        kw = dict(F=c["F"], dt=c["dt"], nsub=c["nsub"], spinup=c["spinup"])
+    else:
+        kw = dict(heat_r=c["heat_r"])
+    return _build(f"c{cfg}", c["model"], c["s"], NN, c["q"], mm, c["B"], c["Q"], c["R"],
+                  seed0, with_rhs=with_rhs, **kw)
+
+
+def custom_problem(s, N, q, m, model="heat", seed0=0, Bp=(0.1, 1.0), Qp=(0.1, 0.1),
+                   Rp=(0.05, 0.05), heat_r=0.25, **kw):
+    """Parity-test sizes: same recipe, arbitrary (s, N, q, m)."""
+    return _build(f"custom_s{s}_N{N}_q{q}_m{m}", model, s, N, q, m, Bp, Qp, Rp, seed0,
+                  heat_r=heat_r, **kw)
+
+
+def random_dense_problem(s, p, N, m, seed=0):
+    """Generic small problem with random dense SPD B,Q,R, random dense M_w and a
+    random strictly-increasing selection H (tests the general API paths)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+
+    def spd(n):
+        A = rng.standard_normal((n, n))
+        return A @ A.T / n + 0.5 * np.eye(n)
+
+    B, Q, R = spd(s), spd(s), spd(p)
+    H_idx = np.sort(rng.choice(s, size=p, replace=False)).astype(np.int32)
+    M = rng.standard_normal((N, s, s)) / np.sqrt(s)
+    W = N + 1
+    prob = Problem(name=f"dense_s{s}_p{p}_N{N}_m{m}", model="dense", s=s, p=p, N=N, m=m,
+                   B=B, Q=Q, R=R, H_idx=H_idx, M_dense=M)
+    prob.rhs = rng.standard_normal((2 * s + p) * W * m)
+    return prob
