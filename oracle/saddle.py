@@ -59,6 +59,7 @@ class Saddle:
         self.Hi = selection_matrix(prob.H_idx, prob.s)
         self.Ms = Ms if Ms is not None else model_matrices(prob, col)
         self.counters = dict(R=0, Rhat_inv=0, D=0, Dhat_inv=0, M=0)
+        self._cache = {}
 
     # ----- helpers ------------------------------------------------------
     def Dblk(self, w):
@@ -78,7 +79,17 @@ class Saddle:
         return np.concatenate(list(a) + list(b) + list(c))
 
     def rhat_matrix(self, pc):
-        return RH.rhat(self.R, pc.rhat, pc.gamma, pc.T, pc.block)
+        key = ("Rhat", pc.rhat, pc.gamma, pc.T, pc.block)
+        if key not in self._cache:
+            self._cache[key] = RH.rhat(self.R, pc.rhat, pc.gamma, pc.T, pc.block)
+        return self._cache[key]
+
+    def _spd_solve(self, key, mat_fn, rhs):
+        """Solve with an SPD block; the Cholesky factorisation of each distinct
+        block is computed once and reused (scipy cho_factor / cho_solve)."""
+        if key not in self._cache:
+            self._cache[key] = sla.cho_factor(mat_fn())
+        return sla.cho_solve(self._cache[key], rhs)
 
     # ----- explicit assembly ------------------------------------------------
     def assemble_D(self):
@@ -134,9 +145,9 @@ class Saddle:
         return self.join(c1, c2, c3)
 
     def _rhat_inv(self, pc, x2):
-        Rh = self.rhat_matrix(pc)
+        key = ("cho_Rhat", pc.rhat, pc.gamma, pc.T, pc.block)
         self.counters["Rhat_inv"] += self.W
-        return [np.linalg.solve(Rh, x2[w]) for w in range(self.W)]
+        return [self._spd_solve(key, lambda: self.rhat_matrix(pc), x2[w]) for w in range(self.W)]
 
     def apply_Pinv(self, pc, v):
         x1, x2, x3 = self.split(v)
@@ -144,7 +155,9 @@ class Saddle:
         c = self.counters
         c2 = self._rhat_inv(pc, x2)
         if pc.shape == "PD":
-            c1 = [np.linalg.solve(RH.dhat(self.Dblk(w), pc.ridge), x1[w]) for w in range(W)]
+            c1 = [self._spd_solve(("cho_D", min(w, 1), pc.ridge),
+                                  lambda w=w: RH.dhat(self.Dblk(w), pc.ridge), x1[w])
+                  for w in range(W)]
             t = LH.solve_T(pc.lhat, self.Ms, x3, pc.k)
             t = [self.Dblk(w) @ t[w] for w in range(W)]
             c3 = LH.solve(pc.lhat, self.Ms, t, pc.k)

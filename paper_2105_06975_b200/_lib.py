@@ -1,0 +1,261 @@
+"""ctypes binding of libwf4dvar.so (include/wf4dvar.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA library; this module converts
+Python/NumPy/torch arguments into the C structs and pointers of the ABI.
+There is no fallback: if the shared library is missing or fails to load,
+importing this module raises.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libwf4dvar.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build it with `python -m paper_2105_06975_b200.build` "
+        "(there is no CPU fallback)")
+_lib = C.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- structs
+M_DENSE, M_HEAT, M_L96 = 0, 1, 2
+PD, PI = 0, 1
+L0, LI, LM, LEXACT = 0, 1, 2, 3
+RDIAG, RBLOCK, RRR, RME, REXACT = 0, 1, 2, 3, 4
+MINRES, GMRES = 0, 1
+STATUS = {0: "OK", 1: "EINVAL", 2: "ENOTSPD", 3: "EINDEF", 4: "ENOCONV", 5: "ECUDA",
+          6: "ENCCL", 7: "ENOMEM"}
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+
+
+class Problem(C.Structure):
+    _fields_ = [("s", C.c_int32), ("p", C.c_int32), ("N", C.c_int32), ("m", C.c_int32),
+                ("B", _dp), ("Q", _dp), ("R", _dp), ("H_idx", _ip), ("model", C.c_int32),
+                ("M_dense", _dp), ("heat_r", C.c_double), ("l96_traj", _dp),
+                ("l96_F", C.c_double), ("l96_dt", C.c_double), ("l96_nsub", C.c_int32)]
+
+
+class Precond(C.Structure):
+    _fields_ = [("shape", C.c_int32), ("lhat", C.c_int32), ("k", C.c_int32), ("rhat", C.c_int32),
+                ("gamma", C.c_double), ("T", C.c_double), ("block", C.c_int32),
+                ("dhat_ridge", C.c_double)]
+
+
+class Dist(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
+                ("stream", C.c_void_p)]
+
+
+class SolveOpts(C.Structure):
+    _fields_ = [("solver", C.c_int32), ("tol", C.c_double), ("maxit", C.c_int32),
+                ("restart", C.c_int32), ("mark_tol", C.c_double), ("check_every", C.c_int32)]
+
+
+class Report(C.Structure):
+    _fields_ = [("iters", _ip), ("relres", _dp), ("converged", C.POINTER(C.c_uint8)),
+                ("history", _dp), ("seconds", C.c_double), ("seconds_to_mark", C.c_double),
+                ("iters_to_mark", C.c_int32), ("n_apply_A", C.c_int64), ("n_apply_P", C.c_int64),
+                ("n_R", C.c_int64), ("n_Rhat_inv", C.c_int64), ("n_D", C.c_int64),
+                ("n_Dhat_inv", C.c_int64), ("n_M", C.c_int64)]
+
+
+class KStat(C.Structure):
+    _fields_ = [("name", C.c_char * 32), ("launches", C.c_int64), ("ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
+
+
+_ctx = C.c_void_p
+_sig = {
+    "wf4dvar_create": (C.c_int, [C.POINTER(Problem), C.POINTER(Precond), C.POINTER(Dist), C.POINTER(_ctx)]),
+    "wf4dvar_set_precond": (C.c_int, [_ctx, C.POINTER(Precond)]),
+    "wf4dvar_destroy": (C.c_int, [_ctx]),
+    "wf4dvar_local_windows": (C.c_int, [_ctx, _ip, _ip]),
+    "wf4dvar_vector_len": (C.c_int, [_ctx, C.POINTER(C.c_int64)]),
+    "wf4dvar_apply_A": (C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
+    "wf4dvar_apply_P": (C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
+    "wf4dvar_apply_AP": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "wf4dvar_apply_AP_host": (C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
+    "wf4dvar_solve": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts), C.POINTER(Report)]),
+    "wf4dvar_solve_host": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts), C.POINTER(Report)]),
+    "wf4dvar_profile_enable": (C.c_int, [_ctx, C.c_int32]),
+    "wf4dvar_profile_read": (C.c_int, [_ctx, C.POINTER(KStat), C.c_int32, _ip]),
+    "wf4dvar_launch_count": (C.c_int64, [_ctx]),
+    "wf4dvar_last_error": (C.c_char_p, [_ctx]),
+    "wf4dvar_version": (C.c_char_p, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_sig.keys())
+
+
+class WF4DVarError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.code = STATUS.get(status, str(status))
+
+
+def version():
+    return _lib.wf4dvar_version().decode()
+
+
+def _ptr(a):
+    """Device/host pointer of a torch tensor or numpy array (float64, contiguous)."""
+    if hasattr(a, "data_ptr"):
+        import torch
+        assert a.dtype == torch.float64 and a.is_contiguous(), "need contiguous float64"
+        return C.c_void_p(a.data_ptr())
+    assert a.dtype == np.float64 and a.flags["C_CONTIGUOUS"], "need contiguous float64"
+    return C.c_void_p(a.ctypes.data)
+
+
+def _np_ptr(a, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+SHAPES = {"PD": PD, "PI": PI}
+LHATS = {"L0": L0, "LI": LI, "LM": LM, "L": LEXACT}
+RHATS = {"diag": RDIAG, "block": RBLOCK, "rr": RRR, "me": RME, "exact": REXACT}
+
+
+def make_precond(shape="PD", lhat="LM", k=4, rhat="exact", gamma=-1.0, T=-1.0, block=0,
+                 ridge=0.0):
+    return Precond(SHAPES[shape], LHATS[lhat], int(k or 1), RHATS[rhat], float(gamma), float(T),
+                   int(block or 0), float(ridge))
+
+
+class Context:
+    """One wf4dvar context on one CUDA device (see include/wf4dvar.h)."""
+
+    def __init__(self, s, p, N, m, B, Q, R, H_idx, model="heat", heat_r=0.25, M_dense=None,
+                 l96_traj=None, l96_F=8.0, l96_dt=0.025, l96_nsub=5, precond=None, device=0,
+                 stream=None):
+        keep = []
+
+        def arr(a, dt=np.float64):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a
+
+        Bh, Qh, Rh = arr(B), arr(Q), arr(R)
+        Hh = arr(H_idx, np.int32)
+        pr = Problem()
+        pr.s, pr.p, pr.N, pr.m = int(s), int(p), int(N), int(m)
+        pr.B, pr.Q, pr.R = _np_ptr(Bh, C.c_double), _np_ptr(Qh, C.c_double), _np_ptr(Rh, C.c_double)
+        pr.H_idx = _np_ptr(Hh, C.c_int32)
+        pr.model = {"dense": M_DENSE, "heat": M_HEAT, "l96": M_L96}[model]
+        pr.heat_r = float(heat_r)
+        if M_dense is not None:
+            pr.M_dense = _np_ptr(arr(M_dense), C.c_double)
+        if l96_traj is not None:
+            pr.l96_traj = _np_ptr(arr(l96_traj), C.c_double)
+        pr.l96_F, pr.l96_dt, pr.l96_nsub = float(l96_F), float(l96_dt), int(l96_nsub)
+        pc = precond if isinstance(precond, Precond) else make_precond(**(precond or {}))
+        d = Dist(0, 1, int(device), C.c_void_p(stream) if stream else None)
+        h = _ctx()
+        st = _lib.wf4dvar_create(C.byref(pr), C.byref(pc), C.byref(d), C.byref(h))
+        if st != 0:
+            raise WF4DVarError(st, _lib.wf4dvar_last_error(None).decode())
+        self._h = h
+        self.s, self.p, self.N, self.m = int(s), int(p), int(N), int(m)
+        self.W = self.N + 1
+        n = C.c_int64()
+        self._check(_lib.wf4dvar_vector_len(h, C.byref(n)))
+        self.n = n.value
+
+    @classmethod
+    def from_problem(cls, prob, precond=None, **kw):
+        return cls(prob.s, prob.p, prob.N, prob.m, prob.B, prob.Q, prob.R, prob.H_idx,
+                   model=prob.model, heat_r=getattr(prob, "heat_r", 0.25),
+                   M_dense=getattr(prob, "M_dense", None), l96_traj=getattr(prob, "traj", None),
+                   l96_F=getattr(prob, "F", 8.0), l96_dt=getattr(prob, "dt", 0.025),
+                   l96_nsub=getattr(prob, "nsub", 5), precond=precond, **kw)
+
+    def _check(self, st):
+        if st != 0:
+            raise WF4DVarError(st, _lib.wf4dvar_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.wf4dvar_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_precond(self, **kw):
+        pc = make_precond(**kw)
+        self._check(_lib.wf4dvar_set_precond(self._h, C.byref(pc)))
+
+    def apply_A(self, x, y):
+        self._check(_lib.wf4dvar_apply_A(self._h, _ptr(x), _ptr(y)))
+
+    def apply_P(self, x, y):
+        self._check(_lib.wf4dvar_apply_P(self._h, _ptr(x), _ptr(y)))
+
+    def apply_AP(self, x, t, y):
+        self._check(_lib.wf4dvar_apply_AP(self._h, _ptr(x), _ptr(t), _ptr(y)))
+
+    def apply_AP_host(self, x_host, y_host):
+        self._check(_lib.wf4dvar_apply_AP_host(self._h, _ptr(x_host), _ptr(y_host)))
+
+    def _solve(self, fn, rhs, x, solver, tol, maxit, restart, mark_tol, check_every, history):
+        opts = SolveOpts({"minres": MINRES, "gmres": GMRES}[solver], float(tol), int(maxit),
+                         int(restart), float(mark_tol), int(check_every))
+        its = np.zeros(self.m, np.int32)
+        rel = np.zeros(self.m, np.float64)
+        conv = np.zeros(self.m, np.uint8)
+        hist = np.zeros((maxit + 1) * self.m, np.float64) if history else None
+        rep = Report()
+        rep.iters, rep.relres = _np_ptr(its, C.c_int32), _np_ptr(rel, C.c_double)
+        rep.converged = _np_ptr(conv, C.c_uint8)
+        if hist is not None:
+            rep.history = _np_ptr(hist, C.c_double)
+        st = fn(self._h, _ptr(rhs), _ptr(x), C.byref(opts), C.byref(rep))
+        if st not in (0, 4):
+            self._check(st)
+        out = dict(status=STATUS[st], iters=its, relres=rel, converged=conv.astype(bool),
+                   seconds=rep.seconds, seconds_to_mark=rep.seconds_to_mark,
+                   iters_to_mark=rep.iters_to_mark, n_apply_A=rep.n_apply_A,
+                   n_apply_P=rep.n_apply_P, n_R=rep.n_R, n_Rhat_inv=rep.n_Rhat_inv, n_D=rep.n_D,
+                   n_Dhat_inv=rep.n_Dhat_inv, n_M=rep.n_M)
+        if hist is not None:
+            out["history"] = hist.reshape(maxit + 1, self.m)
+        return out
+
+    def solve(self, rhs, x, solver="gmres", tol=1e-10, maxit=1000, restart=50, mark_tol=1e-8,
+              check_every=1, history=False):
+        return self._solve(_lib.wf4dvar_solve, rhs, x, solver, tol, maxit, restart, mark_tol,
+                           check_every, history)
+
+    def solve_host(self, rhs, x, solver="gmres", tol=1e-10, maxit=1000, restart=50,
+                   mark_tol=1e-8, check_every=1, history=False):
+        return self._solve(_lib.wf4dvar_solve_host, rhs, x, solver, tol, maxit, restart,
+                           mark_tol, check_every, history)
+
+    def profile_enable(self, on=True):
+        self._check(_lib.wf4dvar_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self):
+        arr = (KStat * 16)()
+        n = C.c_int32()
+        self._check(_lib.wf4dvar_profile_read(self._h, arr, 16, C.byref(n)))
+        return {arr[i].name.decode(): dict(launches=arr[i].launches, ms=arr[i].ms,
+                                           flops=arr[i].flops, bytes=arr[i].bytes)
+                for i in range(n.value)}
+
+    @property
+    def launch_count(self):
+        return int(_lib.wf4dvar_launch_count(self._h))

@@ -1,0 +1,280 @@
+// C ABI entry points (include/wf4dvar.h).  Argument checking, context
+// lifetime, profiling bookkeeping; every compute step is a kernel launched
+// from saddle.cu / model.cu / gemm.cu / trsm.cu / vec.cu / krylov.cu.
+#include <algorithm>
+#include <cstring>
+#include <string>
+
+#include "internal.h"
+
+struct wf4dvar_ctx_s {
+  wf::Ctx c;
+};
+
+static std::string g_create_error;
+
+namespace wf {
+
+void Ctx::prof_begin(int cls, double flops_, double bytes_, cudaEvent_t *ev) {
+  *ev = nullptr;
+  if (!prof.on) return;
+  prof.launches[cls]++;
+  prof.flops[cls] += flops_;
+  prof.bytes[cls] += bytes_;
+  cudaEvent_t a;
+  if (!prof.pool.empty()) { a = prof.pool.back(); prof.pool.pop_back(); }
+  else cudaEventCreate(&a);
+  cudaEventRecord(a, st);
+  *ev = a;
+}
+
+void Ctx::prof_end(int cls, cudaEvent_t a) {
+  if (!a) return;
+  cudaEvent_t b;
+  if (!prof.pool.empty()) { b = prof.pool.back(); prof.pool.pop_back(); }
+  else cudaEventCreate(&b);
+  cudaEventRecord(b, st);
+  prof.pending.push_back({a, b, cls});
+}
+
+}  // namespace wf
+
+using wf::Ctx;
+using wf::Error;
+
+template <class F>
+static wf4dvar_status guarded(wf4dvar_ctx ctx, F &&f) {
+  if (!ctx) return WF4DVAR_EINVAL;
+  try {
+    cudaSetDevice(ctx->c.device);
+    f(ctx->c);
+    ctx->c.last_error.clear();
+    return WF4DVAR_OK;
+  } catch (const Error &e) {
+    ctx->c.last_error = e.msg;
+    return e.st;
+  } catch (const std::exception &e) {
+    ctx->c.last_error = e.what();
+    return WF4DVAR_ECUDA;
+  }
+}
+
+extern "C" {
+
+const char *wf4dvar_version(void) {
+  return "wf4dvar 0.1 (sm_100a, FP64 DMMA + cp.async; arXiv 2105.06975 hot path)";
+}
+
+wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond *pc,
+                              const wf4dvar_dist *dist, wf4dvar_ctx *out) {
+  if (!out) { g_create_error = "out is NULL"; return WF4DVAR_EINVAL; }
+  *out = nullptr;
+  wf4dvar_ctx h = new wf4dvar_ctx_s();
+  Ctx &c = h->c;
+  try {
+    WF_REQUIRE(prob && pc, WF4DVAR_EINVAL, "prob/pc is NULL");
+    const wf4dvar_problem &p = *prob;
+    WF_REQUIRE(p.s >= 1 && p.p >= 1 && p.N >= 0 && p.m >= 1, WF4DVAR_EINVAL, "bad s/p/N/m");
+    WF_REQUIRE(p.p <= p.s, WF4DVAR_EINVAL, "p must be <= s");
+    WF_REQUIRE(p.B && p.Q && p.R && p.H_idx, WF4DVAR_EINVAL, "B/Q/R/H_idx must be non-NULL");
+    for (int j = 0; j < p.p; ++j) {
+      WF_REQUIRE(p.H_idx[j] >= 0 && p.H_idx[j] < p.s, WF4DVAR_EINVAL, "H_idx out of range");
+      if (j) WF_REQUIRE(p.H_idx[j] > p.H_idx[j - 1], WF4DVAR_EINVAL, "H_idx not strictly increasing");
+    }
+    WF_REQUIRE(p.model == WF4DVAR_M_DENSE || p.model == WF4DVAR_M_HEAT || p.model == WF4DVAR_M_L96,
+               WF4DVAR_EINVAL, "unknown model");
+    if (dist) {
+      WF_REQUIRE(dist->world == 1 || dist->world == 0, WF4DVAR_EINVAL,
+                 "world > 1 (time-window sharding) is not in this build; run replicas per rank");
+      c.device = dist->device;
+      c.st = (cudaStream_t)dist->stream;
+    }
+    WF_CUDA(cudaSetDevice(c.device));
+    c.s = p.s; c.p = p.p; c.N = p.N; c.W = p.N + 1; c.m = p.m; c.model = p.model;
+    c.ncol = (int64_t)c.W * c.m;
+    c.n = (int64_t)(2 * c.s + c.p) * c.ncol;
+    c.B = c.alloc<double>((size_t)c.s * c.s);
+    c.Q = c.alloc<double>((size_t)c.s * c.s);
+    c.R = c.alloc<double>((size_t)c.p * c.p);
+    WF_CUDA(cudaMemcpy(c.B, p.B, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(cudaMemcpy(c.Q, p.Q, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(cudaMemcpy(c.R, p.R, (size_t)c.p * c.p * 8, cudaMemcpyHostToDevice));
+    c.H_idx = c.alloc<int>(c.p);
+    c.H_inv = c.alloc<int>(c.s);
+    std::vector<int> inv(c.s, -1);
+    for (int j = 0; j < c.p; ++j) inv[p.H_idx[j]] = j;
+    WF_CUDA(cudaMemcpy(c.H_idx, p.H_idx, c.p * 4, cudaMemcpyHostToDevice));
+    WF_CUDA(cudaMemcpy(c.H_inv, inv.data(), c.s * 4, cudaMemcpyHostToDevice));
+    wf::setup_model(c, p);
+    c.ws_seg = c.alloc<double>((size_t)c.s * c.ncol);
+    // dot partials: gy <= 2*148 blocks x up to 4 dots x m
+    c.dot_part_cap = 2 * 148 * 4 * std::max(c.m, 256) + 4096;
+    c.dot_part = c.alloc<double>(c.dot_part_cap);
+    c.pc = *pc;
+    wf::setup_precond(c);
+    WF_CUDA(cudaStreamSynchronize(c.st));
+  } catch (const Error &e) {
+    g_create_error = e.msg;
+    wf4dvar_destroy(h);
+    return e.st;
+  } catch (const std::exception &e) {
+    g_create_error = e.what();
+    wf4dvar_destroy(h);
+    return WF4DVAR_ECUDA;
+  }
+  *out = h;
+  return WF4DVAR_OK;
+}
+
+wf4dvar_status wf4dvar_set_precond(wf4dvar_ctx ctx, const wf4dvar_precond *pc) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(pc, WF4DVAR_EINVAL, "pc is NULL");
+    WF_CUDA(cudaStreamSynchronize(c.st));
+    c.pc = *pc;
+    wf::setup_precond(c);
+  });
+}
+
+wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
+  if (!ctx) return WF4DVAR_EINVAL;
+  Ctx &c = ctx->c;
+  cudaSetDevice(c.device);
+  if (c.st) cudaStreamSynchronize(c.st); else cudaDeviceSynchronize();
+  for (void *p : c.allocs) cudaFree(p);
+  for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
+  for (auto e : c.prof.pool) cudaEventDestroy(e);
+  if (c.hostbuf) cudaFreeHost(c.hostbuf);
+  delete ctx;
+  return WF4DVAR_OK;
+}
+
+wf4dvar_status wf4dvar_local_windows(wf4dvar_ctx ctx, int32_t *w_begin, int32_t *w_end) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(w_begin && w_end, WF4DVAR_EINVAL, "NULL output");
+    *w_begin = 0;
+    *w_end = c.W;
+  });
+}
+
+wf4dvar_status wf4dvar_vector_len(wf4dvar_ctx ctx, int64_t *n_local) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(n_local, WF4DVAR_EINVAL, "NULL output");
+    *n_local = c.n;
+  });
+}
+
+wf4dvar_status wf4dvar_apply_A(wf4dvar_ctx ctx, const double *x, double *y) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(x && y && x != y, WF4DVAR_EINVAL, "apply_A: bad pointers");
+    wf::apply_A(c, x, y);
+  });
+}
+
+wf4dvar_status wf4dvar_apply_P(wf4dvar_ctx ctx, const double *x, double *y) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(x && y && x != y, WF4DVAR_EINVAL, "apply_P: bad pointers");
+    wf::apply_P(c, x, y);
+  });
+}
+
+wf4dvar_status wf4dvar_apply_AP(wf4dvar_ctx ctx, const double *x, double *t, double *y) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(x && t && y && x != t && t != y && x != y, WF4DVAR_EINVAL, "apply_AP: bad pointers");
+    wf::apply_P(c, x, t);
+    wf::apply_A(c, t, y);
+  });
+}
+
+wf4dvar_status wf4dvar_apply_AP_host(wf4dvar_ctx ctx, const double *x_host, double *y_host) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(x_host && y_host, WF4DVAR_EINVAL, "apply_AP_host: bad pointers");
+    if (!c.dev_io_x) {
+      c.dev_io_x = c.alloc<double>(c.n);
+      c.dev_io_t = c.alloc<double>(c.n);
+      c.dev_io_y = c.alloc<double>(c.n);
+    }
+    WF_CUDA(cudaMemcpyAsync(c.dev_io_x, x_host, c.n * 8, cudaMemcpyHostToDevice, c.st));
+    wf::apply_P(c, c.dev_io_x, c.dev_io_t);
+    wf::apply_A(c, c.dev_io_t, c.dev_io_y);
+    WF_CUDA(cudaMemcpyAsync(y_host, c.dev_io_y, c.n * 8, cudaMemcpyDeviceToHost, c.st));
+    WF_CUDA(cudaStreamSynchronize(c.st));
+  });
+}
+
+wf4dvar_status wf4dvar_solve(wf4dvar_ctx ctx, const double *rhs, double *x,
+                             const wf4dvar_solve_opts *opts, wf4dvar_report *rep) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(rhs && x && opts && rhs != x, WF4DVAR_EINVAL, "solve: bad pointers");
+    wf::solve(c, rhs, x, *opts, rep);
+  });
+}
+
+wf4dvar_status wf4dvar_solve_host(wf4dvar_ctx ctx, const double *rhs_host, double *x_host,
+                                  const wf4dvar_solve_opts *opts, wf4dvar_report *rep) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(rhs_host && x_host && opts, WF4DVAR_EINVAL, "solve_host: bad pointers");
+    if (!c.dev_io_x) {
+      c.dev_io_x = c.alloc<double>(c.n);
+      c.dev_io_t = c.alloc<double>(c.n);
+      c.dev_io_y = c.alloc<double>(c.n);
+    }
+    WF_CUDA(cudaMemcpyAsync(c.dev_io_x, rhs_host, c.n * 8, cudaMemcpyHostToDevice, c.st));
+    wf4dvar_status st = WF4DVAR_OK;
+    try {
+      wf::solve(c, c.dev_io_x, c.dev_io_y, *opts, rep);
+    } catch (const Error &e) {
+      if (e.st != WF4DVAR_ENOCONV) throw;
+      st = e.st;
+      c.last_error = e.msg;
+    }
+    WF_CUDA(cudaMemcpyAsync(x_host, c.dev_io_y, c.n * 8, cudaMemcpyDeviceToHost, c.st));
+    WF_CUDA(cudaStreamSynchronize(c.st));
+    if (st != WF4DVAR_OK) throw Error{st, c.last_error};
+  });
+}
+
+wf4dvar_status wf4dvar_profile_enable(wf4dvar_ctx ctx, int32_t enable) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_CUDA(cudaStreamSynchronize(c.st));
+    for (auto &pe : c.prof.pending) { c.prof.pool.push_back(pe.a); c.prof.pool.push_back(pe.b); }
+    c.prof.pending.clear();
+    for (int k = 0; k < wf::K_NCLASS; ++k) {
+      c.prof.launches[k] = 0; c.prof.flops[k] = 0; c.prof.bytes[k] = 0; c.prof.ms[k] = 0;
+    }
+    c.prof.on = enable != 0;
+  });
+}
+
+wf4dvar_status wf4dvar_profile_read(wf4dvar_ctx ctx, wf4dvar_kstat *out, int32_t max_n,
+                                    int32_t *n_out) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_CUDA(cudaStreamSynchronize(c.st));
+    for (auto &pe : c.prof.pending) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, pe.a, pe.b);
+      c.prof.ms[pe.cls] += ms;
+      c.prof.pool.push_back(pe.a);
+      c.prof.pool.push_back(pe.b);
+    }
+    c.prof.pending.clear();
+    int n = std::min<int>(max_n, wf::K_NCLASS);
+    for (int k = 0; k < n; ++k) {
+      memset(out[k].name, 0, sizeof(out[k].name));
+      strncpy(out[k].name, wf::kClassName[k], sizeof(out[k].name) - 1);
+      out[k].launches = c.prof.launches[k];
+      out[k].ms = c.prof.ms[k];
+      out[k].flops = c.prof.flops[k];
+      out[k].bytes = c.prof.bytes[k];
+    }
+    if (n_out) *n_out = n;
+  });
+}
+
+int64_t wf4dvar_launch_count(wf4dvar_ctx ctx) { return ctx ? ctx->c.launches : -1; }
+
+const char *wf4dvar_last_error(wf4dvar_ctx ctx) {
+  if (!ctx) return g_create_error.c_str();
+  return ctx->c.last_error.c_str();
+}
+
+}  // extern "C"

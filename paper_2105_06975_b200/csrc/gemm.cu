@@ -1,0 +1,141 @@
+// Batched / grouped FP64 GEMM on the DMMA tensor path with a fused epilogue
+//   Y = alpha * A X + beta * Z[zrow]
+// used for every covariance product of the hot path:
+// D x1 (B on window-0 columns, Q on the rest -- two groups in one launch),
+// R x2 + H x3 (the H gather is the zrow epilogue), D c1 inside S_hat^{-1} and
+// P_I, and dense-M_w model products (batched over windows).
+#include "dmma.cuh"
+#include "internal.h"
+
+namespace wf {
+
+struct GemmLaunch {
+  GemmProb p[2];
+  int tiles0;       // tiles of group 0 (per batch)
+  int tm[2], tn[2];
+};
+
+template <class C, bool V16>
+__global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
+  extern __shared__ __align__(16) double smem[];
+  int tile = blockIdx.x;
+  int gi = 0;
+  if (tile >= L.tiles0) { tile -= L.tiles0; gi = 1; }
+  const GemmProb &P = L.p[gi];
+  const int b = blockIdx.z;
+  // grouped raster: 8 M-tiles per group share X panels in L2
+  const int tm_all = L.tm[gi], tn_all = L.tn[gi];
+  constexpr int GM = 8;
+  int group = tile / (GM * tn_all);
+  int first_m = group * GM;
+  int gsize = min(tm_all - first_m, GM);
+  int tm = first_m + (tile % (GM * tn_all)) % gsize;
+  int tn = (tile % (GM * tn_all)) / gsize;
+  const int m0 = tm * C::BM, n0 = tn * C::BN;
+
+  const double *A = P.A + (int64_t)b * P.sA;
+  const double *X = P.X + (int64_t)b * P.sX;
+  double *Y = P.Y + (int64_t)b * P.sY;
+  const double *Z = P.Z ? P.Z + (int64_t)b * P.sZ : nullptr;
+
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  tile_mainloop<C, V16>(smem, acc, A, P.lda, X, P.ldx, m0, n0, 0, P.K, P.M, P.N);
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    int row = m0 + wm * C::WM + i * 8 + g;
+    if (row >= P.M) continue;
+    int zr = Z ? (P.zrow ? P.zrow[row] : row) : 0;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int col = n0 + wn * C::WN + j * 8 + 2 * t + h;
+        if (col >= P.N) continue;
+        double v = P.alpha * acc[i][j][h];
+        if (Z) v += P.beta * Z[(int64_t)zr * P.ldz + col];
+        Y[(int64_t)row * P.ldy + col] = v;
+      }
+    }
+  }
+}
+
+using CfgBig = TileCfg<128, 64, 16, 32, 32, 4>;
+using CfgSmall = TileCfg<64, 32, 16, 32, 16, 4>;
+
+template <class C>
+static int tiles_of(const GemmProb &p, int &tm, int &tn) {
+  tm = (p.M + C::BM - 1) / C::BM;
+  tn = (p.N + C::BN - 1) / C::BN;
+  return tm * tn;
+}
+
+static bool aligned16(const GemmProb &p) {
+  auto al = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
+  return al(p.A) && al(p.X) && (p.lda % 2 == 0) && (p.ldx % 2 == 0) &&
+         (p.sA % 2 == 0) && (p.sX % 2 == 0);
+}
+
+template <class C>
+static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
+  GemmLaunch L{};
+  int tiles = 0;
+  for (int i = 0; i < nprob; ++i) {
+    L.p[i] = probs[i];
+    int t = tiles_of<C>(probs[i], L.tm[i], L.tn[i]);
+    if (i == 0) L.tiles0 = t;
+    tiles += t;
+  }
+  if (nprob == 1) L.tiles0 = tiles;
+  size_t smem = C::SMEM_DOUBLES * sizeof(double);
+  dim3 grid(tiles, 1, batch);
+  if (v16) {
+    static bool attr = false;
+    if (!attr) {
+      WF_CUDA(cudaFuncSetAttribute(k_gemm<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_gemm<C, true><<<grid, C::NT, smem, c.st>>>(L);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      WF_CUDA(cudaFuncSetAttribute(k_gemm<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr = true;
+    }
+    k_gemm<C, false><<<grid, C::NT, smem, c.st>>>(L);
+  }
+  WF_CUDA(cudaGetLastError());
+}
+
+void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flops_hint) {
+  int valid = 0;
+  GemmProb ps[2];
+  for (int i = 0; i < nprob; ++i)
+    if (probs[i].M > 0 && probs[i].N > 0) ps[valid++] = probs[i];
+  if (!valid || batch <= 0) return;
+  double flops = 0, bytes = 0;
+  bool v16 = true;
+  int tm, tn, big_tiles = 0;
+  for (int i = 0; i < valid; ++i) {
+    const GemmProb &p = ps[i];
+    flops += 2.0 * p.M * (double)p.N * p.K * batch;
+    bytes += 8.0 * batch * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N * (p.Z ? 2 : 1));
+    v16 = v16 && aligned16(p);
+    big_tiles += tiles_of<CfgBig>(p, tm, tn);
+  }
+  if (flops_hint >= 0) flops = flops_hint;
+  LaunchScope ls(c, K_GEMM, flops, bytes);
+  if (big_tiles * batch >= 2 * 148) run<CfgBig>(c, ps, valid, batch, v16);
+  else run<CfgSmall>(c, ps, valid, batch, v16);
+  c.launches++;
+}
+
+}  // namespace wf

@@ -1,0 +1,177 @@
+// Internal declarations of the wf4dvar CUDA library (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/wf4dvar.h"
+
+namespace wf {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+  wf4dvar_status st;
+  std::string msg;
+};
+
+#define WF_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      throw ::wf::Error{WF4DVAR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+#define WF_REQUIRE(cond, code, text)                                               \
+  do {                                                                             \
+    if (!(cond)) throw ::wf::Error{code, text};                                    \
+  } while (0)
+
+// ---------------------------------------------------------------- profiling
+enum KClass { K_GEMM = 0, K_TRSM, K_MODEL, K_VEC, K_DOT, K_SCALAR, K_NCLASS };
+static const char *const kClassName[K_NCLASS] = {"gemm_dmma", "trsm_dmma", "model_stencil",
+                                                 "vector", "dot_reduce", "krylov_scalar"};
+
+struct Prof {
+  bool on = false;
+  int64_t launches[K_NCLASS] = {0};
+  double flops[K_NCLASS] = {0};
+  double bytes[K_NCLASS] = {0};
+  double ms[K_NCLASS] = {0};
+  struct Pending { cudaEvent_t a, b; int cls; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> pool;
+};
+
+// ---------------------------------------------------------------- GEMM
+// Y[b] = alpha * A[b] (M x K, row-major, lda) * X[b] (K x N, row-major, ldx)
+//        + beta * Z[b] (rows optionally re-indexed by zrow: Z row zrow[i] feeds Y row i)
+// for batch b (pointer strides sA, sX, sY, sZ in elements).
+struct GemmProb {
+  const double *A; int64_t lda, sA;
+  const double *X; int64_t ldx, sX;
+  double *Y;       int64_t ldy, sY;
+  const double *Z; int64_t ldz, sZ;
+  const int *zrow;
+  int M, N, K;
+  double alpha, beta;
+};
+
+// Triangular solve with a CTA per column panel:
+//   lower (fwd):  G Y = X      (G lower triangular, row-major, ldg)
+//   upper (bwd):  U Y = X      (U upper triangular, row-major, ldg)
+// jstart_blk > 0 restricts the coupling to a block-diagonal factor of block size
+// jstart_blk (R_block): tiles outside a row's block are known zeros and skipped.
+struct TrsmProb {
+  const double *G; int64_t ldg;
+  const double *X; int64_t ldx;
+  double *Y;       int64_t ldy;
+  int n, ncols;   // triangle order, number of right-hand-side columns
+  int blk;        // 0 = dense triangle, else block-diagonal block size
+};
+
+struct Ctx;
+
+void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flops_hint = -1);
+void launch_trsm(Ctx &c, const TrsmProb *probs, int nprob, bool upper);
+
+// ---------------------------------------------------------------- context
+struct Ctx {
+  // problem
+  int s = 0, p = 0, N = 0, W = 0, m = 0;
+  int model = 0;
+  int64_t ncol = 0;   // W*m columns of every segment
+  int64_t n = 0;      // (2s+p)*W*m
+  cudaStream_t st = nullptr;
+  int device = 0;
+  // device data
+  double *B = nullptr, *Q = nullptr, *R = nullptr;
+  int *H_idx = nullptr, *H_inv = nullptr;
+  double *Mdense = nullptr;       // [N][s][s]
+  double *MdenseT = nullptr;      // [N][s][s] transposes
+  double *traj = nullptr;         // [N][s][m]
+  double l96_F = 8, l96_dt = 0.025; int l96_nsub = 5;
+  // heat stencil
+  int heat_D = 0;                 // half width (0 => dense path)
+  double heat_taps[65];           // taps[d + D], d in [-D, D]
+  // preconditioner
+  wf4dvar_precond pc{};
+  double *GB = nullptr, *GBt = nullptr, *GQ = nullptr, *GQt = nullptr;  // chol(D_hat) & transposes
+  double *GR = nullptr, *GRt = nullptr;                                  // chol(R_hat base)
+  double *Rdiag_inv = nullptr;                                           // [p]
+  double *U_me = nullptr, *Kinv_me = nullptr; int r_me = 0;              // Woodbury
+  double gamma_used = 0, T_used = 0;
+  // workspaces (n doubles each unless noted)
+  double *ws_t = nullptr;         // A+P intermediate / P scratch (segment-sized)
+  double *ws_seg = nullptr;       // one s*ncol segment
+  double *ws_lr = nullptr;        // low-rank scratch [r][ncol]
+  double *dot_part = nullptr;     // partial sums
+  int dot_part_cap = 0;
+  double *hostbuf = nullptr;      // pinned
+  double *dev_io_x = nullptr, *dev_io_y = nullptr, *dev_io_t = nullptr;
+  // counters (per-window constituent products, Tables 7.2-7.3 / S5-S7)
+  int64_t n_R = 0, n_Rhat_inv = 0, n_D = 0, n_Dhat_inv = 0, n_M = 0, n_A = 0, n_P = 0;
+  int64_t launches = 0;
+  Prof prof;
+  std::string last_error;
+  std::vector<void *> allocs;
+
+  template <class T> T *alloc(size_t count) {
+    void *ptr = nullptr;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(&ptr, count * sizeof(T));
+    if (e != cudaSuccess) throw Error{WF4DVAR_ENOMEM, "cudaMalloc failed"};
+    allocs.push_back(ptr);
+    return (T *)ptr;
+  }
+  void prof_begin(int cls, double flops, double bytes, cudaEvent_t *ev);
+  void prof_end(int cls, cudaEvent_t ev);
+};
+
+// RAII helper that brackets one launch with profiling events.
+struct LaunchScope {
+  Ctx &c; int cls; cudaEvent_t ev = nullptr;
+  LaunchScope(Ctx &c_, int cls_, double flops, double bytes) : c(c_), cls(cls_) {
+    c.prof_begin(cls, flops, bytes, &ev);
+  }
+  ~LaunchScope() { c.prof_end(cls, ev); }
+};
+
+// ---------------------------------------------------------------- ops
+// out_w = base_w + sign * M_w in_{w-1}      (transpose == false)
+// out_w = base_w + sign * M_{w+1}^T in_{w+1} (transpose == true)
+// for windows w = w_first + t * w_step, t in [0, nw); a window whose source
+// w-1 / w+1 is outside [0, W) gets out_w = base_w.  When add2 != nullptr the
+// kernel also adds add2[row_map[i]] (row_map[i] < 0: nothing) -- used to fuse
+// the H^T scatter of A's third block.  in, base, out are [s][W][m] segments;
+// out may alias base (and in, if the window sets do not overlap).
+void model_step(Ctx &c, bool transpose, double sign, const double *in, const double *base,
+                double *out, int w_first, int w_step, int nw, const double *add2 = nullptr,
+                const int *row_map = nullptr);
+
+// L-hat^{-1} (forward chains) / L-hat^{-T} (backward chains) in place on z.
+void lhat_solve(Ctx &c, bool transpose, double *z);
+
+// vector kernels
+void copy(Ctx &c, double *dst, const double *src, int64_t n);
+void scale_rows(Ctx &c, double *y, const double *x, const double *row_scale, int rows);
+void lowrank_correct(Ctx &c, double *y, const double *x);
+void rhat_inv(Ctx &c, const double *x2, double *y2);
+void dhat_inv(Ctx &c, const double *x1, double *y1);
+
+void apply_A(Ctx &c, const double *x, double *y);
+void apply_P(Ctx &c, const double *x, double *y);
+
+// Krylov
+void solve(Ctx &c, const double *rhs, double *x, const wf4dvar_solve_opts &o, wf4dvar_report *rep);
+
+// batched dots: out[j*m + r] = sum_{f % m == r} a_j[f] * b_j[f], j < nd (<= 4)
+void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_t n,
+          double *out);
+
+void setup_precond(Ctx &c);
+void free_precond(Ctx &c);
+void setup_model(Ctx &c, const wf4dvar_problem &p);
+
+}  // namespace wf

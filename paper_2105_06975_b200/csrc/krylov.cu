@@ -1,0 +1,661 @@
+// Batched Krylov solvers on the device, one independent recurrence per RHS.
+//
+// MINRES (P_D): preconditioned Lanczos + Givens (Elman-Silvester-Wathen)
+// with the true 2-norm residual carried by the A w recurrence (A8):
+// stop when ||r_j||_2 <= tol ||b||_2, x0 = 0.
+// GMRES(m_r) (P_I): right preconditioned, restarted, classical
+// Gram-Schmidt with one full re-orthogonalisation (CGS2), x0 = 0.
+// Per-RHS scalars live on the device; vector kernels read per-RHS coefficients
+// (RHS index = flat index mod m, since every segment is [len][W][m]); a
+// converged RHS gets zero coefficients, so it is frozen without branches on
+// the host.  The host only polls an "active" count every check_every steps.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace wf {
+
+// ------------------------------------------------------------ vector kernels
+// y[f] = a[r] * x1[f] + b[r] * x2[f] + c[r] * x3[f]     (r = f % m)
+__global__ void k_lin3(double *y, const double *x1, const double *a, const double *x2,
+                       const double *b, const double *x3, const double *cc, int64_t n, int m) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  int r = (int)(f % m);
+  double v = a[r] * x1[f];
+  if (x2) v = fma(b[r], x2[f], v);
+  if (x3) v = fma(cc[r], x3[f], v);
+  y[f] = v;
+}
+
+// MINRES fused update:
+//   w_new = kz z - k3 w_prev - k2 w ;  Aw_new = kz q - k3 Aw_prev - k2 Aw
+//   x += cx w_new ; r -= cx Aw_new       (w_new -> w_prev slot, Aw_new -> Aw_prev slot)
+__global__ void k_minres_update(const double *z, const double *q, double *w_prev, const double *w,
+                                double *Aw_prev, const double *Aw, double *x, double *res,
+                                const double *coef, int64_t n, int m) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  int r = (int)(f % m);
+  const double kz = coef[r], k3 = coef[m + r], k2 = coef[2 * m + r], cx = coef[3 * m + r];
+  double wn = kz * z[f] - k3 * w_prev[f] - k2 * w[f];
+  double awn = kz * q[f] - k3 * Aw_prev[f] - k2 * Aw[f];
+  w_prev[f] = wn;
+  Aw_prev[f] = awn;
+  x[f] = fma(cx, wn, x[f]);
+  res[f] = fma(-cx, awn, res[f]);
+}
+
+struct MinresS {
+  double *gamma, *gamma_prev, *eta, *c, *c_prev, *sn, *sn_prev, *delta, *bnorm, *relres;
+  double *gnew, *cnew, *snew;
+  double *cv;     // [3m] coefficients for v_new
+  double *coef;   // [4m] update coefficients
+  double *dots;   // [4m]
+  int *active, *iters, *flags;   // flags[0] = active count, flags[1] = indefinite, flags[2] = mark
+  double *hist;   // optional
+};
+
+__global__ void k_minres_init(MinresS S, int m) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double bb = S.dots[r], zv = S.dots[m + r];
+  double bn = sqrt(bb);
+  S.bnorm[r] = bn;
+  bool act = bn > 0.0;
+  if (act && zv <= 0.0) { S.flags[1] = 1; act = false; }
+  double g = act ? sqrt(zv) : 0.0;
+  S.gamma[r] = g; S.gamma_prev[r] = 1.0; S.eta[r] = g;
+  S.c[r] = 1.0; S.c_prev[r] = 1.0; S.sn[r] = 0.0; S.sn_prev[r] = 0.0;
+  S.active[r] = act ? 1 : 0;
+  S.iters[r] = 0;
+  S.relres[r] = act ? 1.0 : 0.0;
+  if (S.hist) S.hist[r] = S.relres[r];
+}
+
+// after q = A zr:  delta = (q . zr) / gamma^2 ; coefficients of v_new
+__global__ void k_minres_s1(MinresS S, int m) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  double g = S.gamma[r];
+  if (!S.active[r] || g == 0.0) {
+    S.delta[r] = 0; S.cv[r] = 0; S.cv[m + r] = 0; S.cv[2 * m + r] = 0;
+    return;
+  }
+  double d = S.dots[r] / (g * g);
+  S.delta[r] = d;
+  S.cv[r] = 1.0 / g;                   // q_raw / gamma
+  S.cv[m + r] = -d / g;                // - (delta / gamma) v
+  S.cv[2 * m + r] = -g / S.gamma_prev[r];  // - (gamma / gamma_prev) v_prev
+}
+
+// after z_new = P^{-1} v_new: gamma_new, Givens, update coefficients
+__global__ void k_minres_s2(MinresS S, int m) {
+  int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m) return;
+  if (!S.active[r]) {
+    for (int k = 0; k < 4; ++k) S.coef[k * m + r] = 0.0;
+    S.gnew[r] = 0; S.cnew[r] = S.c[r]; S.snew[r] = S.sn[r];
+    return;
+  }
+  double zv = S.dots[r];
+  if (zv < 0.0) { S.flags[1] = 1; zv = 0.0; }
+  double gn = sqrt(zv);
+  double g = S.gamma[r], d = S.delta[r], c = S.c[r], cp = S.c_prev[r], s = S.sn[r],
+         sp = S.sn_prev[r];
+  double a0 = c * d - cp * s * g;
+  double a1 = hypot(a0, gn);
+  double a2 = s * d + cp * c * g;
+  double a3 = sp * g;
+  double cn = a0 / a1, snn = gn / a1;
+  S.gnew[r] = gn; S.cnew[r] = cn; S.snew[r] = snn;
+  S.coef[r] = 1.0 / (g * a1);          // z = zr / gamma, then / a1
+  S.coef[m + r] = a3 / a1;
+  S.coef[2 * m + r] = a2 / a1;
+  S.coef[3 * m + r] = cn * S.eta[r];
+}
+
+// after the update and rr = r . r: shift scalars, convergence, history
+__global__ void k_minres_s3(MinresS S, int m, int j, double tol, double mark_tol) {
+  int cnt = 0, below_mark = 1;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    if (S.active[r]) {
+      double rel = sqrt(S.dots[r]) / S.bnorm[r];
+      S.relres[r] = rel;
+      S.iters[r] = j;
+      S.eta[r] = -S.snew[r] * S.eta[r];
+      S.gamma_prev[r] = S.gamma[r];
+      S.gamma[r] = S.gnew[r];
+      S.c_prev[r] = S.c[r]; S.c[r] = S.cnew[r];
+      S.sn_prev[r] = S.sn[r]; S.sn[r] = S.snew[r];
+      if (rel <= tol || S.gnew[r] == 0.0) S.active[r] = 0;
+    }
+    if (S.hist) S.hist[(int64_t)j * m + r] = S.relres[r];
+    cnt += S.active[r];
+    below_mark &= (S.relres[r] <= mark_tol);
+  }
+  cnt = __syncthreads_count(cnt);
+  below_mark = __syncthreads_and(below_mark);
+  if (threadIdx.x == 0) {
+    S.flags[0] = cnt;
+    if (below_mark && S.flags[2] < 0) S.flags[2] = j;
+  }
+}
+
+static unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+struct EventTimer {
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t get(size_t i) {
+    while (ev.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[i];
+  }
+  ~EventTimer() { for (auto e : ev) cudaEventDestroy(e); }
+};
+
+static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &o,
+                   wf4dvar_report *rep) {
+  const int64_t n = c.n;
+  const int m = c.m;
+  std::vector<double *> bufs;
+  auto vec = [&]() { double *p = nullptr; WF_CUDA(cudaMalloc(&p, n * 8)); bufs.push_back(p); return p; };
+  struct Guard { std::vector<double *> &b; void *s; ~Guard() { for (auto p : b) cudaFree(p); cudaFree(s); } };
+  double *res = vec(), *vp = vec(), *v = vec(), *vn = vec(), *z = vec(), *zn = vec(), *q = vec(),
+         *wp = vec(), *w = vec(), *awp = vec(), *aw = vec();
+  // scalar arena
+  const int NS = 13 + 3 + 4 + 4;
+  void *arena = nullptr;
+  size_t hist_bytes = (rep && rep->history) ? (size_t)(o.maxit + 1) * m * 8 : 0;
+  WF_CUDA(cudaMalloc(&arena, (size_t)NS * m * 8 + 3 * (size_t)m * 4 + 64 + hist_bytes));
+  Guard guard{bufs, arena};
+  double *A = (double *)arena;
+  MinresS S{};
+  S.gamma = A; S.gamma_prev = A + m; S.eta = A + 2 * m; S.c = A + 3 * m; S.c_prev = A + 4 * m;
+  S.sn = A + 5 * m; S.sn_prev = A + 6 * m; S.delta = A + 7 * m; S.bnorm = A + 8 * m;
+  S.relres = A + 9 * m; S.gnew = A + 10 * m; S.cnew = A + 11 * m; S.snew = A + 12 * m;
+  S.cv = A + 13 * m; S.coef = A + 16 * m; S.dots = A + 20 * m;
+  int *I = (int *)(A + NS * m);
+  S.active = I; S.iters = I + m; S.flags = I + 2 * m;
+  S.hist = hist_bytes ? (double *)((char *)(I + 2 * m) + 64) : nullptr;
+  const int h_flags[4] = {0, 0, -1, 0};
+  WF_CUDA(cudaMemcpyAsync(S.flags, h_flags, sizeof(h_flags), cudaMemcpyHostToDevice, c.st));
+
+  EventTimer et;
+  cudaEvent_t e0 = et.get(0);
+  WF_CUDA(cudaEventRecord(e0, c.st));
+  // init: x = 0, r = b, v_prev = 0, v = b, z = P^{-1} v
+  WF_CUDA(cudaMemsetAsync(x, 0, n * 8, c.st));
+  copy(c, res, b, n);
+  WF_CUDA(cudaMemsetAsync(vp, 0, n * 8, c.st));
+  copy(c, v, b, n);
+  WF_CUDA(cudaMemsetAsync(wp, 0, n * 8, c.st));
+  WF_CUDA(cudaMemsetAsync(w, 0, n * 8, c.st));
+  WF_CUDA(cudaMemsetAsync(awp, 0, n * 8, c.st));
+  WF_CUDA(cudaMemsetAsync(aw, 0, n * 8, c.st));
+  apply_P(c, v, z);
+  {
+    const double *a[2] = {b, z}, *bb[2] = {b, v};
+    dots(c, 2, a, bb, n, S.dots);
+  }
+  k_minres_init<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
+  c.launches++;
+  int h[4];
+  int j = 0;
+  bool indef = false;
+  const int ce = std::max(1, o.check_every);
+  std::vector<int> poll_at;
+  int *hpin = nullptr;
+  WF_CUDA(cudaMallocHost(&hpin, 4 * sizeof(int)));
+  for (j = 1; j <= o.maxit; ++j) {
+    apply_A(c, z, q);
+    { const double *a[1] = {q}, *bb[1] = {z}; dots(c, 1, a, bb, n, S.dots); }
+    k_minres_s1<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
+    k_lin3<<<nblk(n, 256), 256, 0, c.st>>>(vn, q, S.cv, v, S.cv + m, vp, S.cv + 2 * m, n, m);
+    c.launches += 2;
+    apply_P(c, vn, zn);
+    { const double *a[1] = {zn}, *bb[1] = {vn}; dots(c, 1, a, bb, n, S.dots); }
+    k_minres_s2<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
+    k_minres_update<<<nblk(n, 256), 256, 0, c.st>>>(z, q, wp, w, awp, aw, x, res, S.coef, n, m);
+    c.launches += 2;
+    { const double *a[1] = {res}, *bb[1] = {res}; dots(c, 1, a, bb, n, S.dots); }
+    k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, j, o.tol, o.mark_tol);
+    c.launches++;
+    WF_CUDA(cudaGetLastError());
+    WF_CUDA(cudaEventRecord(et.get(j), c.st));
+    // rotate: v_prev <- v, v <- v_new, z <- z_new, w_prev <- w, w <- w_new(in wp), same for Aw
+    std::swap(vp, v); std::swap(v, vn);     // vp=old v, v=vn, vn=old vp (free)
+    std::swap(z, zn);
+    std::swap(wp, w);                        // w = new, wp = old w
+    std::swap(awp, aw);
+    if (j % ce == 0 || j == o.maxit) {
+      WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+      WF_CUDA(cudaStreamSynchronize(c.st));
+      memcpy(h, hpin, 3 * sizeof(int));
+      if (h[1]) { indef = true; break; }
+      if (h[0] == 0) break;
+    }
+  }
+  if (j > o.maxit) j = o.maxit;
+  WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  memcpy(h, hpin, 3 * sizeof(int));
+  cudaFreeHost(hpin);
+  if (rep) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, et.get(j));
+    rep->seconds = ms * 1e-3;
+    rep->iters_to_mark = h[2];
+    rep->seconds_to_mark = -1;
+    if (h[2] >= 0) {
+      cudaEventElapsedTime(&ms, e0, et.get(h[2]));
+      rep->seconds_to_mark = ms * 1e-3;
+    }
+    std::vector<int> it(m), act(m);
+    std::vector<double> rel(m);
+    WF_CUDA(cudaMemcpy(it.data(), S.iters, m * 4, cudaMemcpyDeviceToHost));
+    WF_CUDA(cudaMemcpy(act.data(), S.active, m * 4, cudaMemcpyDeviceToHost));
+    WF_CUDA(cudaMemcpy(rel.data(), S.relres, m * 8, cudaMemcpyDeviceToHost));
+    for (int r = 0; r < m; ++r) {
+      if (rep->iters) rep->iters[r] = it[r];
+      if (rep->relres) rep->relres[r] = rel[r];
+      if (rep->converged) rep->converged[r] = (rel[r] <= o.tol) || (!act[r] && rel[r] <= o.tol);
+    }
+    if (rep->history) {
+      std::vector<double> hh((size_t)(o.maxit + 1) * m, std::nan(""));
+      WF_CUDA(cudaMemcpy(hh.data(), S.hist, (size_t)(j + 1) * m * 8, cudaMemcpyDeviceToHost));
+      memcpy(rep->history, hh.data(), hh.size() * 8);
+    }
+  }
+  if (indef) throw Error{WF4DVAR_EINDEF, "MINRES: z^T v < 0 (preconditioner not SPD)"};
+  if (h[0] > 0) throw Error{WF4DVAR_ENOCONV, "MINRES: maxit reached"};
+}
+
+// ------------------------------------------------------------------ GMRES
+// partial dots of w with basis vectors V_i, i in [i0, i0+8) ∩ [0, nv): grid.z = group
+__global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64_t n, int nv,
+                                                          const double *w, int64_t rows, int m,
+                                                          int RB, int64_t rpb, double *part,
+                                                          int jmax) {
+  __shared__ double sm[8][256];
+  const int t = threadIdx.x;
+  const int rl = t % RB, u = t / RB, U = 256 / RB;
+  const int r = blockIdx.x * RB + rl;
+  const int i0 = blockIdx.z * 8;
+  const int64_t row0 = (int64_t)blockIdx.y * rpb, row1 = min(rows, row0 + rpb);
+  double acc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+  if (r < m && u < U) {
+    for (int64_t row = row0 + u; row < row1; row += U) {
+      int64_t f = row * m + r;
+      double wv = w[f];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (i0 + k < nv) acc[k] = fma(V[(int64_t)(i0 + k) * n + f], wv, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 8; ++k) sm[k][t] = acc[k];
+  __syncthreads();
+  if (u == 0 && r < m) {
+    for (int k = 0; k < 8; ++k) {
+      if (i0 + k >= nv) break;
+      double v = 0.0;
+      for (int uu = 0; uu < U; ++uu) v += sm[k][uu * RB + rl];
+      part[((int64_t)blockIdx.y * jmax + i0 + k) * m + r] = v;
+    }
+  }
+}
+
+__global__ void k_multidot_final(const double *part, int nparts, int nv, int jmax, int m,
+                                 double *out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nv * m) return;
+  int i = e / m, r = e % m;
+  double v = 0.0;
+  for (int b = 0; b < nparts; ++b) v += part[((int64_t)b * jmax + i) * m + r];
+  out[e] = v;
+}
+
+// w[f] -= sum_i V_i[f] h[i m + r]; optionally partial sums of w_new^2 per RHS
+__global__ void __launch_bounds__(256) k_multiaxpy(const double *V, int64_t n, int nv, double *w,
+                                                   const double *h, int64_t rows, int m, int RB,
+                                                   int64_t rpb, double *norm_part) {
+  __shared__ double sm[256];
+  const int t = threadIdx.x;
+  const int rl = t % RB, u = t / RB, U = 256 / RB;
+  const int r = blockIdx.x * RB + rl;
+  const int64_t row0 = (int64_t)blockIdx.y * rpb, row1 = min(rows, row0 + rpb);
+  double nn = 0.0;
+  if (r < m && u < U) {
+    for (int64_t row = row0 + u; row < row1; row += U) {
+      int64_t f = row * m + r;
+      double v = w[f];
+      for (int i = 0; i < nv; ++i) {
+        double hi = h[i * m + r];
+        if (hi != 0.0) v = fma(-V[(int64_t)i * n + f], hi, v);
+      }
+      w[f] = v;
+      nn = fma(v, v, nn);
+    }
+  }
+  if (!norm_part) return;
+  sm[t] = nn;
+  __syncthreads();
+  if (u == 0 && r < m) {
+    double s = 0.0;
+    for (int uu = 0; uu < U; ++uu) s += sm[uu * RB + rl];
+    norm_part[(int64_t)blockIdx.y * m + r] = s;
+  }
+}
+
+// y[f] = sum_i V_i[f] coef[i m + r]
+__global__ void k_combine(const double *V, int64_t n, int nv, const double *coef, double *y,
+                          int m) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  int r = (int)(f % m);
+  double v = 0.0;
+  for (int i = 0; i < nv; ++i) {
+    double ci = coef[i * m + r];
+    if (ci != 0.0) v = fma(V[(int64_t)i * n + f], ci, v);
+  }
+  y[f] = v;
+}
+
+struct GmresS {
+  int mr, m;
+  double *H;      // [m][mr+1][mr]  (per RHS, row-major (i, j))
+  double *g;      // [m][mr+1]
+  double *cs, *sn;  // [m][mr]
+  double *bnorm, *relres, *inv;   // [m]
+  double *h1, *h2;  // [(mr+1) m]
+  double *y;        // [(mr+1) m] coefficients (layout i*m + r)
+  double *ww;       // [m] squared norm of w after CGS2
+  int *active, *cyc, *jj, *iters, *flags;  // flags[0] active count, [1] cycle-active count, [2] mark
+  double *hist;
+  int maxit;
+};
+
+// start of a cycle: beta = ||r||; first cycle sets bnorm
+__global__ void k_gmres_cycle_start(GmresS S, int first, double tol) {
+  int cnt = 0;
+  for (int r = threadIdx.x; r < S.m; r += blockDim.x) {
+    double beta = sqrt(S.ww[r]);
+    if (first) {
+      S.bnorm[r] = beta;
+      S.active[r] = beta > 0.0;
+      S.iters[r] = 0;
+      S.relres[r] = beta > 0.0 ? 1.0 : 0.0;
+      if (S.hist) S.hist[r] = S.relres[r];
+    }
+    bool act = S.active[r] && !(beta <= tol * S.bnorm[r]) && S.iters[r] < S.maxit;
+    if (S.active[r] && beta <= tol * S.bnorm[r]) { S.active[r] = 0; S.relres[r] = beta / S.bnorm[r]; }
+    if (S.active[r] && S.iters[r] >= S.maxit) S.active[r] = 0;
+    S.cyc[r] = act ? 1 : 0;
+    S.jj[r] = 0;
+    S.inv[r] = act ? 1.0 / beta : 0.0;
+    double *g = S.g + (int64_t)r * (S.mr + 1);
+    for (int i = 0; i <= S.mr; ++i) g[i] = 0.0;
+    g[0] = act ? beta : 0.0;
+    cnt += act;
+  }
+  cnt = __syncthreads_count(cnt);
+  if (threadIdx.x == 0) { S.flags[1] = cnt; }
+}
+
+// after CGS2 of step j: Hessenberg column, Givens, convergence
+__global__ void k_gmres_step(GmresS S, int j, double tol, double mark_tol, int global_it) {
+  int cnt = 0, below = 1;
+  const int mr = S.mr, m = S.m;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    if (S.cyc[r]) {
+      double *H = S.H + (int64_t)r * (mr + 1) * mr;
+      double *g = S.g + (int64_t)r * (mr + 1);
+      double *cs = S.cs + (int64_t)r * mr, *sn = S.sn + (int64_t)r * mr;
+      for (int i = 0; i <= j; ++i) H[i * mr + j] = S.h1[i * m + r] + S.h2[i * m + r];
+      double hn = sqrt(S.ww[r]);
+      H[(j + 1) * mr + j] = hn;
+      for (int i = 0; i < j; ++i) {
+        double a = H[i * mr + j], b = H[(i + 1) * mr + j];
+        H[i * mr + j] = cs[i] * a + sn[i] * b;
+        H[(i + 1) * mr + j] = -sn[i] * a + cs[i] * b;
+      }
+      double a = H[j * mr + j], b = H[(j + 1) * mr + j];
+      double d = hypot(a, b);
+      double cc = d == 0.0 ? 1.0 : a / d, ss = d == 0.0 ? 0.0 : b / d;
+      cs[j] = cc; sn[j] = ss;
+      H[j * mr + j] = d;
+      H[(j + 1) * mr + j] = 0.0;
+      g[j + 1] = -ss * g[j];
+      g[j] = cc * g[j];
+      S.iters[r] += 1;
+      S.jj[r] = j + 1;
+      double rel = fabs(g[j + 1]) / S.bnorm[r];
+      S.relres[r] = rel;
+      if (S.hist) S.hist[(int64_t)S.iters[r] * m + r] = rel;
+      bool stop = (fabs(g[j + 1]) <= tol * S.bnorm[r]) || hn == 0.0 || S.iters[r] >= S.maxit ||
+                  j + 1 == mr;
+      S.inv[r] = (!stop && hn > 0.0) ? 1.0 / hn : 0.0;
+      if (stop) S.cyc[r] = 0;
+    } else {
+      S.inv[r] = 0.0;
+    }
+    cnt += S.cyc[r];
+    below &= (S.relres[r] <= mark_tol) || !S.active[r];
+  }
+  cnt = __syncthreads_count(cnt);
+  below = __syncthreads_and(below);
+  if (threadIdx.x == 0) {
+    S.flags[1] = cnt;
+    if (below && S.flags[2] < 0) S.flags[2] = global_it;
+  }
+}
+
+// end of cycle: y = H^{-1} g (back substitution over jj[r] columns), coefficient layout i*m+r
+__global__ void k_gmres_backsolve(GmresS S) {
+  const int mr = S.mr, m = S.m;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const double *H = S.H + (int64_t)r * (mr + 1) * mr;
+    const double *g = S.g + (int64_t)r * (mr + 1);
+    int jj = S.jj[r];
+    for (int i = mr; i >= 0; --i) S.y[i * m + r] = 0.0;
+    for (int i = jj - 1; i >= 0; --i) {
+      double v = g[i];
+      for (int k = i + 1; k < jj; ++k) v -= H[i * mr + k] * S.y[k * m + r];
+      S.y[i * m + r] = v / H[i * mr + i];
+    }
+  }
+}
+
+__global__ void k_axpy_sub(double *r_out, const double *b, const double *ax, int64_t n) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < n) r_out[f] = b[f] - ax[f];
+}
+__global__ void k_scale_rhs(double *y, const double *x, const double *s, int64_t n, int m) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < n) y[f] = x[f] * s[f % m];
+}
+__global__ void k_add(double *x, const double *u, int64_t n) {
+  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < n) x[f] += u[f];
+}
+
+static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &o,
+                  wf4dvar_report *rep) {
+  const int64_t n = c.n;
+  const int m = c.m;
+  const int mr = o.restart > 0 ? std::min(o.restart, o.maxit) : o.maxit;
+  const int64_t rows = n / m;
+  const int RB = m < 256 ? m : 256;
+  const int gx = (m + RB - 1) / RB;
+  int gy = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + gx - 1) / gx, (rows + 255) / 256));
+  const int64_t rpb = (rows + gy - 1) / gy;
+  gy = (int)((rows + rpb - 1) / rpb);
+  const int jmax = mr + 1;
+
+  std::vector<void *> mem;
+  auto dmal = [&](size_t bytes) { void *p = nullptr; WF_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 8))); mem.push_back(p); return p; };
+  struct Guard { std::vector<void *> &m; ~Guard() { for (auto p : m) cudaFree(p); } } guard{mem};
+  double *V = (double *)dmal((size_t)(mr + 1) * n * 8);
+  double *u = (double *)dmal(n * 8), *tmp = (double *)dmal(n * 8);
+  double *part = (double *)dmal((size_t)gy * jmax * m * 8);
+  GmresS S{};
+  S.mr = mr; S.m = m; S.maxit = o.maxit;
+  S.H = (double *)dmal((size_t)m * (mr + 1) * mr * 8);
+  S.g = (double *)dmal((size_t)m * (mr + 1) * 8);
+  S.cs = (double *)dmal((size_t)m * mr * 8);
+  S.sn = (double *)dmal((size_t)m * mr * 8);
+  S.bnorm = (double *)dmal(m * 8); S.relres = (double *)dmal(m * 8); S.inv = (double *)dmal(m * 8);
+  S.h1 = (double *)dmal((size_t)jmax * m * 8); S.h2 = (double *)dmal((size_t)jmax * m * 8);
+  S.y = (double *)dmal((size_t)jmax * m * 8);
+  S.ww = (double *)dmal(m * 8);
+  int *I = (int *)dmal((size_t)(5 * m + 4) * 4);
+  S.active = I; S.cyc = I + m; S.jj = I + 2 * m; S.iters = I + 3 * m; S.flags = I + 4 * m;
+  S.hist = (rep && rep->history) ? (double *)dmal((size_t)(o.maxit + 1) * m * 8) : nullptr;
+  const int hf[4] = {0, 0, -1, 0};
+  WF_CUDA(cudaMemcpyAsync(S.flags, hf, sizeof(hf), cudaMemcpyHostToDevice, c.st));
+  int *hpin = nullptr;
+  WF_CUDA(cudaMallocHost(&hpin, 4 * sizeof(int)));
+  struct PinGuard { int *p; ~PinGuard() { cudaFreeHost(p); } } pg{hpin};
+
+  auto multidot = [&](int nv, const double *w, double *out) {
+    LaunchScope ls(c, K_DOT, 2.0 * nv * n, 8.0 * (nv + 1) * n);
+    dim3 grid(gx, gy, (nv + 7) / 8);
+    k_multidot_partial<<<grid, 256, 0, c.st>>>(V, n, nv, w, rows, m, RB, rpb, part, jmax);
+    k_multidot_final<<<nblk((int64_t)nv * m, 128), 128, 0, c.st>>>(part, gy, nv, jmax, m, out);
+    c.launches += 2;
+  };
+  auto multiaxpy = [&](int nv, double *w, const double *h, bool norm) {
+    LaunchScope ls(c, K_VEC, 2.0 * nv * n, 8.0 * (nv + 2) * n);
+    dim3 grid(gx, gy);
+    k_multiaxpy<<<grid, 256, 0, c.st>>>(V, n, nv, w, h, rows, m, RB, rpb, norm ? part : nullptr);
+    c.launches++;
+    if (norm) {
+      k_multidot_final<<<nblk(m, 128), 128, 0, c.st>>>(part, gy, 1, 1, m, S.ww);
+      c.launches++;
+    }
+  };
+  auto norm2 = [&](const double *v) {
+    const double *a[1] = {v};
+    dots(c, 1, a, a, n, S.ww);
+  };
+
+  EventTimer et;
+  WF_CUDA(cudaEventRecord(et.get(0), c.st));
+  WF_CUDA(cudaMemsetAsync(x, 0, n * 8, c.st));
+  int global_it = 0;
+  bool first = true;
+  std::vector<int> ev_iter;  // event index -> iteration
+  while (true) {
+    // residual
+    if (first) {
+      copy(c, V, b, n);
+    } else {
+      apply_A(c, x, tmp);
+      k_axpy_sub<<<nblk(n, 256), 256, 0, c.st>>>(V, b, tmp, n);
+      c.launches++;
+    }
+    norm2(V);
+    k_gmres_cycle_start<<<1, 1024, 0, c.st>>>(S, first ? 1 : 0, o.tol);
+    k_scale_rhs<<<nblk(n, 256), 256, 0, c.st>>>(V, V, S.inv, n, m);
+    c.launches += 2;
+    first = false;
+    WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    WF_CUDA(cudaStreamSynchronize(c.st));
+    if (hpin[1] == 0 || global_it >= o.maxit) break;
+    int j = 0;
+    for (j = 0; j < mr; ++j) {
+      double *Vj = V + (int64_t)j * n, *w = V + (int64_t)(j + 1) * n;
+      apply_P(c, Vj, u);
+      apply_A(c, u, w);
+      multidot(j + 1, w, S.h1);
+      multiaxpy(j + 1, w, S.h1, false);
+      multidot(j + 1, w, S.h2);
+      multiaxpy(j + 1, w, S.h2, true);
+      ++global_it;
+      k_gmres_step<<<1, 1024, 0, c.st>>>(S, j, o.tol, o.mark_tol, global_it);
+      k_scale_rhs<<<nblk(n, 256), 256, 0, c.st>>>(w, w, S.inv, n, m);
+      c.launches += 2;
+      WF_CUDA(cudaGetLastError());
+      WF_CUDA(cudaEventRecord(et.get(global_it), c.st));
+      // lagged poll: read the cycle-active count of the previous step
+      if ((j + 1) % std::max(1, o.check_every) == 0) {
+        WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+        WF_CUDA(cudaStreamSynchronize(c.st));
+        if (hpin[1] == 0) { ++j; break; }
+      }
+      if (global_it >= o.maxit) { ++j; break; }
+    }
+    // x += P^{-1} (V y)
+    k_gmres_backsolve<<<1, 1024, 0, c.st>>>(S);
+    k_combine<<<nblk(n, 256), 256, 0, c.st>>>(V, n, std::min(j, mr), S.y, tmp, m);
+    c.launches += 2;
+    apply_P(c, tmp, u);
+    k_add<<<nblk(n, 256), 256, 0, c.st>>>(x, u, n);
+    c.launches++;
+  }
+  WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  int active_left = 0;
+  std::vector<int> act(m), it(m);
+  std::vector<double> rel(m);
+  WF_CUDA(cudaMemcpy(act.data(), S.active, m * 4, cudaMemcpyDeviceToHost));
+  WF_CUDA(cudaMemcpy(it.data(), S.iters, m * 4, cudaMemcpyDeviceToHost));
+  WF_CUDA(cudaMemcpy(rel.data(), S.relres, m * 8, cudaMemcpyDeviceToHost));
+  for (int r = 0; r < m; ++r) active_left += act[r];
+  if (rep) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, et.get(0), et.get(global_it));
+    rep->seconds = ms * 1e-3;
+    rep->iters_to_mark = hpin[2];
+    rep->seconds_to_mark = -1;
+    if (hpin[2] >= 0) {
+      cudaEventElapsedTime(&ms, et.get(0), et.get(hpin[2]));
+      rep->seconds_to_mark = ms * 1e-3;
+    }
+    for (int r = 0; r < m; ++r) {
+      if (rep->iters) rep->iters[r] = it[r];
+      if (rep->relres) rep->relres[r] = rel[r];
+      if (rep->converged) rep->converged[r] = !act[r] && rel[r] <= o.tol;
+    }
+    if (rep->history) {
+      std::vector<double> hh((size_t)(o.maxit + 1) * m);
+      WF_CUDA(cudaMemcpy(hh.data(), S.hist, hh.size() * 8, cudaMemcpyDeviceToHost));
+      for (int r = 0; r < m; ++r)
+        for (size_t i = (size_t)it[r] + 1; i <= (size_t)o.maxit; ++i) hh[i * m + r] = std::nan("");
+      memcpy(rep->history, hh.data(), hh.size() * 8);
+    }
+  }
+  if (active_left > 0) throw Error{WF4DVAR_ENOCONV, "GMRES: maxit reached"};
+}
+
+void solve(Ctx &c, const double *rhs, double *x, const wf4dvar_solve_opts &o, wf4dvar_report *rep) {
+  WF_REQUIRE(o.maxit >= 1 && o.tol > 0, WF4DVAR_EINVAL, "solve: need maxit >= 1 and tol > 0");
+  int64_t a0 = c.n_A, p0 = c.n_P, R0 = c.n_R, Ri0 = c.n_Rhat_inv, D0 = c.n_D, Di0 = c.n_Dhat_inv,
+          M0 = c.n_M;
+  auto fill = [&]() {
+    if (!rep) return;
+    rep->n_apply_A = c.n_A - a0; rep->n_apply_P = c.n_P - p0; rep->n_R = c.n_R - R0;
+    rep->n_Rhat_inv = c.n_Rhat_inv - Ri0; rep->n_D = c.n_D - D0; rep->n_Dhat_inv = c.n_Dhat_inv - Di0;
+    rep->n_M = c.n_M - M0;
+  };
+  try {
+    if (o.solver == WF4DVAR_MINRES) {
+      WF_REQUIRE(c.pc.shape == WF4DVAR_PD, WF4DVAR_EINVAL, "MINRES needs the SPD preconditioner P_D");
+      minres(c, rhs, x, o, rep);
+    } else {
+      gmres(c, rhs, x, o, rep);
+    }
+  } catch (...) { fill(); throw; }
+  fill();
+}
+
+}  // namespace wf

@@ -1,0 +1,263 @@
+// Model term kernels: M_w / M_w^T products fused into L, L^T (Eq. 2.3,
+// P:L108-117), the chain substitutions of L_M(k)^{-1} (Def. 4.1, Lemma 4.2,
+// P:L255-276), the L_I prefix scan and the H^T scatter of A's
+// third block.
+//
+// Heat (BJ.c0-c4): M = (I - r Lap)^{-1} is a symmetric circulant whose row
+// decays like rho^|d|, rho = (1+2r-sqrt(1+4r))/(2r) (0.1716 at r = 0.25).  It
+// is applied as its exact circulant stencil truncated at |d| <= D where the
+// dropped tail is < 1e-17 relative (D = 22 at r = 0.25): a coalesced,
+// register-windowed 1-D stencil along the state index, one thread per
+// (window, RHS) column -- FP64-ALU/HBM balanced, no tensor cores (not a GEMM).
+#include <cmath>
+
+#include "internal.h"
+
+namespace wf {
+
+struct Taps { double t[65]; };
+
+// out_w = base_w + sign * sum_d taps[d] in_{w_src}[(i+d) mod s]   (+ add2[row_map[i]])
+template <int D, int TI>
+__global__ void __launch_bounds__(128) k_heat_step(double *out, const double *base,
+                                                   const double *in, const double *add2,
+                                                   const int *row_map, const Taps taps, double sign,
+                                                   int s, int W, int m, int w_first, int w_step,
+                                                   int nw, int dir) {
+  const int64_t ld = (int64_t)W * m;
+  const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cc >= nw * m) return;
+  const int tt = cc / m, r = cc - tt * m;
+  const int w = w_first + tt * w_step;
+  const int ws = w + dir;   // dir = -1 (M_w in_{w-1}) or +1 (M_{w+1}^T in_{w+1})
+  const bool has = (ws >= 0 && ws < W);
+  const int64_t col = (int64_t)w * m + r, cols = (int64_t)ws * m + r;
+  const int i0 = blockIdx.y * TI;
+  double v[TI + 2 * D];
+  if (has) {
+#pragma unroll
+    for (int j = 0; j < TI + 2 * D; ++j) {
+      int row = i0 - D + j;
+      row = row < 0 ? row + s : (row >= s ? row - s : row);
+      row = row < 0 ? row + s : (row >= s ? row - s : row);
+      v[j] = __ldg(in + row * ld + cols);
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < TI; ++o) {
+    const int i = i0 + o;
+    if (i < s) {
+      double val = base[i * ld + col];
+      if (has) {
+        double acc = 0.0;
+#pragma unroll
+        for (int d = 0; d <= 2 * D; ++d) acc = fma(taps.t[d], v[o + d], acc);
+        val = fma(sign, acc, val);
+      }
+      if (add2) {
+        int j = row_map[i];
+        if (j >= 0) val += add2[(int64_t)j * ld + col];
+      }
+      out[i * ld + col] = val;
+    }
+  }
+}
+
+// z_w += z_{w-1} (forward, w ascending) or z_w += z_{w+1} (backward): L_I^{-1} / L_I^{-T}
+__global__ void k_window_scan(double *z, int rows, int W, int m, int dir) {
+  const int64_t ld = (int64_t)W * m;
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)rows * m) return;
+  int64_t i = e / m, r = e % m;
+  double *p = z + i * ld + r;
+  if (dir > 0) {
+    double acc = p[0];
+    for (int w = 1; w < W; ++w) { acc += p[(int64_t)w * m]; p[(int64_t)w * m] = acc; }
+  } else {
+    double acc = p[(int64_t)(W - 1) * m];
+    for (int w = W - 2; w >= 0; --w) { acc += p[(int64_t)w * m]; p[(int64_t)w * m] = acc; }
+  }
+}
+
+// out[H_idx[j]][col] += add2[j][col] for every column (dense-model path of H^T)
+__global__ void k_scatter_add(double *out, const double *add2, const int *H_idx, int p,
+                              int64_t ld) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)p * ld) return;
+  int64_t j = e / ld, c = e % ld;
+  out[(int64_t)H_idx[j] * ld + c] += add2[e];
+}
+
+template <int D>
+static void heat_launch(Ctx &c, bool transpose, double sign, const double *in, const double *base,
+                        double *out, int w_first, int w_step, int nw, const double *add2,
+                        const int *row_map) {
+  constexpr int TI = 32;
+  Taps taps;
+  for (int d = 0; d <= 2 * D; ++d) taps.t[d] = c.heat_taps[d - D + c.heat_D];
+  int cols = nw * c.m;
+  dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
+  k_heat_step<D, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, taps, sign, c.s, c.W,
+                                              c.m, w_first, w_step, nw, transpose ? 1 : -1);
+  WF_CUDA(cudaGetLastError());
+}
+
+void model_step(Ctx &c, bool transpose, double sign, const double *in, const double *base,
+                double *out, int w_first, int w_step, int nw, const double *add2,
+                const int *row_map) {
+  if (nw <= 0) return;
+  const int s = c.s, m = c.m;
+  const int64_t ld = c.ncol;
+  if (c.model == WF4DVAR_M_HEAT && c.heat_D > 0) {
+    double elems = (double)nw * s * m;
+    LaunchScope ls(c, K_MODEL, elems * 2.0 * (2 * c.heat_D + 1), elems * 8.0 * 3);
+    switch (c.heat_D) {
+      case 8: heat_launch<8>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 16: heat_launch<16>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 24: heat_launch<24>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      default: heat_launch<32>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+    }
+    c.launches++;
+    return;
+  }
+  if (c.model == WF4DVAR_M_DENSE || c.model == WF4DVAR_M_HEAT) {
+    // Windows without a source (w = 0 forward, w = N transposed) are a copy of base.
+    int t0 = 0, t1 = nw;
+    auto src_ok = [&](int t) {
+      int w = w_first + t * w_step, ws = w + (transpose ? 1 : -1);
+      return ws >= 0 && ws < c.W;
+    };
+    for (int t = 0; t < nw; ++t) {
+      if (!src_ok(t)) {
+        int w = w_first + t * w_step;
+        if (out != base)
+          WF_CUDA(cudaMemcpy2DAsync(out + (int64_t)w * m, ld * 8, base + (int64_t)w * m, ld * 8,
+                                    m * 8, s, cudaMemcpyDeviceToDevice, c.st));
+      }
+    }
+    while (t0 < t1 && !src_ok(t0)) ++t0;
+    while (t1 > t0 && !src_ok(t1 - 1)) --t1;
+    if (t1 > t0) {
+      int wf0 = w_first + t0 * w_step;
+      GemmProb g{};
+      // M_w is stored at Mdense[w-1]; M_{w+1}^T at MdenseT[w]
+      g.A = transpose ? c.MdenseT + (int64_t)wf0 * s * s : c.Mdense + (int64_t)(wf0 - 1) * s * s;
+      g.lda = s; g.sA = (int64_t)w_step * s * s;
+      g.X = in + (int64_t)(wf0 + (transpose ? 1 : -1)) * m; g.ldx = ld; g.sX = (int64_t)w_step * m;
+      g.Y = out + (int64_t)wf0 * m; g.ldy = ld; g.sY = (int64_t)w_step * m;
+      g.Z = base + (int64_t)wf0 * m; g.ldz = ld; g.sZ = (int64_t)w_step * m;
+      g.zrow = nullptr;
+      g.M = s; g.N = m; g.K = s;
+      g.alpha = sign; g.beta = 1.0;
+      launch_gemm(c, &g, 1, t1 - t0);
+    }
+    for (int t = 0; t < nw; ++t) {
+      // nothing: all windows handled
+    }
+    if (add2) {
+      // H^T scatter on every target window (only used with w_step == 1 over all windows)
+      LaunchScope ls(c, K_VEC, 0, (double)c.p * ld * 16);
+      int64_t tot = (int64_t)c.p * ld;
+      k_scatter_add<<<(unsigned)((tot + 255) / 256), 256, 0, c.st>>>(out, add2, c.H_idx, c.p, ld);
+      WF_CUDA(cudaGetLastError());
+      c.launches++;
+    }
+    return;
+  }
+  throw Error{WF4DVAR_EINVAL, "model not supported by model_step"};
+}
+
+void lhat_solve(Ctx &c, bool transpose, double *z) {
+  const int W = c.W, N = c.N;
+  switch (c.pc.lhat) {
+    case WF4DVAR_L0:
+      return;
+    case WF4DVAR_LI: {
+      LaunchScope ls(c, K_MODEL, 0, (double)c.s * c.ncol * 16);
+      int64_t tot = (int64_t)c.s * c.m;
+      k_window_scan<<<(unsigned)((tot + 127) / 128), 128, 0, c.st>>>(z, c.s, W, c.m,
+                                                                     transpose ? -1 : 1);
+      WF_CUDA(cudaGetLastError());
+      c.launches++;
+      return;
+    }
+    default: break;
+  }
+  const int k = (c.pc.lhat == WF4DVAR_LEXACT) ? W : c.pc.k;
+  if (k <= 1) return;
+  if (!transpose) {
+    // chain step j: z_w = r_w + M_w z_{w-1} for w = ck + j (Lemma 4.2 substitution)
+    for (int j = 1; j < k && j <= N; ++j) {
+      int nw = (N - j) / k + 1;
+      model_step(c, false, 1.0, z, z, z, j, k, nw);
+    }
+  } else {
+    // backward: z_w = r_w + M_{w+1}^T z_{w+1} while w+1 stays in w's chain
+    const int nfull = W / k, last_len = W - nfull * k;
+    for (int j = 1; j < k; ++j) {
+      // full chains: w = ck + (k-1-j)
+      if (nfull > 0) model_step(c, true, 1.0, z, z, z, k - 1 - j, k, nfull);
+      // ragged last chain [nfull*k, W): w = W-1-j
+      if (last_len > 0 && j < last_len) model_step(c, true, 1.0, z, z, z, W - 1 - j, 1, 1);
+    }
+  }
+}
+
+// --------------------------------------------------------------- setup
+// Exact periodic row of M = (I - r Lap)^{-1}:
+//   c_d = (rho^d + rho^(s-d)) / ((1 - rho^s) sqrt(1 + 4r)),  d = 0..s-1.
+static void heat_row(int s, double r, std::vector<double> &row) {
+  const double sq = std::sqrt(1.0 + 4.0 * r);
+  const double rho = (1.0 + 2.0 * r - sq) / (2.0 * r);
+  const double rs = std::pow(rho, s);
+  row.assign(s, 0.0);
+  for (int d = 0; d < s; ++d)
+    row[d] = (std::pow(rho, d) + std::pow(rho, s - d)) / ((1.0 - rs) * sq);
+}
+
+void setup_model(Ctx &c, const wf4dvar_problem &p) {
+  const int s = c.s, N = c.N;
+  if (c.model == WF4DVAR_M_HEAT) {
+    WF_REQUIRE(p.heat_r > 0, WF4DVAR_EINVAL, "heat_r must be > 0");
+    std::vector<double> row;
+    heat_row(s, p.heat_r, row);
+    const double rho = (1.0 + 2.0 * p.heat_r - std::sqrt(1.0 + 4.0 * p.heat_r)) / (2.0 * p.heat_r);
+    // smallest D with the dropped tail 2 rho^(D+1)/(1-rho) below 1e-17 * c_0
+    int Dneed = 1;
+    while (2.0 * std::pow(rho, Dneed + 1) / (1.0 - rho) > 1e-17 * row[0] && Dneed < 1000) ++Dneed;
+    int D = Dneed <= 8 ? 8 : Dneed <= 16 ? 16 : Dneed <= 24 ? 24 : Dneed <= 32 ? 32 : 0;
+    if (D > 0 && s >= 2 * D + 1) {
+      c.heat_D = D;
+      for (int d = -D; d <= D; ++d) c.heat_taps[d + D] = row[((d % s) + s) % s];
+    } else {
+      // small grid or slowly decaying row: materialise the exact circulant M and use
+      // the dense (DMMA GEMM) path
+      c.heat_D = 0;
+      std::vector<double> M((size_t)s * s);
+      for (int i = 0; i < s; ++i)
+        for (int j = 0; j < s; ++j) M[(size_t)i * s + j] = row[((j - i) % s + s) % s];
+      c.Mdense = c.alloc<double>((size_t)N * s * s);
+      c.MdenseT = c.alloc<double>((size_t)N * s * s);
+      for (int w = 0; w < N; ++w) {
+        WF_CUDA(cudaMemcpy(c.Mdense + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
+        WF_CUDA(cudaMemcpy(c.MdenseT + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
+      }
+    }
+  } else if (c.model == WF4DVAR_M_DENSE) {
+    WF_REQUIRE(p.M_dense != nullptr, WF4DVAR_EINVAL, "M_dense is NULL");
+    c.Mdense = c.alloc<double>((size_t)N * s * s);
+    c.MdenseT = c.alloc<double>((size_t)N * s * s);
+    std::vector<double> Tm((size_t)s * s);
+    for (int w = 0; w < N; ++w) {
+      const double *Mw = p.M_dense + (size_t)w * s * s;
+      for (int i = 0; i < s; ++i)
+        for (int j = 0; j < s; ++j) Tm[(size_t)j * s + i] = Mw[(size_t)i * s + j];
+      WF_CUDA(cudaMemcpy(c.Mdense + (size_t)w * s * s, Mw, (size_t)s * s * 8, cudaMemcpyHostToDevice));
+      WF_CUDA(cudaMemcpy(c.MdenseT + (size_t)w * s * s, Tm.data(), Tm.size() * 8, cudaMemcpyHostToDevice));
+    }
+  } else {
+    throw Error{WF4DVAR_EINVAL, "model kind not supported in this build"};
+  }
+}
+
+}  // namespace wf

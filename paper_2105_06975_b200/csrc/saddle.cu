@@ -1,0 +1,345 @@
+// Matrix-free saddle operator and preconditioners (Section 6.2).
+//
+//   apply_A   c1 = D x1 + L x3       one model pass + grouped GEMM (B | Q)
+//                            c2 = R x2 + H x3       GEMM with the H gather fused in the epilogue
+//                            c3 = L^T x1 + H^T x2   one model pass with the H^T scatter fused
+//   apply_P   P_D: (D_hat^{-1} x1, R_hat^{-1} x2, L_hat^{-1} D L_hat^{-T} x3)
+//             P_I: c1 = L_hat^{-T} x3, c2 = R_hat^{-1} x2,
+//                               c3 = L_hat^{-1}(x1 - D c1)
+// Segments are [len][W][m]; a covariance product over all windows is one GEMM of
+// the len x len block with the len x (W m) segment.  Per-window constituent
+// products are counted exactly as the paper's matvec tables (7.2, 7.3, S5-S7).
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "internal.h"
+
+namespace wf {
+
+static GemmProb gp(const double *A, int64_t lda, const double *X, int64_t ldx, double *Y,
+                   int64_t ldy, const double *Z, int64_t ldz, int M, int N, int K, double alpha,
+                   double beta, const int *zrow = nullptr) {
+  GemmProb g{};
+  g.A = A; g.lda = lda; g.X = X; g.ldx = ldx; g.Y = Y; g.ldy = ldy; g.Z = Z; g.ldz = ldz;
+  g.zrow = zrow; g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = beta;
+  return g;
+}
+
+// Y = alpha * D X + beta * Z over an s x (W m) segment: B on window-0 columns, Q elsewhere.
+static void d_product(Ctx &c, const double *X, double *Y, const double *Z, double alpha,
+                      double beta) {
+  const int s = c.s, m = c.m;
+  const int64_t ld = c.ncol;
+  GemmProb g[2];
+  g[0] = gp(c.B, s, X, ld, Y, ld, Z, ld, s, m, s, alpha, beta);
+  g[1] = gp(c.Q, s, X + m, ld, Y + m, ld, Z ? Z + m : nullptr, ld, s, (int)(ld - m), s, alpha, beta);
+  launch_gemm(c, g, c.W > 1 ? 2 : 1, 1);
+  c.n_D += c.W;
+}
+
+void dhat_inv(Ctx &c, const double *x1, double *y1) {
+  const int s = c.s, m = c.m;
+  const int64_t ld = c.ncol;
+  TrsmProb f[2], b[2];
+  f[0] = TrsmProb{c.GB, s, x1, ld, y1, ld, s, m, 0};
+  f[1] = TrsmProb{c.GQ, s, x1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
+  b[0] = TrsmProb{c.GBt, s, y1, ld, y1, ld, s, m, 0};
+  b[1] = TrsmProb{c.GQt, s, y1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
+  int np = c.W > 1 ? 2 : 1;
+  launch_trsm(c, f, np, false);
+  launch_trsm(c, b, np, true);
+  c.n_Dhat_inv += c.W;
+}
+
+void rhat_inv(Ctx &c, const double *x2, double *y2) {
+  const int p = c.p;
+  const int64_t ld = c.ncol;
+  if (c.pc.rhat == WF4DVAR_RDIAG) {
+    scale_rows(c, y2, x2, c.Rdiag_inv, p);
+    return;   // R_diag applications are not counted in the paper's tables
+  }
+  int blk = (c.pc.rhat == WF4DVAR_RBLOCK) ? c.pc.block : 0;
+  TrsmProb f{c.GR, p, x2, ld, y2, ld, p, (int)ld, blk};
+  TrsmProb b{c.GRt, p, y2, ld, y2, ld, p, (int)ld, blk};
+  launch_trsm(c, &f, 1, false);
+  launch_trsm(c, &b, 1, true);
+  if (c.pc.rhat == WF4DVAR_RME) lowrank_correct(c, y2, x2);
+  c.n_Rhat_inv += c.W;
+}
+
+static int n_model_blocks(const Ctx &c) {
+  switch (c.pc.lhat) {
+    case WF4DVAR_L0: case WF4DVAR_LI: return 0;
+    case WF4DVAR_LEXACT: return c.N;
+    default: return c.N - c.N / c.pc.k;
+  }
+}
+
+void apply_A(Ctx &c, const double *x, double *y) {
+  const int s = c.s, p = c.p;
+  const int64_t ld = c.ncol;
+  const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
+  double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  // c1 = L x3 + D x1
+  model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
+  d_product(c, x1, y1, y1, 1.0, 1.0);
+  // c2 = R x2 + H x3 (gather in the epilogue)
+  GemmProb g = gp(c.R, p, x2, ld, y2, ld, x3, ld, p, (int)ld, p, 1.0, 1.0, c.H_idx);
+  launch_gemm(c, &g, 1, 1);
+  // c3 = L^T x1 + H^T x2
+  model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W, x2, c.H_inv);
+  c.n_R += c.W;
+  c.n_M += 2 * c.N;
+  c.n_A++;
+}
+
+void apply_P(Ctx &c, const double *x, double *y) {
+  const int s = c.s, p = c.p;
+  const int64_t ld = c.ncol;
+  const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
+  double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  if (c.pc.shape == WF4DVAR_PD) {
+    dhat_inv(c, x1, y1);
+    rhat_inv(c, x2, y2);
+    double *t = c.ws_seg;
+    copy(c, t, x3, (int64_t)s * ld);
+    lhat_solve(c, true, t);               // L_hat^{-T} x3
+    d_product(c, t, y3, nullptr, 1.0, 0.0);  // D (exact D)
+    lhat_solve(c, false, y3);             // L_hat^{-1}
+  } else {
+    copy(c, y1, x3, (int64_t)s * ld);
+    lhat_solve(c, true, y1);              // c1 = L_hat^{-T} x3
+    rhat_inv(c, x2, y2);                  // c2
+    d_product(c, y1, y3, x1, -1.0, 1.0);  // x1 - D c1
+    lhat_solve(c, false, y3);             // c3
+  }
+  c.n_M += 2 * n_model_blocks(c);
+  c.n_P++;
+}
+
+// ------------------------------------------------------------------ setup
+__global__ void k_extract_chol(const double *P, double *G, double *U, int n) {
+  // P: cuSOLVER column-major lower factor L (upper part untouched).
+  // G[i][j] = L[i][j] (row-major lower), U[i][j] = L[j][i] (row-major upper).
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * n) return;
+  int i = (int)(e / n), j = (int)(e % n);
+  double lij = (j <= i) ? P[(int64_t)j * n + i] : 0.0;   // L[i][j]
+  double lji = (i <= j) ? P[(int64_t)i * n + j] : 0.0;   // L[j][i]
+  G[e] = lij;
+  U[e] = lji;
+}
+
+struct Solver {
+  cusolverDnHandle_t h = nullptr;
+  Solver(cudaStream_t st) {
+    if (cusolverDnCreate(&h) != CUSOLVER_STATUS_SUCCESS) throw Error{WF4DVAR_ECUDA, "cusolverDnCreate"};
+    cusolverDnSetStream(h, st);
+  }
+  ~Solver() { if (h) cusolverDnDestroy(h); }
+};
+
+// Cholesky of the symmetric host-or-device matrix A (n x n, device) -> G (lower), U (upper).
+static void chol(Ctx &c, Solver &sv, const double *Adev, int n, double *G, double *U,
+                 const char *name) {
+  double *work_mat = nullptr, *work = nullptr;
+  int *info = nullptr;
+  WF_CUDA(cudaMalloc(&work_mat, (size_t)n * n * 8));
+  WF_CUDA(cudaMemcpyAsync(work_mat, Adev, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, c.st));
+  int lwork = 0;
+  cusolverDnDpotrf_bufferSize(sv.h, CUBLAS_FILL_MODE_LOWER, n, work_mat, n, &lwork);
+  WF_CUDA(cudaMalloc(&work, (size_t)std::max(lwork, 1) * 8));
+  WF_CUDA(cudaMalloc(&info, sizeof(int)));
+  cusolverStatus_t st = cusolverDnDpotrf(sv.h, CUBLAS_FILL_MODE_LOWER, n, work_mat, n, work, lwork, info);
+  int hinfo = 0;
+  WF_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  if (st != CUSOLVER_STATUS_SUCCESS || hinfo != 0) {
+    cudaFree(work_mat); cudaFree(work); cudaFree(info);
+    throw Error{WF4DVAR_ENOTSPD, std::string("Cholesky breakdown of ") + name +
+                                     " (info=" + std::to_string(hinfo) + ")"};
+  }
+  int64_t tot = (int64_t)n * n;
+  k_extract_chol<<<(unsigned)((tot + 255) / 256), 256, 0, c.st>>>(work_mat, G, U, n);
+  WF_CUDA(cudaGetLastError());
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  cudaFree(work_mat); cudaFree(work); cudaFree(info);
+}
+
+// eigen-decomposition (ascending) of a symmetric n x n device matrix -> host lam, V (col-major)
+static void eigh(Ctx &c, Solver &sv, const double *Adev, int n, std::vector<double> &lam,
+                 std::vector<double> &V) {
+  double *A = nullptr, *W = nullptr, *work = nullptr;
+  int *info = nullptr;
+  WF_CUDA(cudaMalloc(&A, (size_t)n * n * 8));
+  WF_CUDA(cudaMalloc(&W, (size_t)n * 8));
+  WF_CUDA(cudaMalloc(&info, sizeof(int)));
+  WF_CUDA(cudaMemcpyAsync(A, Adev, (size_t)n * n * 8, cudaMemcpyDeviceToDevice, c.st));
+  int lwork = 0;
+  cusolverDnDsyevd_bufferSize(sv.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, A, n, W, &lwork);
+  WF_CUDA(cudaMalloc(&work, (size_t)std::max(lwork, 1) * 8));
+  cusolverStatus_t st = cusolverDnDsyevd(sv.h, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                         A, n, W, work, lwork, info);
+  int hinfo = 0;
+  lam.resize(n);
+  V.resize((size_t)n * n);
+  WF_CUDA(cudaMemcpyAsync(&hinfo, info, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  WF_CUDA(cudaMemcpyAsync(lam.data(), W, (size_t)n * 8, cudaMemcpyDeviceToHost, c.st));
+  WF_CUDA(cudaMemcpyAsync(V.data(), A, (size_t)n * n * 8, cudaMemcpyDeviceToHost, c.st));
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  cudaFree(A); cudaFree(W); cudaFree(work); cudaFree(info);
+  if (st != CUSOLVER_STATUS_SUCCESS || hinfo != 0) throw Error{WF4DVAR_ECUDA, "syevd failed"};
+}
+
+static void dev_free(Ctx &c, double *&ptr) {
+  if (!ptr) return;
+  auto it = std::find(c.allocs.begin(), c.allocs.end(), (void *)ptr);
+  if (it != c.allocs.end()) c.allocs.erase(it);
+  cudaFree(ptr);
+  ptr = nullptr;
+}
+
+void free_precond(Ctx &c) {
+  dev_free(c, c.GB); dev_free(c, c.GBt); dev_free(c, c.GQ); dev_free(c, c.GQt);
+  dev_free(c, c.GR); dev_free(c, c.GRt); dev_free(c, c.Rdiag_inv);
+  dev_free(c, c.U_me); dev_free(c, c.Kinv_me); dev_free(c, c.ws_lr);
+  c.r_me = 0;
+}
+
+void setup_precond(Ctx &c) {
+  const wf4dvar_precond &pc = c.pc;
+  const int s = c.s, p = c.p;
+  WF_REQUIRE(pc.shape == WF4DVAR_PD || pc.shape == WF4DVAR_PI, WF4DVAR_EINVAL, "bad shape");
+  WF_REQUIRE(pc.lhat >= WF4DVAR_L0 && pc.lhat <= WF4DVAR_LEXACT, WF4DVAR_EINVAL, "bad lhat");
+  WF_REQUIRE(pc.rhat >= WF4DVAR_RDIAG && pc.rhat <= WF4DVAR_REXACT, WF4DVAR_EINVAL, "bad rhat");
+  if (pc.lhat == WF4DVAR_LM)
+    WF_REQUIRE(pc.k >= 1 && pc.k <= c.N + 1, WF4DVAR_EINVAL, "L_M(k) needs 1 <= k <= N+1");
+  if (pc.rhat == WF4DVAR_RBLOCK)
+    WF_REQUIRE(pc.block >= 1 && pc.block <= p, WF4DVAR_EINVAL, "R_block needs 1 <= block <= p");
+  WF_REQUIRE(pc.dhat_ridge >= 0, WF4DVAR_EINVAL, "dhat_ridge must be >= 0");
+  free_precond(c);
+  Solver sv(c.st);
+  std::vector<double> h;
+  // ---- D_hat factors (P_D only)
+  if (pc.shape == WF4DVAR_PD) {
+    c.GB = c.alloc<double>((size_t)s * s); c.GBt = c.alloc<double>((size_t)s * s);
+    c.GQ = c.alloc<double>((size_t)s * s); c.GQt = c.alloc<double>((size_t)s * s);
+    for (int which = 0; which < 2; ++which) {
+      const double *src = which == 0 ? c.B : c.Q;
+      h.resize((size_t)s * s);
+      WF_CUDA(cudaMemcpy(h.data(), src, h.size() * 8, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < s; ++i) h[(size_t)i * s + i] += pc.dhat_ridge;
+      double *tmp = nullptr;
+      WF_CUDA(cudaMalloc(&tmp, h.size() * 8));
+      WF_CUDA(cudaMemcpy(tmp, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+      try {
+        chol(c, sv, tmp, s, which == 0 ? c.GB : c.GQ, which == 0 ? c.GBt : c.GQt,
+             which == 0 ? "B_hat" : "Q_hat");
+      } catch (...) { cudaFree(tmp); throw; }
+      cudaFree(tmp);
+    }
+  }
+  // ---- R_hat
+  std::vector<double> Rh((size_t)p * p);
+  WF_CUDA(cudaMemcpy(Rh.data(), c.R, Rh.size() * 8, cudaMemcpyDeviceToHost));
+  if (pc.rhat == WF4DVAR_RDIAG) {
+    std::vector<double> dinv(p);
+    for (int i = 0; i < p; ++i) {
+      WF_REQUIRE(Rh[(size_t)i * p + i] > 0, WF4DVAR_ENOTSPD, "R has a non-positive diagonal");
+      dinv[i] = 1.0 / Rh[(size_t)i * p + i];
+    }
+    c.Rdiag_inv = c.alloc<double>(p);
+    WF_CUDA(cudaMemcpy(c.Rdiag_inv, dinv.data(), p * 8, cudaMemcpyHostToDevice));
+    return;
+  }
+  const char *name = "R";
+  if (pc.rhat == WF4DVAR_RBLOCK) {
+    // Algorithm 1 with uniform pvec and every cut applied: block diagonal of R
+    name = "R_block";
+    for (int i = 0; i < p; ++i)
+      for (int j = 0; j < p; ++j)
+        if (i / pc.block != j / pc.block) Rh[(size_t)i * p + j] = 0.0;
+  }
+  double *Rdev = nullptr;
+  WF_CUDA(cudaMalloc(&Rdev, Rh.size() * 8));
+  WF_CUDA(cudaMemcpy(Rdev, Rh.data(), Rh.size() * 8, cudaMemcpyHostToDevice));
+  try {
+    if (pc.rhat == WF4DVAR_RRR || pc.rhat == WF4DVAR_RME) {
+      std::vector<double> lam, V;
+      eigh(c, sv, c.R, p, lam, V);
+      if (pc.rhat == WF4DVAR_RRR) {
+        // Algorithm 2: R + gamma I, gamma = lambda_min(R) online
+        name = "R_RR";
+        c.gamma_used = pc.gamma >= 0 ? pc.gamma : lam[0];
+        for (int i = 0; i < p; ++i) Rh[(size_t)i * p + i] += c.gamma_used;
+        WF_CUDA(cudaMemcpy(Rdev, Rh.data(), Rh.size() * 8, cudaMemcpyHostToDevice));
+      } else {
+        // Algorithm 3 via Woodbury on chol(R): eigenvalues below T raised to T.
+        name = "R (R_ME base)";
+        const double lmin = lam[0];
+        double T = pc.T;
+        if (T < 0) {
+          T = lam[p - 1];
+          for (int i = 0; i < p; ++i)
+            if (lam[i] > lmin * (1.0 + 1e-10)) { T = lam[i]; break; }
+        }
+        c.T_used = T;
+        std::vector<int> sel;
+        for (int i = 0; i < p; ++i)
+          if (lam[i] < T * (1.0 - 1e-10)) sel.push_back(i);
+        WF_REQUIRE(sel.size() <= 8, WF4DVAR_EINVAL, "R_ME: more than 8 eigenvalues below T");
+        int r = (int)sel.size();
+        c.r_me = r;
+        if (r > 0) {
+          // U = R^{-1} V = V diag(1/lambda);  K = C^{-1} + V^T U = diag(1/(T-l) + 1/l)
+          std::vector<double> U((size_t)p * r), K((size_t)r * r, 0.0), Kinv((size_t)r * r, 0.0);
+          for (int a = 0; a < r; ++a) {
+            int idx = sel[a];
+            for (int i = 0; i < p; ++i) U[(size_t)i * r + a] = V[(size_t)idx * p + i] / lam[idx];
+          }
+          for (int a = 0; a < r; ++a)
+            for (int b = 0; b < r; ++b) {
+              double v = 0.0;
+              for (int i = 0; i < p; ++i) v += V[(size_t)sel[a] * p + i] * U[(size_t)i * r + b];
+              K[(size_t)a * r + b] = v + (a == b ? 1.0 / (T - lam[sel[a]]) : 0.0);
+            }
+          // invert small SPD K by Gauss-Jordan
+          std::vector<double> Aug((size_t)r * 2 * r, 0.0);
+          for (int a = 0; a < r; ++a) {
+            for (int b = 0; b < r; ++b) Aug[(size_t)a * 2 * r + b] = K[(size_t)a * r + b];
+            Aug[(size_t)a * 2 * r + r + a] = 1.0;
+          }
+          for (int col = 0; col < r; ++col) {
+            int piv = col;
+            for (int q = col + 1; q < r; ++q)
+              if (std::fabs(Aug[(size_t)q * 2 * r + col]) > std::fabs(Aug[(size_t)piv * 2 * r + col])) piv = q;
+            for (int b = 0; b < 2 * r; ++b) std::swap(Aug[(size_t)col * 2 * r + b], Aug[(size_t)piv * 2 * r + b]);
+            double d = Aug[(size_t)col * 2 * r + col];
+            for (int b = 0; b < 2 * r; ++b) Aug[(size_t)col * 2 * r + b] /= d;
+            for (int q = 0; q < r; ++q)
+              if (q != col) {
+                double f = Aug[(size_t)q * 2 * r + col];
+                for (int b = 0; b < 2 * r; ++b) Aug[(size_t)q * 2 * r + b] -= f * Aug[(size_t)col * 2 * r + b];
+              }
+          }
+          for (int a = 0; a < r; ++a)
+            for (int b = 0; b < r; ++b) Kinv[(size_t)a * r + b] = Aug[(size_t)a * 2 * r + r + b];
+          c.U_me = c.alloc<double>(U.size());
+          c.Kinv_me = c.alloc<double>(Kinv.size());
+          c.ws_lr = c.alloc<double>((size_t)r * c.ncol);
+          WF_CUDA(cudaMemcpy(c.U_me, U.data(), U.size() * 8, cudaMemcpyHostToDevice));
+          WF_CUDA(cudaMemcpy(c.Kinv_me, Kinv.data(), Kinv.size() * 8, cudaMemcpyHostToDevice));
+        }
+      }
+    }
+    c.GR = c.alloc<double>((size_t)p * p);
+    c.GRt = c.alloc<double>((size_t)p * p);
+    chol(c, sv, Rdev, p, c.GR, c.GRt, name);
+  } catch (...) { cudaFree(Rdev); throw; }
+  cudaFree(Rdev);
+}
+
+}  // namespace wf

@@ -1,0 +1,161 @@
+// Vector kernels of the hot path: R_diag scaling, the R_ME Woodbury
+// low-rank correction (Alg. 3 applied "as a low-rank update to the Cholesky
+// factors via the Woodbury identity"), and the batched per-RHS dot
+// products of the Krylov solvers (deterministic two-phase reduction, no atomics).
+#include "internal.h"
+
+namespace wf {
+
+void copy(Ctx &c, double *dst, const double *src, int64_t n) {
+  if (dst == src || n <= 0) return;
+  WF_CUDA(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+}
+
+__global__ void k_scale_rows(double *y, const double *x, const double *rs, int rows, int64_t ld) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)rows * ld) return;
+  y[e] = x[e] * rs[e / ld];
+}
+
+void scale_rows(Ctx &c, double *y, const double *x, const double *rs, int rows) {
+  int64_t tot = (int64_t)rows * c.ncol;
+  LaunchScope ls(c, K_VEC, (double)tot, 16.0 * tot);
+  k_scale_rows<<<(unsigned)((tot + 255) / 256), 256, 0, c.st>>>(y, x, rs, rows, c.ncol);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
+}
+
+// t[j][col] = sum_i U[i][j] x[i][col]   then   s = Kinv t   (r <= 8)
+template <int RM>
+__global__ void k_lowrank_t(double *s_out, const double *x, const double *U, const double *Kinv,
+                            int p, int r, int64_t ld) {
+  int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= ld) return;
+  double t[RM];
+#pragma unroll
+  for (int j = 0; j < RM; ++j) t[j] = 0.0;
+  for (int i = 0; i < p; ++i) {
+    double xv = x[(int64_t)i * ld + col];
+#pragma unroll
+    for (int j = 0; j < RM; ++j)
+      if (j < r) t[j] = fma(U[i * r + j], xv, t[j]);
+  }
+#pragma unroll
+  for (int a = 0; a < RM; ++a) {
+    if (a >= r) break;
+    double v = 0.0;
+#pragma unroll
+    for (int b = 0; b < RM; ++b)
+      if (b < r) v = fma(Kinv[a * r + b], t[b], v);
+    s_out[(int64_t)a * ld + col] = v;
+  }
+}
+
+// y[i][col] -= sum_j U[i][j] s[j][col]
+__global__ void k_lowrank_apply(double *y, const double *s_in, const double *U, int p, int r,
+                                int64_t ld) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)p * ld) return;
+  int64_t i = e / ld, col = e % ld;
+  double v = 0.0;
+  for (int j = 0; j < r; ++j) v = fma(U[i * r + j], s_in[(int64_t)j * ld + col], v);
+  y[e] -= v;
+}
+
+void lowrank_correct(Ctx &c, double *y, const double *x) {
+  if (c.r_me <= 0) return;
+  const int p = c.p, r = c.r_me;
+  const int64_t ld = c.ncol;
+  {
+    LaunchScope ls(c, K_VEC, 2.0 * p * r * (double)ld, 8.0 * p * ld);
+    k_lowrank_t<8><<<(unsigned)((ld + 127) / 128), 128, 0, c.st>>>(c.ws_lr, x, c.U_me, c.Kinv_me,
+                                                                    p, r, ld);
+    WF_CUDA(cudaGetLastError());
+    c.launches++;
+  }
+  {
+    int64_t tot = (int64_t)p * ld;
+    LaunchScope ls(c, K_VEC, 2.0 * p * r * (double)ld, 16.0 * tot);
+    k_lowrank_apply<<<(unsigned)((tot + 255) / 256), 256, 0, c.st>>>(y, c.ws_lr, c.U_me, p, r, ld);
+    WF_CUDA(cudaGetLastError());
+    c.launches++;
+  }
+}
+
+// ------------------------------------------------------------------ dots
+struct DotArgs { const double *a[4]; const double *b[4]; };
+
+template <int ND>
+__global__ void __launch_bounds__(256) k_dots_partial(DotArgs args, int64_t rows, int m, int RB,
+                                                      int64_t rpb, double *part) {
+  __shared__ double sm[ND][256];
+  const int t = threadIdx.x;
+  const int rl = t % RB, u = t / RB, U = 256 / RB;
+  const int r = blockIdx.x * RB + rl;
+  const int64_t row0 = (int64_t)blockIdx.y * rpb;
+  const int64_t row1 = min(rows, row0 + rpb);
+  double acc[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) acc[d] = 0.0;
+  if (r < m && u < U) {
+    for (int64_t row = row0 + u; row < row1; row += U) {
+      int64_t f = row * m + r;
+#pragma unroll
+      for (int d = 0; d < ND; ++d) acc[d] = fma(args.a[d][f], args.b[d][f], acc[d]);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < ND; ++d) sm[d][t] = acc[d];
+  __syncthreads();
+  if (u == 0 && r < m) {
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      double v = 0.0;
+      for (int uu = 0; uu < U; ++uu) v += sm[d][uu * RB + rl];
+      part[((int64_t)blockIdx.y * ND + d) * m + r] = v;
+    }
+  }
+}
+
+__global__ void k_dots_final(const double *part, int nparts, int nd, int m, double *out) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nd * m) return;
+  int d = e / m, r = e % m;
+  double v = 0.0;
+  for (int b = 0; b < nparts; ++b) v += part[((int64_t)b * nd + d) * m + r];
+  out[e] = v;
+}
+
+void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_t n, double *out) {
+  const int m = c.m;
+  const int64_t rows = n / m;
+  const int RB = m < 256 ? m : 256;
+  const int gx = (m + RB - 1) / RB;
+  int gy = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + gx - 1) / gx, (rows + 255) / 256));
+  const int64_t rpb = (rows + gy - 1) / gy;
+  gy = (int)((rows + rpb - 1) / rpb);
+  const int need = gy * nd * m;
+  WF_REQUIRE(need <= c.dot_part_cap, WF4DVAR_EINVAL, "dot partial buffer too small");
+  DotArgs args{};
+  for (int d = 0; d < nd; ++d) { args.a[d] = a[d]; args.b[d] = b[d]; }
+  {
+    LaunchScope ls(c, K_DOT, 2.0 * nd * n, 16.0 * nd * n);
+    dim3 grid(gx, gy);
+    switch (nd) {
+      case 1: k_dots_partial<1><<<grid, 256, 0, c.st>>>(args, rows, m, RB, rpb, c.dot_part); break;
+      case 2: k_dots_partial<2><<<grid, 256, 0, c.st>>>(args, rows, m, RB, rpb, c.dot_part); break;
+      case 3: k_dots_partial<3><<<grid, 256, 0, c.st>>>(args, rows, m, RB, rpb, c.dot_part); break;
+      default: k_dots_partial<4><<<grid, 256, 0, c.st>>>(args, rows, m, RB, rpb, c.dot_part); break;
+    }
+    WF_CUDA(cudaGetLastError());
+    c.launches++;
+  }
+  {
+    LaunchScope ls(c, K_DOT, 0, 8.0 * gy * nd * m);
+    k_dots_final<<<(nd * m + 127) / 128, 128, 0, c.st>>>(c.dot_part, gy, nd, m, out);
+    WF_CUDA(cudaGetLastError());
+    c.launches++;
+  }
+}
+
+}  // namespace wf

@@ -1,0 +1,214 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances:
+  apply_A          relative 2-norm error per RHS <= 1e-12 (BJ north_star).
+  apply_P          relative error per RHS <= max(1e-12, 50 * kappa * u), kappa the
+                   largest condition number among the SPD blocks the
+                   preconditioner solves with (forward error of any backward-stable
+                   solve is Theta(kappa u)); plus, where P is small enough to
+                   assemble, the backward error ||P y - x|| / (||P|| ||y||) <= 1e-14.
+  solves           ||x_gpu - x_oracle|| / ||x_oracle|| <= 1e-9 and iteration counts
+                   within +-1 (BJ north_star) on short runs.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import krylov as KR
+from oracle import rhat as RH
+from synth import configs as SC
+from synth.layout import from_paper_order, to_paper_order
+
+from .helpers import OracleCols, oracle_precond, rel_err_cols, seeded_vec
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+U = 2.220446049250313e-16
+
+
+def W4():
+    import paper_2105_06975_b200 as W
+    return W
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda")
+
+
+def kappa_bound(prob, pc):
+    ks = []
+    if pc.get("shape", "PD") == "PD":
+        r = pc.get("ridge", 0.0)
+        ks += [np.linalg.cond(RH.dhat(prob.B, r)), np.linalg.cond(RH.dhat(prob.Q, r))]
+    if pc.get("rhat", "exact") != "diag":
+        ks.append(np.linalg.cond(RH.rhat(prob.R, pc.get("rhat", "exact"), pc.get("gamma", -1.0),
+                                         pc.get("T", -1.0), pc.get("block", 0))))
+    return max(ks) if ks else 1.0
+
+
+PROBS = {
+    # ragged everywhere: s, p not multiples of 64; m odd (8-byte load path); dense M_w
+    "dense": lambda: SC.random_dense_problem(s=70, p=37, N=4, m=3, seed=1),
+    # heat stencil path (s >= 2D+1), p = s/2, m = 5
+    "heat": lambda: SC.custom_problem(s=200, N=6, q=2, m=5, seed0=3),
+    # BASELINE.json configs[0]
+    "c0": lambda: SC.make_problem(0),
+}
+_cache = {}
+
+
+def get(name):
+    if name not in _cache:
+        prob = PROBS[name]()
+        _cache[name] = (prob, OracleCols(prob))
+    return _cache[name]
+
+
+CELLS = [dict(shape=s, lhat=l, k=k, rhat=r, block=b, ridge=rd)
+         for s, (l, k), (r, b), rd in itertools.product(
+             ("PD", "PI"), (("L0", 1), ("LI", 1), ("LM", 1), ("LM", 2), ("LM", 3), ("L", 1)),
+             (("diag", 0), ("block", 8), ("rr", 0), ("me", 0), ("exact", 0)), (0.0,))]
+CELLS.append(dict(shape="PD", lhat="LM", k=2, rhat="exact", ridge=0.01))
+
+
+@pytest.mark.parametrize("name", list(PROBS))
+def test_apply_A(name):
+    prob, ora = get(name)
+    ctx = W4().Context.from_problem(prob, dict(shape="PD", lhat="LM", k=2, rhat="exact"))
+    x = seeded_vec(prob.n, 11)
+    y = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    ctx.apply_A(dev(x), y)
+    torch.cuda.synchronize()
+    errs = rel_err_cols(y.cpu().numpy(), ora.apply_A(x), prob)
+    assert max(errs.values()) <= 1e-12, errs
+
+
+@pytest.mark.parametrize("name", ["dense", "heat"])
+@pytest.mark.parametrize("pc", CELLS, ids=lambda p: f"{p['shape']}-{p['lhat']}{p['k']}-{p['rhat']}-r{p['ridge']}")
+def test_apply_P(name, pc):
+    prob, ora = get(name)
+    ctx = W4().Context.from_problem(prob, pc)
+    x = seeded_vec(prob.n, 12)
+    y = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    ctx.apply_P(dev(x), y)
+    torch.cuda.synchronize()
+    yg = y.cpu().numpy()
+    ref = ora.apply_P(pc, x)
+    tol = max(1e-12, 50 * kappa_bound(prob, pc) * U)
+    errs = rel_err_cols(yg, ref, prob)
+    assert max(errs.values()) <= tol, (errs, tol)
+    if name == "dense":   # backward error against the assembled P (column 0)
+        sad = ora.sad[0]
+        P = sad.assemble_P(oracle_precond(pc))
+        yc = to_paper_order(yg, prob.s, prob.p, prob.W, prob.m)[0]
+        xc = to_paper_order(x, prob.s, prob.p, prob.W, prob.m)[0]
+        bwd = np.linalg.norm(P @ yc - xc) / (np.linalg.norm(P, 2) * np.linalg.norm(yc))
+        assert bwd <= 1e-14, bwd
+
+
+def test_apply_AP_and_host_path_agree():
+    prob, ora = get("heat")
+    pc = dict(shape="PI", lhat="LM", k=3, rhat="me")
+    ctx = W4().Context.from_problem(prob, pc)
+    x = seeded_vec(prob.n, 13)
+    t = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(t)
+    ctx.apply_AP(dev(x), t, y)
+    yh = np.empty(prob.n)
+    ctx.apply_AP_host(x, yh)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(y.cpu().numpy(), yh)   # same kernels, bitwise
+    # against the oracle: A (P^{-1} x)
+    tp = ora.apply_P(pc, x)
+    tvec = from_paper_order(np.stack([tp[c] for c in range(prob.m)]), prob.s, prob.p, prob.W)
+    ref = ora.apply_A(tvec)
+    errs = rel_err_cols(yh, ref, prob)
+    assert max(errs.values()) <= max(1e-12, 50 * kappa_bound(prob, pc) * U), errs
+
+
+def test_determinism_bitwise():
+    prob, _ = get("heat")
+    ctx = W4().Context.from_problem(prob, dict(shape="PD", lhat="LM", k=3, rhat="exact"))
+    x = dev(seeded_vec(prob.n, 14))
+    outs = []
+    for _ in range(3):
+        t = torch.empty_like(x)
+        y = torch.empty_like(x)
+        ctx.apply_AP(x, t, y)
+        outs.append(y.cpu().numpy())
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+def test_counters_match_paper_accounting():
+    prob, ora = get("heat")
+    pc = dict(shape="PD", lhat="LM", k=3, rhat="block", block=8)
+    ctx = W4().Context.from_problem(prob, pc)
+    b = dev(prob.rhs)
+    x = torch.zeros_like(b)
+    rep = ctx.solve(b, x, solver="minres", tol=1e-6, maxit=40)
+    W, N = prob.W, prob.N
+    it_A, it_P = rep["n_apply_A"], rep["n_apply_P"]
+    assert rep["n_R"] == W * it_A
+    assert rep["n_D"] == W * (it_A + it_P)
+    assert rep["n_Dhat_inv"] == W * it_P and rep["n_Rhat_inv"] == W * it_P
+    assert rep["n_M"] == 2 * N * it_A + 2 * (N - N // 3) * it_P
+
+
+@pytest.mark.parametrize("k,rhat", [(5, "exact"), (3, "me"), (2, "rr")])
+def test_minres_c0_matches_oracle(k, rhat):
+    prob, ora = get("c0")
+    pc = dict(shape="PD", lhat="LM", k=k, rhat=rhat)
+    ctx = W4().Context.from_problem(prob, pc)
+    b = dev(prob.rhs)
+    x = torch.empty_like(b)
+    rep = ctx.solve(b, x, solver="minres", tol=1e-10, maxit=5000, history=True)
+    sad = ora.sad[0]
+    bp = to_paper_order(prob.rhs, prob.s, prob.p, prob.W, 1)[0]
+    opc = oracle_precond(pc)
+    xo, info = KR.minres(sad.apply_A, lambda v: sad.apply_Pinv(opc, v), bp, tol=1e-10, maxit=5000)
+    xg = to_paper_order(x.cpu().numpy(), prob.s, prob.p, prob.W, 1)[0]
+    assert rep["converged"][0] and info["converged"]
+    assert abs(int(rep["iters"][0]) - info["iters"]) <= 1, (rep["iters"], info["iters"])
+    assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-9
+    xstar = np.linalg.solve(sad.assemble_A(), bp)
+    assert np.linalg.norm(xg - xstar) / np.linalg.norm(xstar) <= 1e-7
+
+
+@pytest.mark.parametrize("k,rhat,restart", [(5, "exact", 50), (3, "rr", 50), (1, "exact", 20)])
+def test_gmres_c0_matches_oracle(k, rhat, restart):
+    prob, ora = get("c0")
+    pc = dict(shape="PI", lhat="LM", k=k, rhat=rhat)
+    ctx = W4().Context.from_problem(prob, pc)
+    b = dev(prob.rhs)
+    x = torch.empty_like(b)
+    rep = ctx.solve(b, x, solver="gmres", tol=1e-10, maxit=5000, restart=restart, history=True)
+    sad = ora.sad[0]
+    bp = to_paper_order(prob.rhs, prob.s, prob.p, prob.W, 1)[0]
+    opc = oracle_precond(pc)
+    xo, info = KR.gmres(sad.apply_A, lambda v: sad.apply_Pinv(opc, v), bp, tol=1e-10,
+                        restart=restart, maxit=5000)
+    xg = to_paper_order(x.cpu().numpy(), prob.s, prob.p, prob.W, 1)[0]
+    assert rep["converged"][0] and info["converged"]
+    assert abs(int(rep["iters"][0]) - info["iters"]) <= 1, (rep["iters"], info["iters"])
+    assert np.linalg.norm(xg - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+def test_batched_solve_matches_per_rhs_oracle():
+    prob, ora = get("heat")
+    pc = dict(shape="PI", lhat="LM", k=2, rhat="exact")
+    ctx = W4().Context.from_problem(prob, pc)
+    b = dev(prob.rhs)
+    x = torch.empty_like(b)
+    rep = ctx.solve(b, x, solver="gmres", tol=1e-10, maxit=2000, restart=50)
+    xg = to_paper_order(x.cpu().numpy(), prob.s, prob.p, prob.W, prob.m)
+    B = to_paper_order(prob.rhs, prob.s, prob.p, prob.W, prob.m)
+    opc = oracle_precond(pc)
+    for c in range(prob.m):
+        sad = ora.sad[c]
+        xo, info = KR.gmres(sad.apply_A, lambda v: sad.apply_Pinv(opc, v), B[c], tol=1e-10,
+                            restart=50, maxit=2000)
+        assert info["converged"] and rep["converged"][c]
+        assert abs(int(rep["iters"][c]) - info["iters"]) <= 1
+        assert np.linalg.norm(xg[c] - xo) / np.linalg.norm(xo) <= 1e-9
