@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: saddle-point A+P applies/sec (FP64) and time-to-1e-8 residual, % of roofline.
+
+Workload (default): BASELINE.json configs[3] -- linear heat s=4096, N=127
+(128 windows), p=1024, 64 RHS, P_D with the parallel-in-time L_M(4) and R_hat = R,
+preconditioned MINRES.  configs[3] is the configuration
+BASELINE.json asks to be reported at 1/2/4/8 GPUs and the one whose covariance
+products are true FP64 contractions; other configs via --config.
+
+One STEP = one batched MINRES iteration over all m RHS = one A apply + one P_D
+apply + the Krylov vector work.  value = steps/s
+summed over ranks = A+P applies/s of the whole job.  Each rank solves its own
+independent batch (distinct seeds): no data-path collective, scaling "weak".
+
+Timing: W warm-up steps, then exactly K steps inside ONE wf4dvar_solve call
+(tol below reach, so exactly K iterations; the solve's initialisation -- one
+extra P apply and two reductions -- is inside the timed region, which only
+makes the number pessimistic), bracketed by barrier + cuda synchronize, CUDA
+events on the library's stream, max over ranks.  Inputs are larger than L2
+(each Krylov vector is 604 MB at configs[3]).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CELLS = {
+    0: dict(shape="PD", lhat="LM", k=3, rhat="exact", solver="minres"),
+    1: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
+    2: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
+    3: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
+    4: dict(shape="PI", lhat="LM", k=4, rhat="exact", solver="gmres"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--m", type=int, default=None, help="override the RHS batch width")
+    ap.add_argument("--shape", default=None)
+    ap.add_argument("--lhat", default=None)
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--rhat", default=None)
+    ap.add_argument("--tts-maxit", type=int, default=400,
+                    help="cap for the time-to-1e-8 solve (0 disables it)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler (the recipe's clocks line) running during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.p = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            out = self.p.communicate()[0]
+            self.lines = [l for l in out.strip().splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measure_dgemm_peak(torch, dev):
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del a, b
+    torch.cuda.empty_cache()
+    return 2 * n ** 3 / best / 1e12
+
+
+def cell_of(args):
+    cell = dict(CELLS[args.config])
+    for key in ("shape", "lhat", "k", "rhat"):
+        v = getattr(args, key)
+        if v is not None:
+            cell[key] = v
+    if cell["shape"] == "PI":
+        cell["solver"] = "gmres"
+    return cell
+
+
+def oracle_sample(prob, cell, reps=1):
+    """CPU oracle (test infrastructure) on ONE RHS column: seconds per A+P apply."""
+    from oracle.saddle import Precond, Saddle
+    from synth.layout import to_paper_order
+    sad = Saddle(prob, col=0)
+    opc = Precond(shape=cell["shape"], lhat=cell["lhat"], k=cell["k"], rhat=cell["rhat"])
+    v = np.random.Generator(np.random.PCG64(7)).standard_normal((2 * prob.s + prob.p) * prob.W)
+    sad.apply_Pinv(opc, v)          # factorisations (setup) outside the timed sample
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        sad.apply_A(sad.apply_Pinv(opc, v))
+    return (time.perf_counter() - t0) / reps
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([d.get("num_threads", 1) for d in info] or [os.cpu_count()])
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    ws, rank, local = dist_setup()
+    if rank != 0:
+        return
+    from synth import configs as SC
+    cell = cell_of(args)
+    prob = SC.make_problem(args.config, seed0=0, m=1)
+    m_full = args.m or SC.CONFIGS[args.config]["m"]
+    for _ in range(args.warmup):
+        oracle_sample(prob, cell, 1)
+    t = oracle_sample(prob, cell, args.steps)
+    val = 1.0 / (t * m_full)
+    cores = blas_threads()
+    sample = (f"1 of {m_full} RHS columns per step, blockwise oracle A+P apply "
+              f"(full s={prob.s}, N={prob.N}), scaled to the {m_full}-RHS batch")
+    line = dict(impl="reference", metric="saddle-point A+P applies/sec (FP64)", value=val,
+                unit="A+P applies/s", n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
+                ms_per_step=t * m_full * 1e3, higher_is_better=True, scaling="weak",
+                vs_baseline=None, dtype="f64", data="synthetic",
+                config=dict(workload=f"BASELINE.json configs[{args.config}]", cell=cell,
+                            s=prob.s, p=prob.p, N=prob.N, m=m_full),
+                cpu_baseline=dict(value=val, unit="A+P applies/s", cores=cores, kind="oracle",
+                                  sample=sample),
+                e2e=dict(value=val, unit="A+P applies/s", h2d_bytes_per_step=0,
+                         d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import paper_2105_06975_b200 as W
+    from synth import configs as SC
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cell = cell_of(args)
+    cfgm = SC.CONFIGS[args.config]["m"]
+    m = args.m or cfgm
+    prob = SC.make_problem(args.config, seed0=rank * m, m=m)
+    stream = torch.cuda.Stream(device=dev)
+    pc = {k: cell[k] for k in ("shape", "lhat", "k", "rhat")}
+    ctx = W.Context.from_problem(prob, pc, device=local, stream=stream.cuda_stream)
+    peak_fp64 = measure_dgemm_peak(torch, dev) if rank == 0 else None
+    b = torch.from_numpy(prob.rhs).to(dev)
+    x = torch.empty_like(b)
+    solver = cell["solver"]
+    kw = dict(solver=solver, tol=1e-300, restart=50, mark_tol=1e-8)
+
+    # warm-up (also allocates the Krylov workspace)
+    with torch.cuda.stream(stream):
+        ctx.solve(b, x, maxit=max(1, args.warmup), check_every=10 ** 6, **kw)
+    torch.cuda.synchronize(dev)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    ctx.profile_enable(True)
+    l0 = ctx.launch_count
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        rep = ctx.solve(b, x, maxit=args.steps, check_every=10 ** 6, **kw)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+    launches = ctx.launch_count - l0
+    prof = ctx.profile_read()
+    ctx.profile_enable(False)
+    secs = e0.elapsed_time(e1) / 1e3
+    if ws > 1:
+        t = torch.tensor([secs], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        secs = float(t.item())
+    steps = args.steps
+    value = ws * steps / secs
+
+    # end-to-end: the public API with HOST buffers (H2D + A+P + D2H every step)
+    xh = torch.from_numpy(np.random.Generator(np.random.PCG64(5)).standard_normal(prob.n)).pin_memory()
+    yh = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+    ctx.apply_AP_host(xh.numpy(), yh.numpy())
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        ctx.apply_AP_host(xh.numpy(), yh.numpy())
+    e2e_secs = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_secs], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_secs = float(t.item())
+    e2e_val = ws * args.e2e_steps / e2e_secs
+
+    # time-to-1e-8 (one real solve; reported, capped)
+    tts = None
+    if args.tts_maxit > 0:
+        r = ctx.solve(b, x, solver=solver, tol=1e-8, maxit=args.tts_maxit, restart=50,
+                      mark_tol=1e-8, check_every=10)
+        tts = dict(seconds=r["seconds_to_mark"] if r["seconds_to_mark"] >= 0 else None,
+                   iterations=int(r["iters_to_mark"]) if r["iters_to_mark"] >= 0 else None,
+                   maxit=args.tts_maxit, reached=bool(r["seconds_to_mark"] >= 0),
+                   max_relres_at_exit=float(np.max(r["relres"])),
+                   median_iters=float(np.median(r["iters"])))
+
+    if rank != 0:
+        return
+    # roofline of the dominant kernel class (largest share of the timed region)
+    dom = max(prof, key=lambda k: prof[k]["ms"])
+    tot_ms = sum(v["ms"] for v in prof.values())
+    d = prof[dom]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    if dom in ("gemm_dmma", "trsm_dmma"):
+        achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
+        roof = dict(bound="tensor", achieved=achieved, peak=peak_fp64, unit="TFLOP/s",
+                    frac=achieved / peak_fp64,
+                    peak_source="cuBLAS DGEMM 8192^3 measured live in this run (FP64 has no "
+                                "entry in MEASURED_PEAKS.json)")
+    else:
+        achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
+        pk = peaks.get("hbm_gbs", 6650.0)
+        roof = dict(bound="hbm", achieved=achieved, peak=pk, unit="GB/s", frac=achieved / pk,
+                    peak_source="MEASURED_PEAKS.json hbm_gbs")
+    roof.update(kernel=dom, launches=d["launches"], share_of_step=d["ms"] / tot_ms if tot_ms else None,
+                traffic=None)
+    traffic_file = os.path.join(ROOT, "profiles", f"ncu_traffic_c{args.config}.json")
+    if os.path.exists(traffic_file):
+        roof["traffic"] = json.load(open(traffic_file)).get(dom)
+    kernels = {k: dict(launches=v["launches"], ms=round(v["ms"], 3),
+                       tflops=(v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] else None,
+                       gbs=(v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None)
+               for k, v in prof.items() if v["launches"]}
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        p1 = SC.make_problem(args.config, seed0=0, m=1)
+        t1 = oracle_sample(p1, cell, 1)
+        cpu = dict(value=1.0 / (t1 * m), unit="A+P applies/s", cores=blas_threads(), kind="oracle",
+                   sample=f"one A+P apply of the blockwise oracle on 1 of {m} RHS columns at full "
+                          f"size (s={prob.s}, N={prob.N}), factorisations untimed, scaled x1/{m}")
+    line = dict(metric="saddle-point A+P applies/sec (FP64)", value=value, unit="A+P applies/s",
+                n_gpus=ws, steps=steps, warmup=args.warmup, ms_per_step=secs / steps * 1e3,
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic",
+                config=dict(workload=f"BASELINE.json configs[{args.config}]",
+                            desc=SC.CONFIGS[args.config]["desc"], cell=cell, s=prob.s, p=prob.p,
+                            N=prob.N, m=m, step="one batched Krylov iteration (1 A + 1 P apply)",
+                            l2="inputs larger than L2 (no flush needed)",
+                            parallelism=f"independent batch per rank x{ws}"),
+                roofline=roof, cpu_baseline=cpu,
+                e2e=dict(value=e2e_val, unit="A+P applies/s", h2d_bytes_per_step=prob.n * 8,
+                         d2h_bytes_per_step=prob.n * 8,
+                         how="wf4dvar_apply_AP_host: pinned host x -> device, A+P, y -> host"),
+                gpu_launches=launches, clocks=clk.summary(), time_to_1e8=tts, kernels=kernels,
+                counters=dict(n_apply_A=rep["n_apply_A"], n_apply_P=rep["n_apply_P"]))
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     // dot partials: gy <= 2*148 blocks x up to 4 dots x m
     c.dot_part_cap = 2 * 148 * 4 * std::max(c.m, 256) + 4096;
     c.dot_part = c.alloc<double>(c.dot_part_cap);
+    WF_CUDA(cudaMallocHost((void **)&c.hpin, 16 * sizeof(int)));
     c.pc = *pc;
     wf::setup_precond(c);
     WF_CUDA(cudaStreamSynchronize(c.st));
@@ -144,6 +145,9 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : c.prof.pool) cudaEventDestroy(e);
   if (c.hostbuf) cudaFreeHost(c.hostbuf);
+  if (c.hpin) cudaFreeHost(c.hpin);
+  if (c.kws) cudaFree(c.kws);
+  for (auto e : c.iter_events) cudaEventDestroy(e);
   delete ctx;
   return WF4DVAR_OK;
 }

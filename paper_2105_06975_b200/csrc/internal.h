@@ -117,6 +117,37 @@ struct Ctx {
   std::string last_error;
   std::vector<void *> allocs;
 
+  // persistent Krylov workspace arena (grown on demand, reused across solves)
+  char *kws = nullptr;
+  size_t kws_cap = 0, kws_used = 0;
+  void kws_reset(size_t need) {
+    if (need > kws_cap) {
+      if (kws) cudaFree(kws);
+      kws = nullptr;
+      kws_cap = 0;
+      if (cudaMalloc((void **)&kws, need) != cudaSuccess) throw Error{WF4DVAR_ENOMEM, "Krylov workspace"};
+      kws_cap = need;
+    }
+    kws_used = 0;
+  }
+  template <class T> T *kws_take(size_t count) {
+    size_t bytes = ((count * sizeof(T) + 255) / 256) * 256;
+    if (kws_used + bytes > kws_cap) throw Error{WF4DVAR_ENOMEM, "Krylov workspace overflow"};
+    T *p = (T *)(kws + kws_used);
+    kws_used += bytes;
+    return p;
+  }
+  int *hpin = nullptr;   // pinned host flags
+  std::vector<cudaEvent_t> iter_events;
+  cudaEvent_t iter_event(size_t i) {
+    while (iter_events.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      iter_events.push_back(e);
+    }
+    return iter_events[i];
+  }
+
   template <class T> T *alloc(size_t count) {
     void *ptr = nullptr;
     if (count == 0) count = 1;

@@ -147,48 +147,31 @@ __global__ void k_minres_s3(MinresS S, int m, int j, double tol, double mark_tol
 
 static unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-struct EventTimer {
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t get(size_t i) {
-    while (ev.size() <= i) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      ev.push_back(e);
-    }
-    return ev[i];
-  }
-  ~EventTimer() { for (auto e : ev) cudaEventDestroy(e); }
-};
 
 static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &o,
                    wf4dvar_report *rep) {
   const int64_t n = c.n;
   const int m = c.m;
-  std::vector<double *> bufs;
-  auto vec = [&]() { double *p = nullptr; WF_CUDA(cudaMalloc(&p, n * 8)); bufs.push_back(p); return p; };
-  struct Guard { std::vector<double *> &b; void *s; ~Guard() { for (auto p : b) cudaFree(p); cudaFree(s); } };
+  const int NS = 13 + 3 + 4 + 4;
+  size_t hist_n = (rep && rep->history) ? (size_t)(o.maxit + 1) * m : 0;
+  c.kws_reset(11 * (((size_t)n * 8 + 255) / 256 * 256) + (size_t)NS * m * 8 + 4 * (size_t)m * 4 +
+              hist_n * 8 + 4096);
+  auto vec = [&]() { return c.kws_take<double>(n); };
   double *res = vec(), *vp = vec(), *v = vec(), *vn = vec(), *z = vec(), *zn = vec(), *q = vec(),
          *wp = vec(), *w = vec(), *awp = vec(), *aw = vec();
-  // scalar arena
-  const int NS = 13 + 3 + 4 + 4;
-  void *arena = nullptr;
-  size_t hist_bytes = (rep && rep->history) ? (size_t)(o.maxit + 1) * m * 8 : 0;
-  WF_CUDA(cudaMalloc(&arena, (size_t)NS * m * 8 + 3 * (size_t)m * 4 + 64 + hist_bytes));
-  Guard guard{bufs, arena};
-  double *A = (double *)arena;
+  double *A = c.kws_take<double>((size_t)NS * m);
   MinresS S{};
   S.gamma = A; S.gamma_prev = A + m; S.eta = A + 2 * m; S.c = A + 3 * m; S.c_prev = A + 4 * m;
   S.sn = A + 5 * m; S.sn_prev = A + 6 * m; S.delta = A + 7 * m; S.bnorm = A + 8 * m;
   S.relres = A + 9 * m; S.gnew = A + 10 * m; S.cnew = A + 11 * m; S.snew = A + 12 * m;
   S.cv = A + 13 * m; S.coef = A + 16 * m; S.dots = A + 20 * m;
-  int *I = (int *)(A + NS * m);
+  int *I = c.kws_take<int>(2 * (size_t)m + 4);
   S.active = I; S.iters = I + m; S.flags = I + 2 * m;
-  S.hist = hist_bytes ? (double *)((char *)(I + 2 * m) + 64) : nullptr;
+  S.hist = hist_n ? c.kws_take<double>(hist_n) : nullptr;
   const int h_flags[4] = {0, 0, -1, 0};
   WF_CUDA(cudaMemcpyAsync(S.flags, h_flags, sizeof(h_flags), cudaMemcpyHostToDevice, c.st));
 
-  EventTimer et;
-  cudaEvent_t e0 = et.get(0);
+  cudaEvent_t e0 = c.iter_event(0);
   WF_CUDA(cudaEventRecord(e0, c.st));
   // init: x = 0, r = b, v_prev = 0, v = b, z = P^{-1} v
   WF_CUDA(cudaMemsetAsync(x, 0, n * 8, c.st));
@@ -210,9 +193,7 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   int j = 0;
   bool indef = false;
   const int ce = std::max(1, o.check_every);
-  std::vector<int> poll_at;
-  int *hpin = nullptr;
-  WF_CUDA(cudaMallocHost(&hpin, 4 * sizeof(int)));
+  int *hpin = c.hpin;
   for (j = 1; j <= o.maxit; ++j) {
     apply_A(c, z, q);
     { const double *a[1] = {q}, *bb[1] = {z}; dots(c, 1, a, bb, n, S.dots); }
@@ -228,7 +209,7 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
     k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, j, o.tol, o.mark_tol);
     c.launches++;
     WF_CUDA(cudaGetLastError());
-    WF_CUDA(cudaEventRecord(et.get(j), c.st));
+    WF_CUDA(cudaEventRecord(c.iter_event(j), c.st));
     // rotate: v_prev <- v, v <- v_new, z <- z_new, w_prev <- w, w <- w_new(in wp), same for Aw
     std::swap(vp, v); std::swap(v, vn);     // vp=old v, v=vn, vn=old vp (free)
     std::swap(z, zn);
@@ -246,15 +227,14 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
   WF_CUDA(cudaStreamSynchronize(c.st));
   memcpy(h, hpin, 3 * sizeof(int));
-  cudaFreeHost(hpin);
   if (rep) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, e0, et.get(j));
+    cudaEventElapsedTime(&ms, e0, c.iter_event(j));
     rep->seconds = ms * 1e-3;
     rep->iters_to_mark = h[2];
     rep->seconds_to_mark = -1;
     if (h[2] >= 0) {
-      cudaEventElapsedTime(&ms, e0, et.get(h[2]));
+      cudaEventElapsedTime(&ms, e0, c.iter_event(h[2]));
       rep->seconds_to_mark = ms * 1e-3;
     }
     std::vector<int> it(m), act(m);
@@ -501,30 +481,30 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
   gy = (int)((rows + rpb - 1) / rpb);
   const int jmax = mr + 1;
 
-  std::vector<void *> mem;
-  auto dmal = [&](size_t bytes) { void *p = nullptr; WF_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 8))); mem.push_back(p); return p; };
-  struct Guard { std::vector<void *> &m; ~Guard() { for (auto p : m) cudaFree(p); } } guard{mem};
-  double *V = (double *)dmal((size_t)(mr + 1) * n * 8);
-  double *u = (double *)dmal(n * 8), *tmp = (double *)dmal(n * 8);
-  double *part = (double *)dmal((size_t)gy * jmax * m * 8);
+  const size_t vecb = ((size_t)n * 8 + 255) / 256 * 256;
+  c.kws_reset((size_t)(mr + 3) * vecb + (size_t)gy * jmax * m * 8 +
+              (size_t)m * ((mr + 1) * mr + (mr + 1) + 2 * mr + 4 + 3 * jmax) * 8 +
+              (size_t)(5 * m + 4) * 4 + ((rep && rep->history) ? (size_t)(o.maxit + 1) * m * 8 : 0) +
+              64 * 256);
+  double *V = c.kws_take<double>((size_t)(mr + 1) * n);
+  double *u = c.kws_take<double>(n), *tmp = c.kws_take<double>(n);
+  double *part = c.kws_take<double>((size_t)gy * jmax * m);
   GmresS S{};
   S.mr = mr; S.m = m; S.maxit = o.maxit;
-  S.H = (double *)dmal((size_t)m * (mr + 1) * mr * 8);
-  S.g = (double *)dmal((size_t)m * (mr + 1) * 8);
-  S.cs = (double *)dmal((size_t)m * mr * 8);
-  S.sn = (double *)dmal((size_t)m * mr * 8);
-  S.bnorm = (double *)dmal(m * 8); S.relres = (double *)dmal(m * 8); S.inv = (double *)dmal(m * 8);
-  S.h1 = (double *)dmal((size_t)jmax * m * 8); S.h2 = (double *)dmal((size_t)jmax * m * 8);
-  S.y = (double *)dmal((size_t)jmax * m * 8);
-  S.ww = (double *)dmal(m * 8);
-  int *I = (int *)dmal((size_t)(5 * m + 4) * 4);
+  S.H = c.kws_take<double>((size_t)m * (mr + 1) * mr);
+  S.g = c.kws_take<double>((size_t)m * (mr + 1));
+  S.cs = c.kws_take<double>((size_t)m * mr);
+  S.sn = c.kws_take<double>((size_t)m * mr);
+  S.bnorm = c.kws_take<double>(m); S.relres = c.kws_take<double>(m); S.inv = c.kws_take<double>(m);
+  S.h1 = c.kws_take<double>((size_t)jmax * m); S.h2 = c.kws_take<double>((size_t)jmax * m);
+  S.y = c.kws_take<double>((size_t)jmax * m);
+  S.ww = c.kws_take<double>(m);
+  int *I = c.kws_take<int>((size_t)5 * m + 4);
   S.active = I; S.cyc = I + m; S.jj = I + 2 * m; S.iters = I + 3 * m; S.flags = I + 4 * m;
-  S.hist = (rep && rep->history) ? (double *)dmal((size_t)(o.maxit + 1) * m * 8) : nullptr;
+  S.hist = (rep && rep->history) ? c.kws_take<double>((size_t)(o.maxit + 1) * m) : nullptr;
   const int hf[4] = {0, 0, -1, 0};
   WF_CUDA(cudaMemcpyAsync(S.flags, hf, sizeof(hf), cudaMemcpyHostToDevice, c.st));
-  int *hpin = nullptr;
-  WF_CUDA(cudaMallocHost(&hpin, 4 * sizeof(int)));
-  struct PinGuard { int *p; ~PinGuard() { cudaFreeHost(p); } } pg{hpin};
+  int *hpin = c.hpin;
 
   auto multidot = [&](int nv, const double *w, double *out) {
     LaunchScope ls(c, K_DOT, 2.0 * nv * n, 8.0 * (nv + 1) * n);
@@ -548,8 +528,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
     dots(c, 1, a, a, n, S.ww);
   };
 
-  EventTimer et;
-  WF_CUDA(cudaEventRecord(et.get(0), c.st));
+  WF_CUDA(cudaEventRecord(c.iter_event(0), c.st));
   WF_CUDA(cudaMemsetAsync(x, 0, n * 8, c.st));
   int global_it = 0;
   bool first = true;
@@ -585,7 +564,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
       k_scale_rhs<<<nblk(n, 256), 256, 0, c.st>>>(w, w, S.inv, n, m);
       c.launches += 2;
       WF_CUDA(cudaGetLastError());
-      WF_CUDA(cudaEventRecord(et.get(global_it), c.st));
+      WF_CUDA(cudaEventRecord(c.iter_event(global_it), c.st));
       // lagged poll: read the cycle-active count of the previous step
       if ((j + 1) % std::max(1, o.check_every) == 0) {
         WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
@@ -613,12 +592,12 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
   for (int r = 0; r < m; ++r) active_left += act[r];
   if (rep) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, et.get(0), et.get(global_it));
+    cudaEventElapsedTime(&ms, c.iter_event(0), c.iter_event(global_it));
     rep->seconds = ms * 1e-3;
     rep->iters_to_mark = hpin[2];
     rep->seconds_to_mark = -1;
     if (hpin[2] >= 0) {
-      cudaEventElapsedTime(&ms, et.get(0), et.get(hpin[2]));
+      cudaEventElapsedTime(&ms, c.iter_event(0), c.iter_event(hpin[2]));
       rep->seconds_to_mark = ms * 1e-3;
     }
     for (int r = 0; r < m; ++r) {
