@@ -68,6 +68,10 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
   }
 }
 
+// 128x128 CTA tile, 8 warps of 64x32: 32 independent DMMA accumulator tiles per
+// warp per k-step (hides the DMMA result latency; ncu r01 showed "wait" stalls
+// dominating the 32x32 warp tile), BK = 32 halves the barriers per FLOP.
+using CfgHuge = TileCfg<128, 128, 32, 64, 32, 3>;
 using CfgBig = TileCfg<128, 64, 16, 32, 32, 4>;
 using CfgSmall = TileCfg<64, 32, 16, 32, 16, 4>;
 
@@ -123,17 +127,19 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
   if (!valid || batch <= 0) return;
   double flops = 0, bytes = 0;
   bool v16 = true;
-  int tm, tn, big_tiles = 0;
+  int tm, tn, huge_tiles = 0, big_tiles = 0;
   for (int i = 0; i < valid; ++i) {
     const GemmProb &p = ps[i];
     flops += 2.0 * p.M * (double)p.N * p.K * batch;
     bytes += 8.0 * batch * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N * (p.Z ? 2 : 1));
     v16 = v16 && aligned16(p);
+    huge_tiles += tiles_of<CfgHuge>(p, tm, tn);
     big_tiles += tiles_of<CfgBig>(p, tm, tn);
   }
   if (flops_hint >= 0) flops = flops_hint;
   LaunchScope ls(c, K_GEMM, flops, bytes);
-  if (big_tiles * batch >= 2 * 148) run<CfgBig>(c, ps, valid, batch, v16);
+  if (huge_tiles * batch >= 2 * 148) run<CfgHuge>(c, ps, valid, batch, v16);
+  else if (big_tiles * batch >= 148) run<CfgBig>(c, ps, valid, batch, v16);
   else run<CfgSmall>(c, ps, valid, batch, v16);
   c.launches++;
 }

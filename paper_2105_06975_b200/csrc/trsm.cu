@@ -1,16 +1,19 @@
-// Cholesky-factor triangular solves for D_hat^{-1} and R_hat^{-1} (P:L647-651,
-// "apply ... using the (incomplete) Cholesky factors").
+// Cholesky-factor triangular solves for D_hat^{-1} and R_hat^{-1} (
+// R_hat^{-1} "using the ... Cholesky factors").
 //
-// One CTA owns a panel of NB right-hand-side columns and walks the 64-row
-// tiles of the triangle in dependency order (down for G, up for U = G^T):
-//   T_i = X_i - sum_{j<i} G_ij Y_j      DMMA tile GEMM (dmma.cuh pipeline),
-//   Y_i = G_ii^{-1} T_i                 exact substitution in registers, one
-//                                       warp per column group, the diagonal
-//                                       tile staged transposed in shared memory.
-// The off-diagonal work is a true FP64 contraction on the tensor path; the
-// diagonal solve is plain forward/backward substitution (backward stable).
-// For R_block the factor is block diagonal: tiles left of the row's block are
-// known zeros and are skipped (blk > 0).
+// Blocked right-looking TRSM, B200 layout:
+//   * the triangle is cut into diagonal super-blocks of SB rows;
+//   * each super-block is solved by k_trsm: one CTA per NB-column panel walks
+//     the 64-row tiles of the super-block,
+//         T_i = X_i - sum_{j<i, j in block} G_ij Y_j    (DMMA tile GEMM)
+//         Y_i = G_ii^{-1} T_i                           (exact substitution,
+//                                                         one warp per column group)
+//   * the coupling of the solved super-block to all remaining rows is one large
+//     DMMA GEMM  Y_rest -= G_rest,blk Y_blk  (gemm.cu), which is where almost
+//     all the FLOPs go.
+// R_block (Alg. 1 with uniform blocks) has a block-diagonal factor: every
+// diagonal block is an independent segment (grid.y), no GEMM coupling.
+#include <algorithm>
 #include <type_traits>
 
 #include "dmma.cuh"
@@ -27,6 +30,7 @@ using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, 3>,
 struct TrsmLaunch {
   TrsmProb p[2];
   int panels0;
+  int seg_lo, seg_len, seg_hi;   // segment j covers [seg_lo + j*seg_len, min(.. + seg_len, seg_hi))
 };
 
 template <int NB, bool UPPER, bool V16>
@@ -36,13 +40,16 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   double *sPipe = smem;                        // C::SMEM_DOUBLES
   double *sT = smem + C::SMEM_DOUBLES;         // [64][NB+1]
   double *sG = sT + TB * (NB + 1);             // [64][65] diagonal tile, transposed
+  double *sD = sG + TB * (TB + 1);             // [64] reciprocal diagonal
 
   int panel = blockIdx.x, gi = 0;
   if (panel >= L.panels0) { panel -= L.panels0; gi = 1; }
   const TrsmProb &P = L.p[gi];
   const int c0 = panel * NB;
-  const int n = P.n;
-  const int ntile = (n + TB - 1) / TB;
+  const int slo = L.seg_lo + blockIdx.y * L.seg_len;
+  const int shi = min(L.seg_hi, slo + L.seg_len);
+  if (slo >= shi) return;
+  const int ntile = (shi - slo + TB - 1) / TB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
@@ -53,17 +60,10 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
 
   for (int it = 0; it < ntile; ++it) {
     const int ti = UPPER ? (ntile - 1 - it) : it;
-    const int r0 = ti * TB, r1 = min(n, r0 + TB), nr = r1 - r0;
-    // ---- off-diagonal update: acc = G[r0:r1, K] * Y[K, panel]
-    int kbeg, kend;
-    if (!UPPER) {
-      kbeg = P.blk > 0 ? (r0 / P.blk) * P.blk : 0;
-      kbeg = (kbeg / 16) * 16;
-      kend = r0;
-    } else {
-      kbeg = r1;
-      kend = P.blk > 0 ? min(n, ((r1 - 1) / P.blk + 1) * P.blk) : n;
-    }
+    const int r0 = slo + ti * TB, r1 = min(shi, r0 + TB), nr = r1 - r0;
+    // ---- in-segment off-diagonal update: acc = G[r0:r1, K] * Y[K, panel]
+    const int kbeg = UPPER ? r1 : slo;
+    const int kend = UPPER ? shi : r0;
     double acc[C::FM][C::FN][2];
 #pragma unroll
     for (int i = 0; i < C::FM; ++i)
@@ -88,11 +88,12 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
     }
     // ---- diagonal tile, transposed: sG[c][r] = G[r0 + r][r0 + c]; identity padding
     for (int e = tid; e < TB * TB; e += 128) {
-      int r = e / TB, cc = e % TB;
+      int cc = e / TB, r = e % TB;   // consecutive threads -> consecutive r (conflict-free stores)
       double v;
       if (r < nr && cc < nr) v = G[(int64_t)(r0 + r) * P.ldg + r0 + cc];
       else v = (r == cc) ? 1.0 : 0.0;
       sG[cc * (TB + 1) + r] = v;
+      if (r == cc) sD[r] = 1.0 / v;
     }
     __syncthreads();
     // ---- substitution: warp w solves columns w, w+4, ...; lane holds rows lane, lane+32
@@ -105,33 +106,37 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
       v1[q] = sT[(lane + 32) * (NB + 1) + cc];
     }
     if (!UPPER) {
+#pragma unroll 2
       for (int r = 0; r < TB; ++r) {
-        const double diag = sG[r * (TB + 1) + r];
+        const double dinv = sD[r];
         const double g0 = sG[r * (TB + 1) + lane];        // G[lane][r]
         const double g1 = sG[r * (TB + 1) + lane + 32];   // G[lane+32][r]
         const int src = r & 31;
+        const bool hi = r >= 32;
 #pragma unroll
         for (int q = 0; q < CPW; ++q) {
-          double mine = (r < 32) ? v0[q] : v1[q];
-          double yr = __shfl_sync(0xffffffffu, mine, src) / diag;
-          if (lane == src) { if (r < 32) v0[q] = yr; else v1[q] = yr; }
-          if (lane > r) v0[q] -= g0 * yr;
-          if (lane + 32 > r) v1[q] -= g1 * yr;
+          double mine = hi ? v1[q] : v0[q];
+          double yr = __shfl_sync(0xffffffffu, mine, src) * dinv;
+          if (lane == src) { if (hi) v1[q] = yr; else v0[q] = yr; }
+          if (lane > r) v0[q] = fma(-g0, yr, v0[q]);
+          if (lane + 32 > r) v1[q] = fma(-g1, yr, v1[q]);
         }
       }
     } else {
+#pragma unroll 2
       for (int r = TB - 1; r >= 0; --r) {
-        const double diag = sG[r * (TB + 1) + r];
+        const double dinv = sD[r];
         const double g0 = sG[r * (TB + 1) + lane];        // U[lane][r]
         const double g1 = sG[r * (TB + 1) + lane + 32];
         const int src = r & 31;
+        const bool hi = r >= 32;
 #pragma unroll
         for (int q = 0; q < CPW; ++q) {
-          double mine = (r < 32) ? v0[q] : v1[q];
-          double yr = __shfl_sync(0xffffffffu, mine, src) / diag;
-          if (lane == src) { if (r < 32) v0[q] = yr; else v1[q] = yr; }
-          if (lane < r) v0[q] -= g0 * yr;
-          if (lane + 32 < r) v1[q] -= g1 * yr;
+          double mine = hi ? v1[q] : v0[q];
+          double yr = __shfl_sync(0xffffffffu, mine, src) * dinv;
+          if (lane == src) { if (hi) v1[q] = yr; else v0[q] = yr; }
+          if (lane < r) v0[q] = fma(-g0, yr, v0[q]);
+          if (lane + 32 < r) v1[q] = fma(-g1, yr, v1[q]);
         }
       }
     }
@@ -150,56 +155,107 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
 }
 
 template <int NB, bool UPPER>
-static void run(Ctx &c, const TrsmLaunch &L, int panels, bool v16) {
+static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   using C = TrsmCfg<NB>;
-  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + TB * (TB + 1)) * sizeof(double);
+  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + TB * (TB + 1) + TB) * sizeof(double);
   auto kern = v16 ? k_trsm<NB, UPPER, true> : k_trsm<NB, UPPER, false>;
   static bool attr[2] = {false, false};
   if (!attr[v16]) {
     WF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr[v16] = true;
   }
-  kern<<<panels, 128, smem, c.st>>>(L);
+  kern<<<dim3(panels, nseg), 128, smem, c.st>>>(L);
   WF_CUDA(cudaGetLastError());
 }
 
-void launch_trsm(Ctx &c, const TrsmProb *probs, int nprob, bool upper) {
+// one k_trsm launch over segments [seg_lo + j*seg_len ...) of every problem
+static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int seg_lo,
+                          int seg_len, int seg_hi) {
   TrsmLaunch L{};
-  int total_cols = 0, valid = 0;
+  int total_cols = 0;
+  bool v16 = (seg_len % 2 == 0) && (seg_lo % 2 == 0);
   double flops = 0, bytes = 0;
-  bool v16 = true;
-  for (int i = 0; i < nprob; ++i) {
-    if (probs[i].ncols <= 0 || probs[i].n <= 0) continue;
-    L.p[valid++] = probs[i];
+  const int nseg = (seg_hi - seg_lo + seg_len - 1) / seg_len;
+  // algorithmic work: each segment of length l is a triangle of l^2/2 FMAs per column
+  const int last = seg_hi - seg_lo - (nseg - 1) * seg_len;
+  const double tri = (double)(nseg - 1) * seg_len * seg_len + (double)last * last;
+  for (int i = 0; i < np; ++i) {
+    L.p[i] = probs[i];
     total_cols += probs[i].ncols;
-    double tri = (double)probs[i].n * probs[i].n;
-    if (probs[i].blk > 0) tri = (double)probs[i].n * probs[i].blk;
-    flops += tri * probs[i].ncols;   // n^2 * ncols multiply-adds / 2 * 2
-    bytes += 8.0 * (tri / 2 + 2.0 * probs[i].n * probs[i].ncols);
+    double rows = seg_hi - seg_lo;
+    flops += tri * probs[i].ncols;
+    bytes += 8.0 * (tri / 2 + 2.0 * rows * probs[i].ncols);
     v16 = v16 && ((uintptr_t)probs[i].G % 16 == 0) && ((uintptr_t)probs[i].Y % 16 == 0) &&
           (probs[i].ldg % 2 == 0) && (probs[i].ldy % 2 == 0);
   }
-  if (!valid) return;
-  // panel width: as wide as possible while still giving >= ~1 CTA per SM
+  L.seg_lo = seg_lo; L.seg_len = seg_len; L.seg_hi = seg_hi;
+  // panel width: as wide as possible while still filling the SMs
+  const int ctas_per_col = nseg;
   int NB = 64;
-  if ((total_cols + 63) / 64 < 148) NB = 32;
-  if ((total_cols + 31) / 32 < 148) NB = 16;
-  if ((total_cols + 15) / 16 < 148) NB = 8;
+  if ((total_cols + 63) / 64 * ctas_per_col < 148) NB = 32;
+  if ((total_cols + 31) / 32 * ctas_per_col < 148) NB = 16;
+  if ((total_cols + 15) / 16 * ctas_per_col < 148) NB = 8;
   int panels = 0;
-  for (int i = 0; i < valid; ++i) {
+  for (int i = 0; i < np; ++i) {
     int pi = (L.p[i].ncols + NB - 1) / NB;
     if (i == 0) L.panels0 = pi;
     panels += pi;
   }
-  if (valid == 1) L.panels0 = panels;
+  if (np == 1) L.panels0 = panels;
   LaunchScope ls(c, K_TRSM, flops, bytes);
   switch (NB) {
-    case 64: upper ? run<64, true>(c, L, panels, v16) : run<64, false>(c, L, panels, v16); break;
-    case 32: upper ? run<32, true>(c, L, panels, v16) : run<32, false>(c, L, panels, v16); break;
-    case 16: upper ? run<16, true>(c, L, panels, v16) : run<16, false>(c, L, panels, v16); break;
-    default: upper ? run<8, true>(c, L, panels, v16) : run<8, false>(c, L, panels, v16); break;
+    case 64: upper ? run<64, true>(c, L, panels, nseg, v16) : run<64, false>(c, L, panels, nseg, v16); break;
+    case 32: upper ? run<32, true>(c, L, panels, nseg, v16) : run<32, false>(c, L, panels, nseg, v16); break;
+    case 16: upper ? run<16, true>(c, L, panels, nseg, v16) : run<16, false>(c, L, panels, nseg, v16); break;
+    default: upper ? run<8, true>(c, L, panels, nseg, v16) : run<8, false>(c, L, panels, nseg, v16); break;
   }
   c.launches++;
+}
+
+void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
+  TrsmProb probs[2];
+  int np = 0;
+  for (int i = 0; i < nprob; ++i)
+    if (probs_in[i].ncols > 0 && probs_in[i].n > 0) probs[np++] = probs_in[i];
+  if (!np) return;
+  const int n = probs[0].n;
+  const int blk = probs[0].blk;
+  if (blk > 0) {   // block-diagonal factor: independent segments
+    trsm_segments(c, probs, np, upper, 0, blk, n);
+    return;
+  }
+  const int SB = n >= 2048 ? 512 : (n >= 512 ? 256 : 128);
+  if (n <= SB) {
+    trsm_segments(c, probs, np, upper, 0, n, n);
+    return;
+  }
+  const int nsb = (n + SB - 1) / SB;
+  TrsmProb cur[2];
+  for (int i = 0; i < np; ++i) cur[i] = probs[i];
+  for (int it = 0; it < nsb; ++it) {
+    const int kb = upper ? nsb - 1 - it : it;
+    const int lo = kb * SB, hi = std::min(n, lo + SB);
+    trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
+    // couple the solved block to the rest:  Y_rest = Z_rest - G_rest,blk Y_blk
+    const int rlo = upper ? 0 : hi, rhi = upper ? lo : n;
+    if (rhi > rlo) {
+      GemmProb g[2];
+      for (int i = 0; i < np; ++i) {
+        const TrsmProb &P = cur[i];
+        GemmProb &q = g[i];
+        q = GemmProb{};
+        q.A = P.G + (int64_t)rlo * P.ldg + lo; q.lda = P.ldg;
+        q.X = P.Y + (int64_t)lo * P.ldy; q.ldx = P.ldy;
+        q.Y = P.Y + (int64_t)rlo * P.ldy; q.ldy = P.ldy;
+        q.Z = P.X + (int64_t)rlo * P.ldx; q.ldz = P.ldx;
+        q.M = rhi - rlo; q.N = P.ncols; q.K = hi - lo;
+        q.alpha = -1.0; q.beta = 1.0;
+      }
+      launch_gemm(c, g, np, 1);
+    }
+    // after the first coupling every remaining row of Y is initialised: solve in place
+    for (int i = 0; i < np; ++i) { cur[i].X = cur[i].Y; cur[i].ldx = cur[i].ldy; }
+  }
 }
 
 }  // namespace wf

@@ -55,6 +55,11 @@ PROBS = {
     "heat": lambda: SC.custom_problem(s=200, N=6, q=2, m=5, seed0=3),
     # BASELINE.json configs[0]
     "c0": lambda: SC.make_problem(0),
+    # blocked TRSM with several ragged super-blocks (s = 600 > SB = 256), m = 7
+    "mid": lambda: SC.custom_problem(s=600, N=3, q=2, m=7, seed0=5, Bp=(0.05, 1.0),
+                                     Qp=(0.05, 0.1), Rp=(0.03, 0.05)),
+    # BASELINE.json configs[1] at full size
+    "c1": lambda: SC.make_problem(1),
 }
 _cache = {}
 
@@ -73,7 +78,7 @@ CELLS = [dict(shape=s, lhat=l, k=k, rhat=r, block=b, ridge=rd)
 CELLS.append(dict(shape="PD", lhat="LM", k=2, rhat="exact", ridge=0.01))
 
 
-@pytest.mark.parametrize("name", list(PROBS))
+@pytest.mark.parametrize("name", ["dense", "heat", "c0", "mid", "c1"])
 def test_apply_A(name):
     prob, ora = get(name)
     ctx = W4().Context.from_problem(prob, dict(shape="PD", lhat="LM", k=2, rhat="exact"))
@@ -106,6 +111,27 @@ def test_apply_P(name, pc):
         xc = to_paper_order(x, prob.s, prob.p, prob.W, prob.m)[0]
         bwd = np.linalg.norm(P @ yc - xc) / (np.linalg.norm(P, 2) * np.linalg.norm(yc))
         assert bwd <= 1e-14, bwd
+
+
+LARGE_CELLS = [dict(shape="PD", lhat="LM", k=4, rhat="exact"),
+               dict(shape="PI", lhat="LM", k=3, rhat="me"),
+               dict(shape="PD", lhat="LI", k=1, rhat="block", block=50),
+               dict(shape="PI", lhat="L0", k=1, rhat="diag"),
+               dict(shape="PD", lhat="L", k=1, rhat="rr", ridge=0.01)]
+
+
+@pytest.mark.parametrize("name", ["mid", "c1"])
+@pytest.mark.parametrize("pc", LARGE_CELLS, ids=lambda p: f"{p['shape']}-{p['lhat']}{p['k']}-{p['rhat']}")
+def test_apply_P_large(name, pc):
+    prob, ora = get(name)
+    ctx = W4().Context.from_problem(prob, pc)
+    x = seeded_vec(prob.n, 21)
+    y = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    ctx.apply_P(dev(x), y)
+    torch.cuda.synchronize()
+    errs = rel_err_cols(y.cpu().numpy(), ora.apply_P(pc, x), prob)
+    tol = max(1e-12, 50 * kappa_bound(prob, pc) * U)
+    assert max(errs.values()) <= tol, (errs, tol)
 
 
 def test_apply_AP_and_host_path_agree():
