@@ -103,17 +103,29 @@ __device__ __forceinline__ void mma_stage(const double *sA, const double *sB,
                                           double (&acc)[C::FM][C::FN][2], int wm, int wn,
                                           int lane) {
   const int g = lane >> 2, t = lane & 3;
+  // fragments are double-buffered in registers: the shared-memory loads of step
+  // kk+4 are issued before the DMMAs of step kk, hiding the LDS latency (ncu r01:
+  // the tensor pipe idled on LDS->DMMA dependencies with single buffering)
+  double a[2][C::FM], b[2][C::FN];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) a[0][i] = sA[(wm * C::WM + i * 8 + g) * C::LDA + t];
+#pragma unroll
+  for (int j = 0; j < C::FN; ++j) b[0][j] = sB[t * C::LDB + wn * C::WN + j * 8 + g];
 #pragma unroll
   for (int kk = 0; kk < C::BK; kk += 4) {
-    double a[C::FM], b[C::FN];
+    const int cur = (kk >> 2) & 1;
+    if (kk + 4 < C::BK) {
 #pragma unroll
-    for (int i = 0; i < C::FM; ++i) a[i] = sA[(wm * C::WM + i * 8 + g) * C::LDA + kk + t];
+      for (int i = 0; i < C::FM; ++i)
+        a[cur ^ 1][i] = sA[(wm * C::WM + i * 8 + g) * C::LDA + kk + 4 + t];
 #pragma unroll
-    for (int j = 0; j < C::FN; ++j) b[j] = sB[(kk + t) * C::LDB + wn * C::WN + j * 8 + g];
+      for (int j = 0; j < C::FN; ++j)
+        b[cur ^ 1][j] = sB[(kk + 4 + t) * C::LDB + wn * C::WN + j * 8 + g];
+    }
 #pragma unroll
     for (int i = 0; i < C::FM; ++i)
 #pragma unroll
-      for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
   }
 }
 
