@@ -259,3 +259,38 @@ class Context:
     @property
     def launch_count(self):
         return int(_lib.wf4dvar_launch_count(self._h))
+
+
+# ------------------------------------------------ kernel test hooks (wf4dvar_testing.h)
+_lib.wf4dvar_test_gemm.restype = C.c_int
+_lib.wf4dvar_test_gemm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int64,
+                                   C.c_void_p, C.c_int64, C.c_double, C.c_void_p, C.c_int64,
+                                   C.c_void_p, C.c_int64, C.c_void_p]
+_lib.wf4dvar_test_trsm.restype = C.c_int
+_lib.wf4dvar_test_trsm.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+TEST_EXPORTED = ("wf4dvar_test_gemm", "wf4dvar_test_trsm")
+
+
+def test_gemm(A, X, Y, alpha=1.0, beta=0.0, Z=None, stream=None):
+    """Y = alpha A X + beta Z on torch float64 CUDA matrices (row-major, may be strided views)."""
+    M, K = A.shape
+    N = X.shape[1]
+    st = _lib.wf4dvar_test_gemm(M, N, K, alpha, C.c_void_p(A.data_ptr()), A.stride(0),
+                                C.c_void_p(X.data_ptr()), X.stride(0), beta,
+                                C.c_void_p(Z.data_ptr()) if Z is not None else None,
+                                Z.stride(0) if Z is not None else 0,
+                                C.c_void_p(Y.data_ptr()), Y.stride(0),
+                                C.c_void_p(stream) if stream else None)
+    if st:
+        raise WF4DVarError(st, "wf4dvar_test_gemm")
+
+
+def test_trsm(G, X, Y, upper=False, blk=0, stream=None):
+    """Y = G^{-1} X (lower) or U^{-1} X (upper) for contiguous torch float64 CUDA tensors."""
+    n, ncols = X.shape
+    st = _lib.wf4dvar_test_trsm(n, ncols, 1 if upper else 0, blk, C.c_void_p(G.data_ptr()),
+                                C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()),
+                                C.c_void_p(stream) if stream else None)
+    if st:
+        raise WF4DVarError(st, "wf4dvar_test_trsm")

@@ -282,3 +282,37 @@ const char *wf4dvar_last_error(wf4dvar_ctx ctx) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- test hooks
+#include "../../include/wf4dvar_testing.h"
+
+extern "C" int wf4dvar_test_gemm(int M, int N, int K, double alpha, const double *A, int64_t lda,
+                                 const double *X, int64_t ldx, double beta, const double *Z,
+                                 int64_t ldz, double *Y, int64_t ldy, void *stream) {
+  if (M < 0 || N < 0 || K < 0 || !A || !X || !Y) return WF4DVAR_EINVAL;
+  try {
+    Ctx c;
+    c.st = (cudaStream_t)stream;
+    wf::GemmProb g{};
+    g.A = A; g.lda = lda; g.X = X; g.ldx = ldx; g.Y = Y; g.ldy = ldy; g.Z = Z; g.ldz = ldz;
+    g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = Z ? beta : 0.0;
+    wf::launch_gemm(c, &g, 1, 1);
+  } catch (const Error &e) {
+    return e.st;
+  }
+  return 0;
+}
+
+extern "C" int wf4dvar_test_trsm(int n, int ncols, int upper, int blk, const double *G,
+                                 const double *X, double *Y, void *stream) {
+  if (n <= 0 || ncols <= 0 || !G || !X || !Y || blk < 0) return WF4DVAR_EINVAL;
+  try {
+    Ctx c;
+    c.st = (cudaStream_t)stream;
+    wf::TrsmProb p{G, n, X, ncols, Y, ncols, n, ncols, blk};
+    wf::launch_trsm(c, &p, 1, upper != 0);
+  } catch (const Error &e) {
+    return e.st;
+  }
+  return 0;
+}

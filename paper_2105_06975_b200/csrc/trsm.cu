@@ -86,17 +86,22 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
           sT[rr * (NB + 1) + cc] = xv - acc[i][j][h];
         }
     }
-    // ---- diagonal tile, transposed: sG[c][r] = G[r0 + r][r0 + c]; identity padding
+    // ---- diagonal tile, transposed and masked:
+    //   sG[c][r] = G[r0 + r][r0 + c] for r strictly below (lower) / above (upper) c, else 0;
+    //   sD[r] = 1 / G[r0 + r][r0 + r]   (identity padding of a ragged last tile).
+    // Consecutive threads read consecutive columns of one row (coalesced).
     for (int e = tid; e < TB * TB; e += 128) {
-      int cc = e / TB, r = e % TB;   // consecutive threads -> consecutive r (conflict-free stores)
-      double v;
+      int r = e / TB, cc = e % TB;
+      double v = 0.0;
       if (r < nr && cc < nr) v = G[(int64_t)(r0 + r) * P.ldg + r0 + cc];
-      else v = (r == cc) ? 1.0 : 0.0;
-      sG[cc * (TB + 1) + r] = v;
-      if (r == cc) sD[r] = 1.0 / v;
+      if (r == cc) sD[r] = (r < nr) ? 1.0 / v : 1.0;
+      bool keep = UPPER ? (r < cc) : (r > cc);
+      sG[cc * (TB + 1) + r] = keep ? v : 0.0;
     }
     __syncthreads();
-    // ---- substitution: warp w solves columns w, w+4, ...; lane holds rows lane, lane+32
+    // ---- substitution: warp w solves columns w, w+4, ...; lane holds rows lane, lane+32.
+    // Step r: y_r = t_r / G_rr (owner lane, broadcast by shuffle), then every lane
+    // t_l -= G_lr y_r with the masked column (zeros where l is not below r).
     constexpr int CPW = NB / 4;
     double v0[CPW], v1[CPW];
 #pragma unroll
@@ -105,40 +110,34 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
       v0[q] = sT[lane * (NB + 1) + cc];
       v1[q] = sT[(lane + 32) * (NB + 1) + cc];
     }
+    auto step = [&](int r, auto hi_tag) {
+      constexpr bool HI = decltype(hi_tag)::value;
+      const double dinv = sD[r];
+      const double g0 = sG[r * (TB + 1) + lane];
+      const double g1 = sG[r * (TB + 1) + lane + 32];
+      const int src = r & 31;
+#pragma unroll
+      for (int q = 0; q < CPW; ++q) {
+        const double yr = __shfl_sync(0xffffffffu, HI ? v1[q] : v0[q], src) * dinv;
+        if (HI) {
+          v1[q] = (lane == src) ? yr : fma(-g1, yr, v1[q]);
+          if (UPPER) v0[q] = fma(-g0, yr, v0[q]);
+        } else {
+          v0[q] = (lane == src) ? yr : fma(-g0, yr, v0[q]);
+          if (!UPPER) v1[q] = fma(-g1, yr, v1[q]);
+        }
+      }
+    };
     if (!UPPER) {
-#pragma unroll 2
-      for (int r = 0; r < TB; ++r) {
-        const double dinv = sD[r];
-        const double g0 = sG[r * (TB + 1) + lane];        // G[lane][r]
-        const double g1 = sG[r * (TB + 1) + lane + 32];   // G[lane+32][r]
-        const int src = r & 31;
-        const bool hi = r >= 32;
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) {
-          double mine = hi ? v1[q] : v0[q];
-          double yr = __shfl_sync(0xffffffffu, mine, src) * dinv;
-          if (lane == src) { if (hi) v1[q] = yr; else v0[q] = yr; }
-          if (lane > r) v0[q] = fma(-g0, yr, v0[q]);
-          if (lane + 32 > r) v1[q] = fma(-g1, yr, v1[q]);
-        }
-      }
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) step(r, std::false_type{});
+#pragma unroll 4
+      for (int r = 32; r < TB; ++r) step(r, std::true_type{});
     } else {
-#pragma unroll 2
-      for (int r = TB - 1; r >= 0; --r) {
-        const double dinv = sD[r];
-        const double g0 = sG[r * (TB + 1) + lane];        // U[lane][r]
-        const double g1 = sG[r * (TB + 1) + lane + 32];
-        const int src = r & 31;
-        const bool hi = r >= 32;
-#pragma unroll
-        for (int q = 0; q < CPW; ++q) {
-          double mine = hi ? v1[q] : v0[q];
-          double yr = __shfl_sync(0xffffffffu, mine, src) * dinv;
-          if (lane == src) { if (hi) v1[q] = yr; else v0[q] = yr; }
-          if (lane < r) v0[q] = fma(-g0, yr, v0[q]);
-          if (lane + 32 < r) v1[q] = fma(-g1, yr, v1[q]);
-        }
-      }
+#pragma unroll 4
+      for (int r = TB - 1; r >= 32; --r) step(r, std::true_type{});
+#pragma unroll 4
+      for (int r = 31; r >= 0; --r) step(r, std::false_type{});
     }
     // ---- store Y rows of this tile
 #pragma unroll

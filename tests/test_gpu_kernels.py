@@ -1,0 +1,77 @@
+"""Kernel-level parity of the FP64 tensor-core building blocks (through the
+wf4dvar_testing.h hooks) against plain float64 references: torch matmul and a
+triangular solve.  Sizes span several tiles and ragged tails."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def L():
+    from paper_2105_06975_b200 import _lib
+    return _lib
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 19, 5), (128, 128, 32), (300, 517, 129),
+                                   (1000, 336, 1000), (64, 8128, 512)])
+@pytest.mark.parametrize("with_z", [False, True])
+def test_gemm_vs_float64_reference(M, N, K, with_z):
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g, dtype=torch.float64).cuda()
+    X = torch.randn(K, N, generator=g, dtype=torch.float64).cuda()
+    Z = torch.randn(M, N, generator=g, dtype=torch.float64).cuda() if with_z else None
+    Y = torch.empty(M, N, dtype=torch.float64, device="cuda")
+    L().test_gemm(A, X, Y, alpha=-0.5, beta=2.0, Z=Z)
+    ref = -0.5 * (A.cpu() @ X.cpu()) + (2.0 * Z.cpu() if with_z else 0.0)
+    err = (Y.cpu() - ref).abs().max().item()
+    scale = (A.cpu().abs() @ X.cpu().abs()).max().item() + 1.0
+    assert err <= 1e-14 * scale * max(1, K) ** 0.5 * 4, err
+
+
+def test_gemm_strided_views_and_odd_ld():
+    # odd leading dimensions force the 8-byte cp.async path
+    A = torch.randn(51, 77, dtype=torch.float64, device="cuda")[:, :33]
+    X = torch.randn(33, 45, dtype=torch.float64, device="cuda")[:, 1:44]
+    Y = torch.zeros(51, 43, dtype=torch.float64, device="cuda")
+    L().test_gemm(A, X, Y)
+    torch.testing.assert_close(Y, A @ X, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("n,ncols,blk", [(5, 3, 0), (64, 64, 0), (130, 17, 0), (600, 40, 0),
+                                         (1000, 336, 0), (2048, 96, 0), (500, 21, 50),
+                                         (256, 64, 64)])
+@pytest.mark.parametrize("upper", [False, True])
+def test_trsm_vs_float64_reference(n, ncols, blk, upper):
+    g = torch.Generator().manual_seed(n + ncols + blk)
+    M = torch.randn(n, n, generator=g, dtype=torch.float64)
+    S = M @ M.T / n + torch.eye(n, dtype=torch.float64)
+    if blk:
+        mask = torch.zeros(n, n, dtype=torch.bool)
+        for a in range(0, n, blk):
+            mask[a:a + blk, a:a + blk] = True
+        S = torch.where(mask, S, torch.zeros_like(S))
+    Gl = torch.linalg.cholesky(S)
+    F = (Gl.T if upper else Gl).contiguous()
+    X = torch.randn(n, ncols, generator=g, dtype=torch.float64)
+    Y = torch.empty(n, ncols, dtype=torch.float64, device="cuda")
+    L().test_trsm(F.cuda(), X.cuda(), Y, upper=upper, blk=blk)
+    Yc = Y.cpu()
+    ref = torch.linalg.solve_triangular(F, X, upper=upper)
+    # backward error of the triangular solve (implementation independent)
+    bwd = ((F @ Yc - X).norm() / (F.norm() * Yc.norm())).item()
+    assert bwd <= 1e-15 * 4, bwd
+    fwd = ((Yc - ref).norm() / ref.norm()).item()
+    assert fwd <= 1e-12, fwd
+
+
+def test_trsm_in_place():
+    n, ncols = 700, 50
+    S = torch.randn(n, n, dtype=torch.float64)
+    S = S @ S.T / n + torch.eye(n, dtype=torch.float64)
+    G = torch.linalg.cholesky(S)
+    X = torch.randn(n, ncols, dtype=torch.float64)
+    Yd = X.clone().cuda()
+    L().test_trsm(G.cuda(), Yd, Yd, upper=False)
+    torch.testing.assert_close(Yd.cpu(), torch.linalg.solve_triangular(G, X, upper=False),
+                               rtol=1e-12, atol=1e-12)
