@@ -289,6 +289,7 @@ def test_gemm(A, X, Y, alpha=1.0, beta=0.0, Z=None, stream=None):
 def test_trsm(G, X, Y, upper=False, blk=0, stream=None):
     """Y = G^{-1} X (lower) or U^{-1} X (upper) for contiguous torch float64 CUDA tensors."""
     n, ncols = X.shape
+    assert G.is_contiguous() and X.is_contiguous() and Y.is_contiguous(), "row-major contiguous"
     st = _lib.wf4dvar_test_trsm(n, ncols, 1 if upper else 0, blk, C.c_void_p(G.data_ptr()),
                                 C.c_void_p(X.data_ptr()), C.c_void_p(Y.data_ptr()),
                                 C.c_void_p(stream) if stream else None)

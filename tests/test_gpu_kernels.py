@@ -55,7 +55,9 @@ def test_trsm_vs_float64_reference(n, ncols, blk, upper):
     F = (Gl.T if upper else Gl).contiguous()
     X = torch.randn(n, ncols, generator=g, dtype=torch.float64)
     Y = torch.empty(n, ncols, dtype=torch.float64, device="cuda")
-    L().test_trsm(F.cuda(), X.cuda(), Y, upper=upper, blk=blk)
+    Fd, Xd = F.cuda(), X.cuda()
+    L().test_trsm(Fd, Xd, Y, upper=upper, blk=blk)
+    torch.cuda.synchronize()
     Yc = Y.cpu()
     ref = torch.linalg.solve_triangular(F, X, upper=upper)
     # backward error of the triangular solve (implementation independent)
@@ -69,9 +71,11 @@ def test_trsm_in_place():
     n, ncols = 700, 50
     S = torch.randn(n, n, dtype=torch.float64)
     S = S @ S.T / n + torch.eye(n, dtype=torch.float64)
-    G = torch.linalg.cholesky(S)
+    G = torch.linalg.cholesky(S).contiguous()   # LAPACK returns Fortran strides
     X = torch.randn(n, ncols, dtype=torch.float64)
     Yd = X.clone().cuda()
-    L().test_trsm(G.cuda(), Yd, Yd, upper=False)
+    Gd = G.cuda()
+    L().test_trsm(Gd, Yd, Yd, upper=False)
+    torch.cuda.synchronize()
     torch.testing.assert_close(Yd.cpu(), torch.linalg.solve_triangular(G, X, upper=False),
                                rtol=1e-12, atol=1e-12)
