@@ -4,6 +4,8 @@
 // D x1 (B on window-0 columns, Q on the rest -- two groups in one launch),
 // R x2 + H x3 (the H gather is the zrow epilogue), D c1 inside S_hat^{-1} and
 // P_I, and dense-M_w model products (batched over windows).
+#include <cstdlib>
+
 #include "dmma.cuh"
 #include "internal.h"
 
@@ -72,6 +74,10 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
 // warp per k-step (hides the DMMA result latency; ncu r01 showed "wait" stalls
 // dominating the 32x32 warp tile), BK = 32 halves the barriers per FLOP.
 using CfgHuge = TileCfg<128, 128, 32, 64, 32, 3>;
+// 16 warps of 32x32 (4 per SMSP): more warps to hide LDS->DMMA latency
+using CfgWide = TileCfg<128, 128, 32, 32, 32, 3>;
+// 256x128, 16 warps of 64x32
+using CfgTall = TileCfg<256, 128, 16, 64, 32, 3>;
 using CfgBig = TileCfg<128, 64, 16, 32, 32, 4>;
 using CfgSmall = TileCfg<64, 32, 16, 32, 16, 4>;
 
@@ -138,7 +144,16 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
   }
   if (flops_hint >= 0) flops = flops_hint;
   LaunchScope ls(c, K_GEMM, flops, bytes);
-  if (huge_tiles * batch >= 2 * 148) run<CfgHuge>(c, ps, valid, batch, v16);
+  static int force = -2;
+  if (force == -2) {
+    const char *e = getenv("WF4DVAR_GEMM_CFG");   // tuning experiments only
+    force = e ? atoi(e) : -1;
+  }
+  if (force >= 0 && huge_tiles * batch >= 2 * 148) {
+    if (force == 1) run<CfgWide>(c, ps, valid, batch, v16);
+    else if (force == 2) run<CfgTall>(c, ps, valid, batch, v16);
+    else run<CfgHuge>(c, ps, valid, batch, v16);
+  } else if (huge_tiles * batch >= 2 * 148) run<CfgHuge>(c, ps, valid, batch, v16);
   else if (big_tiles * batch >= 148) run<CfgBig>(c, ps, valid, batch, v16);
   else run<CfgSmall>(c, ps, valid, batch, v16);
   c.launches++;
