@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
 using CfgHuge = TileCfg<128, 128, 32, 64, 32, 3>;
 // 16 warps of 32x32 (4 per SMSP): more warps to hide LDS->DMMA latency
 using CfgWide = TileCfg<128, 128, 32, 32, 32, 3>;
-// 256x128, 16 warps of 64x32
-using CfgTall = TileCfg<256, 128, 16, 64, 32, 3>;
+
+
 using CfgBig = TileCfg<128, 64, 16, 32, 32, 4>;
 using CfgSmall = TileCfg<64, 32, 16, 32, 16, 4>;
 
@@ -151,7 +151,10 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
   }
   if (force >= 0 && huge_tiles * batch >= 2 * 148) {
     if (force == 1) run<CfgWide>(c, ps, valid, batch, v16);
-    else if (force == 2) run<CfgTall>(c, ps, valid, batch, v16);
+    else if (force == 3) run<TileCfg<64, 128, 16, 32, 64, 3>>(c, ps, valid, batch, v16);
+    else if (force == 4) run<TileCfg<128, 128, 16, 64, 32, 4>>(c, ps, valid, batch, v16);
+    else if (force == 5) run<TileCfg<64, 128, 16, 32, 64, 4>>(c, ps, valid, batch, v16);
+    else if (force == 6) run<TileCfg<128, 64, 16, 64, 32, 3>>(c, ps, valid, batch, v16);
     else run<CfgHuge>(c, ps, valid, batch, v16);
   } else if (huge_tiles * batch >= 2 * 148) run<CfgHuge>(c, ps, valid, batch, v16);
   else if (big_tiles * batch >= 148) run<CfgBig>(c, ps, valid, batch, v16);
