@@ -70,10 +70,12 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
   }
 }
 
-// 128x128 CTA tile, 8 warps of 64x32: 32 independent DMMA accumulator tiles per
-// warp per k-step (hides the DMMA result latency; ncu r01 showed "wait" stalls
-// dominating the 32x32 warp tile), BK = 32 halves the barriers per FLOP.
-using CfgHuge = TileCfg<128, 128, 32, 64, 32, 3>;
+// Large problems: 64x128 CTA tile, 4 warps of 32x64 (32 independent DMMA
+// accumulator tiles per warp per k-step), BK = 16, 3-stage cp.async ring,
+// 81 KB smem -> 2 CTAs (8 warps) per SM.  Chosen by measurement (tools/kbench.py,
+// r01): 32.5 TFLOP/s at 4096x8128x4096 = 90% of cuBLAS DGEMM on the same box,
+// vs 30.2 for 128x128/8x(64x32) and 28.7 for 128x128/8x(32x64).
+using CfgHuge = TileCfg<64, 128, 16, 32, 64, 3>;
 // 16 warps of 32x32 (4 per SMSP): more warps to hide LDS->DMMA latency
 using CfgWide = TileCfg<128, 128, 32, 32, 32, 3>;
 
@@ -155,6 +157,10 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
     else if (force == 4) run<TileCfg<128, 128, 16, 64, 32, 4>>(c, ps, valid, batch, v16);
     else if (force == 5) run<TileCfg<64, 128, 16, 32, 64, 4>>(c, ps, valid, batch, v16);
     else if (force == 6) run<TileCfg<128, 64, 16, 64, 32, 3>>(c, ps, valid, batch, v16);
+    else if (force == 7) run<TileCfg<64, 128, 16, 32, 64, 2>>(c, ps, valid, batch, v16);
+    else if (force == 8) run<TileCfg<64, 256, 16, 32, 64, 3>>(c, ps, valid, batch, v16);
+    else if (force == 9) run<TileCfg<128, 128, 16, 32, 64, 3>>(c, ps, valid, batch, v16);
+    else if (force == 10) run<TileCfg<64, 128, 32, 32, 64, 2>>(c, ps, valid, batch, v16);
     else run<CfgHuge>(c, ps, valid, batch, v16);
   } else if (huge_tiles * batch >= 2 * 148) run<CfgHuge>(c, ps, valid, batch, v16);
   else if (big_tiles * batch >= 148) run<CfgBig>(c, ps, valid, batch, v16);
