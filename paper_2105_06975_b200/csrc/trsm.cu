@@ -14,6 +14,7 @@
 // R_block (Alg. 1 with uniform blocks) has a block-diagonal factor: every
 // diagonal block is an independent segment (grid.y), no GEMM coupling.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "dmma.cuh"
@@ -22,10 +23,12 @@
 namespace wf {
 
 constexpr int TB = 64;  // rows per triangle tile
+// The in-panel GEMMs are short (K < SB) and latency bound: a 4-deep cp.async ring.
+#define TRSM_STAGES 4
 
 template <int NB>
-using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, 3>,
-                                          TileCfg<64, NB, 16, 32, NB / 2, 3>>::type;
+using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, TRSM_STAGES>,
+                                          TileCfg<64, NB, 16, 32, NB / 2, TRSM_STAGES>>::type;
 
 struct TrsmLaunch {
   TrsmProb p[2];
@@ -223,7 +226,12 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     trsm_segments(c, probs, np, upper, 0, blk, n);
     return;
   }
-  const int SB = n >= 2048 ? 512 : (n >= 512 ? 256 : 128);
+  static int sb_env = -1;
+  if (sb_env < 0) {
+    const char *e = getenv("WF4DVAR_TRSM_SB");   // tuning experiments only
+    sb_env = e ? atoi(e) : 0;
+  }
+  const int SB = sb_env > 0 ? sb_env : (n >= 512 ? 256 : 128);
   if (n <= SB) {
     trsm_segments(c, probs, np, upper, 0, n, n);
     return;
