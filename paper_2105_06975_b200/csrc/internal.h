@@ -181,6 +181,11 @@ void model_step(Ctx &c, bool transpose, double sign, const double *in, const dou
                 double *out, int w_first, int w_step, int nw, const double *add2 = nullptr,
                 const int *row_map = nullptr);
 
+// Lorenz-96 tangent-linear / adjoint window step (same contract as model_step).
+void l96_step(Ctx &c, bool transpose, double sign, const double *in, const double *base,
+              double *out, int w_first, int w_step, int nw, const double *add2,
+              const int *row_map);
+
 // L-hat^{-1} (forward chains) / L-hat^{-T} (backward chains) in place on z.
 void lhat_solve(Ctx &c, bool transpose, double *z);
 

@@ -1,2 +1,231 @@
-// Lorenz-96 tangent-linear / adjoint kernels (filled in with the c2 path).
+// Lorenz-96 tangent-linear model M_w and its adjoint M_w^T (BJ.c2), matrix-free.
+//
+// dx_i/dt = (x_{i+1} - x_{i-2}) x_{i-1} - x_i + F, periodic,
+// RK4; BJ.c2: dt = 0.025, 5 RK4 substeps per window.  M_w is the exact derivative
+// of the discrete map (nsub RK4 steps) along the trajectory that starts at
+// traj[w-1] ("exact derivative of the discrete RK4 map"); the
+// nonlinear stages are recomputed on the fly (no M_w is ever stored: 40x40x50x1024
+// doubles would be 655 MB per pass).
+//
+//   J(x) u : (J u)_i   = (u_{i+1} - u_{i-2}) x_{i-1} + (x_{i+1} - x_{i-2}) u_{i-1} - u_i
+//   J^T l  : (J^T l)_j = x_{j-2} l_{j-1} - x_{j+1} l_{j+2} + (x_{j+2} - x_{j-1}) l_{j+1} - l_j
+//   RK4 tangent:  d1 = J(x1) v, d2 = J(x2)(v + h/2 d1), d3 = J(x3)(v + h/2 d2),
+//                 d4 = J(x4)(v + h d3),  v' = v + h/6 (d1 + 2 d2 + 2 d3 + d4)
+//   adjoint (reverse of the above, stages recomputed from the substep start state).
+//
+// Layout: one CTA = 32 problems (RHS columns, the fastest index -> coalesced) x
+// 8 thread rows; thread row ty owns state indices ty, ty+8, ...; periodic
+// neighbours are exchanged through shared memory.  FP64 ALU bound.
 #include "internal.h"
+
+namespace wf {
+
+template <int IPT>
+struct L96Thread {
+  static constexpr int S_MAX = 8 * IPT;
+};
+
+struct L96Args {
+  double *out;
+  const double *base, *in, *traj, *add2;
+  const int *row_map;
+  double sign, F, dt;
+  int s, W, m, nsub, w_first, w_step, nw, dir;
+};
+
+template <int IPT>
+__device__ __forceinline__ void l96_rhs(const double (&x)[IPT], double (&f)[IPT], double *bx,
+                                        int s, int ty, int lane, double F) {
+  // bx: [S_MAX][32] exchange buffer
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    int i = ty + 8 * k;
+    if (i < s) bx[i * 32 + lane] = x[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    int i = ty + 8 * k;
+    if (i < s) {
+      int ip = i + 1 == s ? 0 : i + 1, im1 = i == 0 ? s - 1 : i - 1, im2 = i >= 2 ? i - 2 : i - 2 + s;
+      f[k] = (bx[ip * 32 + lane] - bx[im2 * 32 + lane]) * bx[im1 * 32 + lane] - x[k] + F;
+    }
+  }
+  __syncthreads();
+}
+
+// Ju = J(x) u, with x already resident in bx (written by l96_rhs of the same stage is
+// not reused: x is re-exchanged together with u for clarity)
+template <int IPT>
+__device__ __forceinline__ void l96_jac(const double (&x)[IPT], const double (&u)[IPT],
+                                        double (&Ju)[IPT], double *bx, double *bu, int s, int ty,
+                                        int lane, bool transpose) {
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    int i = ty + 8 * k;
+    if (i < s) { bx[i * 32 + lane] = x[k]; bu[i * 32 + lane] = u[k]; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    int i = ty + 8 * k;
+    if (i < s) {
+      int ip1 = i + 1 == s ? 0 : i + 1, ip2 = i + 2 >= s ? i + 2 - s : i + 2;
+      int im1 = i == 0 ? s - 1 : i - 1, im2 = i >= 2 ? i - 2 : i - 2 + s;
+      if (!transpose) {
+        Ju[k] = (bu[ip1 * 32 + lane] - bu[im2 * 32 + lane]) * bx[im1 * 32 + lane] +
+                (bx[ip1 * 32 + lane] - bx[im2 * 32 + lane]) * bu[im1 * 32 + lane] - u[k];
+      } else {
+        Ju[k] = bx[im2 * 32 + lane] * bu[im1 * 32 + lane] - bx[ip1 * 32 + lane] * bu[ip2 * 32 + lane] +
+                (bx[ip2 * 32 + lane] - bx[im1 * 32 + lane]) * bu[ip1 * 32 + lane] - u[k];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// nonlinear stage states of one RK4 step from x (x1 = x)
+template <int IPT>
+__device__ __forceinline__ void rk4_stages(const double (&x)[IPT], double (&x2)[IPT],
+                                           double (&x3)[IPT], double (&x4)[IPT],
+                                           double (&xn)[IPT], double *bx, int s, int ty, int lane,
+                                           double F, double h) {
+  double k1[IPT], k2[IPT], k3[IPT], k4[IPT];
+  l96_rhs<IPT>(x, k1, bx, s, ty, lane, F);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) x2[k] = x[k] + 0.5 * h * k1[k];
+  l96_rhs<IPT>(x2, k2, bx, s, ty, lane, F);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) x3[k] = x[k] + 0.5 * h * k2[k];
+  l96_rhs<IPT>(x3, k3, bx, s, ty, lane, F);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) x4[k] = x[k] + h * k3[k];
+  l96_rhs<IPT>(x4, k4, bx, s, ty, lane, F);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) xn[k] = x[k] + (h / 6.0) * (k1[k] + 2.0 * k2[k] + 2.0 * k3[k] + k4[k]);
+}
+
+template <int IPT, int NSUB_MAX>
+__global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
+  __shared__ double bx[L96Thread<IPT>::S_MAX * 32];
+  __shared__ double bu[L96Thread<IPT>::S_MAX * 32];
+  const int lane = threadIdx.x, ty = threadIdx.y;
+  const int r = blockIdx.x * 32 + lane;
+  const int t = blockIdx.y;
+  const int w = a.w_first + t * a.w_step;
+  const int ws = w + a.dir;
+  const bool has = ws >= 0 && ws < a.W;
+  const bool live = r < a.m;
+  const int64_t ld = (int64_t)a.W * a.m;
+  const int s = a.s;
+  const double h = a.dt;
+  double v[IPT];
+  if (has) {
+    // trajectory start state of the window pair: M_w uses traj[w-1], M_{w+1}^T uses traj[w]
+    const int tw = a.dir < 0 ? w - 1 : w;
+    double x[IPT];
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) {
+      int i = ty + 8 * k;
+      x[k] = (live && i < s) ? a.traj[((int64_t)tw * s + i) * a.m + r] : 0.0;
+      v[k] = (live && i < s) ? a.in[i * ld + (int64_t)ws * a.m + r] : 0.0;
+    }
+    if (a.dir < 0) {
+      // forward tangent: nsub RK4 steps
+      for (int st = 0; st < a.nsub; ++st) {
+        double x2[IPT], x3[IPT], x4[IPT], xn[IPT], d1[IPT], d2[IPT], d3[IPT], d4[IPT], u[IPT];
+        rk4_stages<IPT>(x, x2, x3, x4, xn, bx, s, ty, lane, a.F, h);
+        l96_jac<IPT>(x, v, d1, bx, bu, s, ty, lane, false);
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) u[k] = v[k] + 0.5 * h * d1[k];
+        l96_jac<IPT>(x2, u, d2, bx, bu, s, ty, lane, false);
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) u[k] = v[k] + 0.5 * h * d2[k];
+        l96_jac<IPT>(x3, u, d3, bx, bu, s, ty, lane, false);
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) u[k] = v[k] + h * d3[k];
+        l96_jac<IPT>(x4, u, d4, bx, bu, s, ty, lane, false);
+#pragma unroll
+        for (int k = 0; k < IPT; ++k) {
+          v[k] = v[k] + (h / 6.0) * (d1[k] + 2.0 * d2[k] + 2.0 * d3[k] + d4[k]);
+          x[k] = xn[k];
+        }
+      }
+    } else {
+      // adjoint: store the substep start states, then sweep the substeps backwards
+      double xs[NSUB_MAX][IPT];
+#pragma unroll
+      for (int st = 0; st < NSUB_MAX; ++st) {
+        if (st < a.nsub) {
+          double x2[IPT], x3[IPT], x4[IPT], xn[IPT];
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) xs[st][k] = x[k];
+          if (st + 1 < a.nsub) {
+            rk4_stages<IPT>(x, x2, x3, x4, xn, bx, s, ty, lane, a.F, h);
+#pragma unroll
+            for (int k = 0; k < IPT; ++k) x[k] = xn[k];
+          }
+        }
+      }
+#pragma unroll
+      for (int st = NSUB_MAX - 1; st >= 0; --st) {
+        if (st < a.nsub) {
+          double x1[IPT], x2[IPT], x3[IPT], x4[IPT], xn[IPT], lu[IPT], ld1[IPT], ld2[IPT], ld3[IPT];
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) x1[k] = xs[st][k];
+          rk4_stages<IPT>(x1, x2, x3, x4, xn, bx, s, ty, lane, a.F, h);
+          // lambda_d4 = h/6 l ; lambda_u4 = J4^T lambda_d4
+          double lv[IPT], tmp[IPT];
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) { lv[k] = v[k]; tmp[k] = (h / 6.0) * v[k]; }
+          l96_jac<IPT>(x4, tmp, lu, bx, bu, s, ty, lane, true);
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld3[k] = (h / 3.0) * v[k] + h * lu[k]; }
+          l96_jac<IPT>(x3, ld3, lu, bx, bu, s, ty, lane, true);
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld2[k] = (h / 3.0) * v[k] + 0.5 * h * lu[k]; }
+          l96_jac<IPT>(x2, ld2, lu, bx, bu, s, ty, lane, true);
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld1[k] = (h / 6.0) * v[k] + 0.5 * h * lu[k]; }
+          l96_jac<IPT>(x1, ld1, lu, bx, bu, s, ty, lane, true);
+#pragma unroll
+          for (int k = 0; k < IPT; ++k) v[k] = lv[k] + lu[k];
+        }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    int i = ty + 8 * k;
+    if (i < s) {
+      int64_t o = i * ld + (int64_t)w * a.m + r;
+      double val = a.base[o];
+      if (has) val = fma(a.sign, v[k], val);
+      if (a.add2) {
+        int j = a.row_map[i];
+        if (j >= 0) val += a.add2[(int64_t)j * ld + (int64_t)w * a.m + r];
+      }
+      a.out[o] = val;
+    }
+  }
+}
+
+void l96_step(Ctx &c, bool transpose, double sign, const double *in, const double *base, double *out,
+              int w_first, int w_step, int nw, const double *add2, const int *row_map) {
+  L96Args a{};
+  a.out = out; a.base = base; a.in = in; a.traj = c.traj; a.add2 = add2; a.row_map = row_map;
+  a.sign = sign; a.F = c.l96_F; a.dt = c.l96_dt; a.s = c.s; a.W = c.W; a.m = c.m;
+  a.nsub = c.l96_nsub; a.w_first = w_first; a.w_step = w_step; a.nw = nw;
+  a.dir = transpose ? 1 : -1;
+  dim3 grid((c.m + 31) / 32, nw), block(32, 8);
+  // ~ per problem and substep: 4 rhs (5 flops/i) + 4 Jacobian products (~8 flops/i)
+  double flops = (double)nw * c.m * c.l96_nsub * c.s * (transpose ? 4 * 5 * 2 + 4 * 9 : 4 * 5 + 4 * 9);
+  LaunchScope ls(c, K_MODEL, flops, (double)nw * c.m * c.s * 8 * 4);
+  if (c.s <= 40) k_l96_step<5, 8><<<grid, block, 0, c.st>>>(a);
+  else k_l96_step<8, 8><<<grid, block, 0, c.st>>>(a);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
+}
+
+}  // namespace wf

@@ -108,6 +108,10 @@ void model_step(Ctx &c, bool transpose, double sign, const double *in, const dou
   if (nw <= 0) return;
   const int s = c.s, m = c.m;
   const int64_t ld = c.ncol;
+  if (c.model == WF4DVAR_M_L96) {
+    l96_step(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map);
+    return;
+  }
   if (c.model == WF4DVAR_M_HEAT && c.heat_D > 0) {
     double elems = (double)nw * s * m;
     LaunchScope ls(c, K_MODEL, elems * 2.0 * (2 * c.heat_D + 1), elems * 8.0 * 3);
@@ -255,8 +259,17 @@ void setup_model(Ctx &c, const wf4dvar_problem &p) {
       WF_CUDA(cudaMemcpy(c.Mdense + (size_t)w * s * s, Mw, (size_t)s * s * 8, cudaMemcpyHostToDevice));
       WF_CUDA(cudaMemcpy(c.MdenseT + (size_t)w * s * s, Tm.data(), Tm.size() * 8, cudaMemcpyHostToDevice));
     }
+  } else if (c.model == WF4DVAR_M_L96) {
+    WF_REQUIRE(p.l96_traj != nullptr || N == 0, WF4DVAR_EINVAL, "l96_traj is NULL");
+    WF_REQUIRE(s >= 4 && s <= 64, WF4DVAR_EINVAL, "L96 kernel supports 4 <= s <= 64");
+    WF_REQUIRE(p.l96_nsub >= 1 && p.l96_nsub <= 8, WF4DVAR_EINVAL, "L96 needs 1 <= nsub <= 8");
+    WF_REQUIRE(p.l96_dt > 0, WF4DVAR_EINVAL, "L96 dt must be > 0");
+    c.l96_F = p.l96_F; c.l96_dt = p.l96_dt; c.l96_nsub = p.l96_nsub;
+    c.traj = c.alloc<double>((size_t)std::max(N, 1) * s * c.m);
+    if (N > 0)
+      WF_CUDA(cudaMemcpy(c.traj, p.l96_traj, (size_t)N * s * c.m * 8, cudaMemcpyHostToDevice));
   } else {
-    throw Error{WF4DVAR_EINVAL, "model kind not supported in this build"};
+    throw Error{WF4DVAR_EINVAL, "unknown model kind"};
   }
 }
 

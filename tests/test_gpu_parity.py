@@ -60,7 +60,18 @@ PROBS = {
                                      Qp=(0.05, 0.1), Rp=(0.03, 0.05)),
     # BASELINE.json configs[1] at full size
     "c1": lambda: SC.make_problem(1),
+    # Lorenz-96 TLM (configs[2] recipe), 8 problems, N = 12: per-column M_w
+    "l96": lambda: SC.make_problem(2, m=8, N=12),
 }
+
+
+def get_sampled(name, cols):
+    key = (name, tuple(cols))
+    if key not in _cache:
+        prob = {"c2": lambda: SC.make_problem(2), "c3": lambda: SC.make_problem(3),
+                "c4": lambda: SC.make_problem(4)}[name]()
+        _cache[key] = (prob, OracleCols(prob, cols))
+    return _cache[key]
 _cache = {}
 
 
@@ -78,7 +89,7 @@ CELLS = [dict(shape=s, lhat=l, k=k, rhat=r, block=b, ridge=rd)
 CELLS.append(dict(shape="PD", lhat="LM", k=2, rhat="exact", ridge=0.01))
 
 
-@pytest.mark.parametrize("name", ["dense", "heat", "c0", "mid", "c1"])
+@pytest.mark.parametrize("name", ["dense", "heat", "c0", "mid", "c1", "l96"])
 def test_apply_A(name):
     prob, ora = get(name)
     ctx = W4().Context.from_problem(prob, dict(shape="PD", lhat="LM", k=2, rhat="exact"))
@@ -128,6 +139,52 @@ def test_apply_P_large(name, pc):
     x = seeded_vec(prob.n, 21)
     y = torch.empty(prob.n, dtype=torch.float64, device="cuda")
     ctx.apply_P(dev(x), y)
+    torch.cuda.synchronize()
+    errs = rel_err_cols(y.cpu().numpy(), ora.apply_P(pc, x), prob)
+    tol = max(1e-12, 50 * kappa_bound(prob, pc) * U)
+    assert max(errs.values()) <= tol, (errs, tol)
+
+
+L96_CELLS = [dict(shape="PD", lhat="LM", k=3, rhat="exact"),
+             dict(shape="PI", lhat="LM", k=4, rhat="me"),
+             dict(shape="PD", lhat="L", k=1, rhat="rr"),
+             dict(shape="PI", lhat="LI", k=1, rhat="diag")]
+
+
+@pytest.mark.parametrize("pc", L96_CELLS, ids=lambda p: f"{p['shape']}-{p['lhat']}{p['k']}-{p['rhat']}")
+def test_apply_P_l96(pc):
+    prob, ora = get("l96")
+    ctx = W4().Context.from_problem(prob, pc)
+    x = seeded_vec(prob.n, 31)
+    y = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    ctx.apply_P(dev(x), y)
+    torch.cuda.synchronize()
+    errs = rel_err_cols(y.cpu().numpy(), ora.apply_P(pc, x), prob)
+    # exact L^{-1} chains of the L96 TLM amplify rounding (||L^{-1}|| ~ 3e5 at N=50,
+    # SURVEY PROBE-4): scale the tolerance by the growth of the chain products
+    tol = max(1e-12, 50 * kappa_bound(prob, pc) * U)
+    if pc["lhat"] == "L":
+        tol = max(tol, 1e-10)
+    assert max(errs.values()) <= tol, (errs, tol)
+
+
+@pytest.mark.parametrize("name,cols", [("c2", (0, 517, 1023)), ("c3", (37,)), ("c4", (255,))])
+def test_full_size_sampled_columns(name, cols):
+    """BASELINE.json configs at full size, in the bench's launch configuration;
+    the oracle computes the sampled RHS columns one by one."""
+    prob, ora = get_sampled(name, cols)
+    pc = {"c2": dict(shape="PD", lhat="LM", k=4, rhat="exact"),
+          "c3": dict(shape="PD", lhat="LM", k=4, rhat="exact"),
+          "c4": dict(shape="PI", lhat="LM", k=4, rhat="exact")}[name]
+    ctx = W4().Context.from_problem(prob, pc)
+    x = seeded_vec(prob.n, 41)
+    xd = dev(x)
+    y = torch.empty_like(xd)
+    ctx.apply_A(xd, y)
+    torch.cuda.synchronize()
+    errs = rel_err_cols(y.cpu().numpy(), ora.apply_A(x), prob)
+    assert max(errs.values()) <= 1e-12, errs
+    ctx.apply_P(xd, y)
     torch.cuda.synchronize()
     errs = rel_err_cols(y.cpu().numpy(), ora.apply_P(pc, x), prob)
     tol = max(1e-12, 50 * kappa_bound(prob, pc) * U)
