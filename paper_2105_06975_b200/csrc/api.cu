@@ -90,6 +90,11 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       c.st = (cudaStream_t)dist->stream;
     }
     WF_CUDA(cudaSetDevice(c.device));
+    for (int i = 0; i < 2; ++i) {
+      WF_CUDA(cudaStreamCreateWithFlags(&c.aux[i], cudaStreamNonBlocking));
+      WF_CUDA(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
+    }
+    WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     c.s = p.s; c.p = p.p; c.N = p.N; c.W = p.N + 1; c.m = p.m; c.model = p.model;
     c.ncol = (int64_t)c.W * c.m;
     c.n = (int64_t)(2 * c.s + c.p) * c.ncol;
@@ -141,6 +146,11 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   Ctx &c = ctx->c;
   cudaSetDevice(c.device);
   if (c.st) cudaStreamSynchronize(c.st); else cudaDeviceSynchronize();
+  for (int i = 0; i < 2; ++i) {
+    if (c.aux[i]) { cudaStreamSynchronize(c.aux[i]); cudaStreamDestroy(c.aux[i]); }
+    if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
+  }
+  if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   for (void *p : c.allocs) cudaFree(p);
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : c.prof.pool) cudaEventDestroy(e);

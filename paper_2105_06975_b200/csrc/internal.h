@@ -84,6 +84,9 @@ struct Ctx {
   int64_t ncol = 0;   // W*m columns of every segment
   int64_t n = 0;      // (2s+p)*W*m
   cudaStream_t st = nullptr;
+  // fork/join streams: the three independent blocks of A and of P_D run concurrently
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   int device = 0;
   // device data
   double *B = nullptr, *Q = nullptr, *R = nullptr;
@@ -159,6 +162,15 @@ struct Ctx {
   void prof_begin(int cls, double flops, double bytes, cudaEvent_t *ev);
   void prof_end(int cls, cudaEvent_t ev);
 };
+
+// Run the enclosed launches on another stream of the context.
+struct OnStream {
+  Ctx &c; cudaStream_t saved;
+  OnStream(Ctx &c_, cudaStream_t s) : c(c_), saved(c_.st) { c.st = s; }
+  ~OnStream() { c.st = saved; }
+};
+void fork(Ctx &c);   // aux streams wait for the work enqueued so far on c.st
+void join(Ctx &c);   // c.st waits for the aux streams
 
 // RAII helper that brackets one launch with profiling events.
 struct LaunchScope {

@@ -78,19 +78,40 @@ static int n_model_blocks(const Ctx &c) {
   }
 }
 
+void fork(Ctx &c) {
+  WF_CUDA(cudaEventRecord(c.ev_fork, c.st));
+  for (int i = 0; i < 2; ++i) WF_CUDA(cudaStreamWaitEvent(c.aux[i], c.ev_fork, 0));
+}
+
+void join(Ctx &c) {
+  for (int i = 0; i < 2; ++i) {
+    WF_CUDA(cudaEventRecord(c.ev_join[i], c.aux[i]));
+    WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_join[i], 0));
+  }
+}
+
 void apply_A(Ctx &c, const double *x, double *y) {
   const int s = c.s, p = c.p;
   const int64_t ld = c.ncol;
   const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
   double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  // the three output blocks are independent: c2 and c3 run on the aux streams
+  fork(c);
+  {
+    // c2 = R x2 + H x3 (gather in the epilogue)
+    OnStream os(c, c.aux[0]);
+    GemmProb g = gp(c.R, p, x2, ld, y2, ld, x3, ld, p, (int)ld, p, 1.0, 1.0, c.H_idx);
+    launch_gemm(c, &g, 1, 1);
+  }
+  {
+    // c3 = L^T x1 + H^T x2
+    OnStream os(c, c.aux[1]);
+    model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W, x2, c.H_inv);
+  }
   // c1 = L x3 + D x1
   model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
   d_product(c, x1, y1, y1, 1.0, 1.0);
-  // c2 = R x2 + H x3 (gather in the epilogue)
-  GemmProb g = gp(c.R, p, x2, ld, y2, ld, x3, ld, p, (int)ld, p, 1.0, 1.0, c.H_idx);
-  launch_gemm(c, &g, 1, 1);
-  // c3 = L^T x1 + H^T x2
-  model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W, x2, c.H_inv);
+  join(c);
   c.n_R += c.W;
   c.n_M += 2 * c.N;
   c.n_A++;
@@ -101,21 +122,33 @@ void apply_P(Ctx &c, const double *x, double *y) {
   const int64_t ld = c.ncol;
   const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
   double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  fork(c);
   if (c.pc.shape == WF4DVAR_PD) {
+    // three independent blocks: D_hat^{-1} | R_hat^{-1} | S_hat^{-1}
+    {
+      OnStream os(c, c.aux[0]);
+      rhat_inv(c, x2, y2);
+    }
+    {
+      OnStream os(c, c.aux[1]);
+      double *t = c.ws_seg;
+      copy(c, t, x3, (int64_t)s * ld);
+      lhat_solve(c, true, t);                  // L_hat^{-T} x3
+      d_product(c, t, y3, nullptr, 1.0, 0.0);  // D (exact D)
+      lhat_solve(c, false, y3);                // L_hat^{-1}
+    }
     dhat_inv(c, x1, y1);
-    rhat_inv(c, x2, y2);
-    double *t = c.ws_seg;
-    copy(c, t, x3, (int64_t)s * ld);
-    lhat_solve(c, true, t);               // L_hat^{-T} x3
-    d_product(c, t, y3, nullptr, 1.0, 0.0);  // D (exact D)
-    lhat_solve(c, false, y3);             // L_hat^{-1}
   } else {
+    {
+      OnStream os(c, c.aux[0]);
+      rhat_inv(c, x2, y2);                     // c2
+    }
     copy(c, y1, x3, (int64_t)s * ld);
-    lhat_solve(c, true, y1);              // c1 = L_hat^{-T} x3
-    rhat_inv(c, x2, y2);                  // c2
-    d_product(c, y1, y3, x1, -1.0, 1.0);  // x1 - D c1
-    lhat_solve(c, false, y3);             // c3
+    lhat_solve(c, true, y1);                   // c1 = L_hat^{-T} x3
+    d_product(c, y1, y3, x1, -1.0, 1.0);       // x1 - D c1
+    lhat_solve(c, false, y3);                  // c3
   }
+  join(c);
   c.n_M += 2 * n_model_blocks(c);
   c.n_P++;
 }
