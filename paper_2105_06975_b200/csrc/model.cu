@@ -43,17 +43,26 @@ __global__ void __launch_bounds__(128) k_heat_step(double *out, const double *ba
       v[j] = __ldg(in + row * ld + cols);
     }
   }
+  // tap-outer / row-inner: TI independent accumulation chains advance together
+  // (ILP TI instead of one 2D+1-long dependent FMA chain at a time; ncu r01 showed
+  // the row-outer form stalled on fixed-latency FMA dependencies)
+  double acc[TI];
+#pragma unroll
+  for (int o = 0; o < TI; ++o) acc[o] = 0.0;
+  if (has) {
+#pragma unroll
+    for (int d = 0; d <= 2 * D; ++d) {
+      const double td = taps.t[d];
+#pragma unroll
+      for (int o = 0; o < TI; ++o) acc[o] = fma(td, v[o + d], acc[o]);
+    }
+  }
 #pragma unroll
   for (int o = 0; o < TI; ++o) {
     const int i = i0 + o;
     if (i < s) {
       double val = base[i * ld + col];
-      if (has) {
-        double acc = 0.0;
-#pragma unroll
-        for (int d = 0; d <= 2 * D; ++d) acc = fma(taps.t[d], v[o + d], acc);
-        val = fma(sign, acc, val);
-      }
+      if (has) val = fma(sign, acc[o], val);
       if (add2) {
         int j = row_map[i];
         if (j >= 0) val += add2[(int64_t)j * ld + col];
@@ -92,7 +101,7 @@ template <int D>
 static void heat_launch(Ctx &c, bool transpose, double sign, const double *in, const double *base,
                         double *out, int w_first, int w_step, int nw, const double *add2,
                         const int *row_map) {
-  constexpr int TI = 32;
+  constexpr int TI = 16;
   Taps taps;
   for (int d = 0; d <= 2 * D; ++d) taps.t[d] = c.heat_taps[d - D + c.heat_D];
   int cols = nw * c.m;
