@@ -113,7 +113,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     wf::setup_model(c, p);
     c.ws_seg = c.alloc<double>((size_t)c.s * c.ncol);
     // dot partials: gy <= 2*148 blocks x up to 4 dots x m
-    c.dot_part_cap = 2 * 148 * 4 * std::max(c.m, 256) + 4096;
+    c.dot_part_cap = 4 * 148 * 4 * std::max(c.m, 256) + 4096;
     c.dot_part = c.alloc<double>(c.dot_part_cap);
     WF_CUDA(cudaMallocHost((void **)&c.hpin, 16 * sizeof(int)));
     c.pc = *pc;

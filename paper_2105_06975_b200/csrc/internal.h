@@ -214,6 +214,12 @@ void apply_P(Ctx &c, const double *x, double *y);
 // Krylov
 void solve(Ctx &c, const double *rhs, double *x, const wf4dvar_solve_opts &o, wf4dvar_report *rep);
 
+// launch geometry of the per-RHS reductions over a [n/m][m] view (see vec.cu)
+struct RedGrid { int gx, gy, RB; int64_t rows, rpb; };
+RedGrid red_grid(const Ctx &c, int64_t n);
+// fixed-order final reduction of per-block partials (part[(b*nd + d)*m + r]) -> out[d*m + r]
+void reduce_final(Ctx &c, const double *part, int nparts, int nd, double *out);
+
 // batched dots: out[j*m + r] = sum_{f % m == r} a_j[f] * b_j[f], j < nd (<= 4)
 void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_t n,
           double *out);

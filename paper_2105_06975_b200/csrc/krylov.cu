@@ -34,19 +34,39 @@ __global__ void k_lin3(double *y, const double *x1, const double *a, const doubl
 // MINRES fused update:
 //   w_new = kz z - k3 w_prev - k2 w ;  Aw_new = kz q - k3 Aw_prev - k2 Aw
 //   x += cx w_new ; r -= cx Aw_new       (w_new -> w_prev slot, Aw_new -> Aw_prev slot)
-__global__ void k_minres_update(const double *z, const double *q, double *w_prev, const double *w,
-                                double *Aw_prev, const double *Aw, double *x, double *res,
-                                const double *coef, int64_t n, int m) {
-  int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= n) return;
-  int r = (int)(f % m);
-  const double kz = coef[r], k3 = coef[m + r], k2 = coef[2 * m + r], cx = coef[3 * m + r];
-  double wn = kz * z[f] - k3 * w_prev[f] - k2 * w[f];
-  double awn = kz * q[f] - k3 * Aw_prev[f] - k2 * Aw[f];
-  w_prev[f] = wn;
-  Aw_prev[f] = awn;
-  x[f] = fma(cx, wn, x[f]);
-  res[f] = fma(-cx, awn, res[f]);
+// (also accumulates per-block partial sums of the new ||r||^2: one pass less)
+__global__ void __launch_bounds__(256) k_minres_update(
+    const double *z, const double *q, double *w_prev, const double *w, double *Aw_prev,
+    const double *Aw, double *x, double *res, const double *coef, int64_t rows, int m, int RB,
+    int64_t rpb, double *part) {
+  __shared__ double sm[256];
+  const int t = threadIdx.x;
+  const int rl = t % RB, u = t / RB, U = 256 / RB;
+  const int r = blockIdx.x * RB + rl;
+  const int64_t row0 = (int64_t)blockIdx.y * rpb, row1 = min(rows, row0 + rpb);
+  double rr = 0.0;
+  if (r < m && u < U) {
+    const double kz = coef[r], k3 = coef[m + r], k2 = coef[2 * m + r], cx = coef[3 * m + r];
+#pragma unroll 2
+    for (int64_t row = row0 + u; row < row1; row += U) {
+      const int64_t f = row * m + r;
+      double wn = kz * z[f] - k3 * w_prev[f] - k2 * w[f];
+      double awn = kz * q[f] - k3 * Aw_prev[f] - k2 * Aw[f];
+      w_prev[f] = wn;
+      Aw_prev[f] = awn;
+      x[f] = fma(cx, wn, x[f]);
+      double rn = fma(-cx, awn, res[f]);
+      res[f] = rn;
+      rr = fma(rn, rn, rr);
+    }
+  }
+  sm[t] = rr;
+  __syncthreads();
+  if (u == 0 && r < m) {
+    double v = 0.0;
+    for (int uu = 0; uu < U; ++uu) v += sm[uu * RB + rl];
+    part[(int64_t)blockIdx.y * m + r] = v;
+  }
 }
 
 struct MinresS {
@@ -203,9 +223,14 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
     apply_P(c, vn, zn);
     { const double *a[1] = {zn}, *bb[1] = {vn}; dots(c, 1, a, bb, n, S.dots); }
     k_minres_s2<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
-    k_minres_update<<<nblk(n, 256), 256, 0, c.st>>>(z, q, wp, w, awp, aw, x, res, S.coef, n, m);
-    c.launches += 2;
-    { const double *a[1] = {res}, *bb[1] = {res}; dots(c, 1, a, bb, n, S.dots); }
+    {
+      const RedGrid rg = red_grid(c, n);
+      LaunchScope ls(c, K_VEC, 10.0 * n, 8.0 * 12 * n);
+      k_minres_update<<<dim3(rg.gx, rg.gy), 256, 0, c.st>>>(z, q, wp, w, awp, aw, x, res, S.coef,
+                                                            rg.rows, m, rg.RB, rg.rpb, c.dot_part);
+      c.launches += 2;
+      reduce_final(c, c.dot_part, rg.gy, 1, S.dots);   // ||r_j||^2
+    }
     k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, j, o.tol, o.mark_tol);
     c.launches++;
     WF_CUDA(cudaGetLastError());
@@ -294,14 +319,18 @@ __global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64
   }
 }
 
+// one warp per (vector, RHS) output, fixed-order shuffle tree (deterministic)
 __global__ void k_multidot_final(const double *part, int nparts, int nv, int jmax, int m,
                                  double *out) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (e >= nv * m) return;
-  int i = e / m, r = e % m;
+  const int i = e / m, r = e % m;
   double v = 0.0;
-  for (int b = 0; b < nparts; ++b) v += part[((int64_t)b * jmax + i) * m + r];
-  out[e] = v;
+  for (int b = lane; b < nparts; b += 32) v += part[((int64_t)b * jmax + i) * m + r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) out[e] = v;
 }
 
 // w[f] -= sum_i V_i[f] h[i m + r]; optionally partial sums of w_new^2 per RHS
@@ -510,7 +539,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
     LaunchScope ls(c, K_DOT, 2.0 * nv * n, 8.0 * (nv + 1) * n);
     dim3 grid(gx, gy, (nv + 7) / 8);
     k_multidot_partial<<<grid, 256, 0, c.st>>>(V, n, nv, w, rows, m, RB, rpb, part, jmax);
-    k_multidot_final<<<nblk((int64_t)nv * m, 128), 128, 0, c.st>>>(part, gy, nv, jmax, m, out);
+    k_multidot_final<<<nblk((int64_t)nv * m, 8), 256, 0, c.st>>>(part, gy, nv, jmax, m, out);
     c.launches += 2;
   };
   auto multiaxpy = [&](int nv, double *w, const double *h, bool norm) {
@@ -519,7 +548,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
     k_multiaxpy<<<grid, 256, 0, c.st>>>(V, n, nv, w, h, rows, m, RB, rpb, norm ? part : nullptr);
     c.launches++;
     if (norm) {
-      k_multidot_final<<<nblk(m, 128), 128, 0, c.st>>>(part, gy, 1, 1, m, S.ww);
+      k_multidot_final<<<nblk(m, 8), 256, 0, c.st>>>(part, gy, 1, 1, m, S.ww);
       c.launches++;
     }
   };

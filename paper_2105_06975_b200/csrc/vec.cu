@@ -98,11 +98,28 @@ __global__ void __launch_bounds__(256) k_dots_partial(DotArgs args, int64_t rows
 #pragma unroll
   for (int d = 0; d < ND; ++d) acc[d] = 0.0;
   if (r < m && u < U) {
-    for (int64_t row = row0 + u; row < row1; row += U) {
+    // 4 rows in flight per thread (independent partial sums, combined in fixed order)
+    double acc2[4][ND];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int d = 0; d < ND; ++d) acc2[q][d] = 0.0;
+    int64_t row = row0 + u;
+    for (; row + 3 * U < row1; row += 4 * U) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        int64_t f = (row + q * U) * m + r;
+#pragma unroll
+        for (int d = 0; d < ND; ++d) acc2[q][d] = fma(args.a[d][f], args.b[d][f], acc2[q][d]);
+      }
+    }
+    for (; row < row1; row += U) {
       int64_t f = row * m + r;
 #pragma unroll
-      for (int d = 0; d < ND; ++d) acc[d] = fma(args.a[d][f], args.b[d][f], acc[d]);
+      for (int d = 0; d < ND; ++d) acc2[0][d] = fma(args.a[d][f], args.b[d][f], acc2[0][d]);
     }
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc[d] = (acc2[0][d] + acc2[1][d]) + (acc2[2][d] + acc2[3][d]);
   }
 #pragma unroll
   for (int d = 0; d < ND; ++d) sm[d][t] = acc[d];
@@ -117,23 +134,44 @@ __global__ void __launch_bounds__(256) k_dots_partial(DotArgs args, int64_t rows
   }
 }
 
+// one warp per output: lane-strided partial sums, then a fixed-order shuffle tree
+// (deterministic; r01 ncu: the one-thread-per-output version took ~50 us)
 __global__ void k_dots_final(const double *part, int nparts, int nd, int m, double *out) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (e >= nd * m) return;
-  int d = e / m, r = e % m;
+  const int d = e / m, r = e % m;
   double v = 0.0;
-  for (int b = 0; b < nparts; ++b) v += part[((int64_t)b * nd + d) * m + r];
-  out[e] = v;
+  for (int b = lane; b < nparts; b += 32) v += part[((int64_t)b * nd + d) * m + r];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) out[e] = v;
+}
+
+RedGrid red_grid(const Ctx &c, int64_t n) {
+  RedGrid g;
+  const int m = c.m;
+  g.rows = n / m;
+  g.RB = m < 256 ? m : 256;
+  g.gx = (m + g.RB - 1) / g.RB;
+  g.gy = (int)std::max<int64_t>(1, std::min<int64_t>((4 * 148 + g.gx - 1) / g.gx, (g.rows + 255) / 256));
+  g.rpb = (g.rows + g.gy - 1) / g.gy;
+  g.gy = (int)((g.rows + g.rpb - 1) / g.rpb);
+  return g;
+}
+
+void reduce_final(Ctx &c, const double *part, int nparts, int nd, double *out) {
+  LaunchScope ls(c, K_DOT, 0, 8.0 * nparts * nd * c.m);
+  k_dots_final<<<(nd * c.m + 7) / 8, 256, 0, c.st>>>(part, nparts, nd, c.m, out);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
 }
 
 void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_t n, double *out) {
   const int m = c.m;
-  const int64_t rows = n / m;
-  const int RB = m < 256 ? m : 256;
-  const int gx = (m + RB - 1) / RB;
-  int gy = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + gx - 1) / gx, (rows + 255) / 256));
-  const int64_t rpb = (rows + gy - 1) / gy;
-  gy = (int)((rows + rpb - 1) / rpb);
+  const RedGrid rg = red_grid(c, n);
+  const int64_t rows = rg.rows, rpb = rg.rpb;
+  const int RB = rg.RB, gx = rg.gx, gy = rg.gy;
   const int need = gy * nd * m;
   WF_REQUIRE(need <= c.dot_part_cap, WF4DVAR_EINVAL, "dot partial buffer too small");
   DotArgs args{};
@@ -150,12 +188,7 @@ void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_
     WF_CUDA(cudaGetLastError());
     c.launches++;
   }
-  {
-    LaunchScope ls(c, K_DOT, 0, 8.0 * gy * nd * m);
-    k_dots_final<<<(nd * m + 127) / 128, 128, 0, c.st>>>(c.dot_part, gy, nd, m, out);
-    WF_CUDA(cudaGetLastError());
-    c.launches++;
-  }
+  reduce_final(c, c.dot_part, gy, nd, out);
 }
 
 }  // namespace wf
