@@ -249,9 +249,9 @@ class Context:
         self._check(_lib.wf4dvar_profile_enable(self._h, 1 if on else 0))
 
     def profile_read(self):
-        arr = (KStat * 16)()
+        arr = (KStat * 32)()
         n = C.c_int32()
-        self._check(_lib.wf4dvar_profile_read(self._h, arr, 16, C.byref(n)))
+        self._check(_lib.wf4dvar_profile_read(self._h, arr, 32, C.byref(n)))
         return {arr[i].name.decode(): dict(launches=arr[i].launches, ms=arr[i].ms,
                                            flops=arr[i].flops, bytes=arr[i].bytes)
                 for i in range(n.value)}

@@ -145,7 +145,7 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
     big_tiles += tiles_of<CfgBig>(p, tm, tn);
   }
   if (flops_hint >= 0) flops = flops_hint;
-  LaunchScope ls(c, K_GEMM, flops, bytes);
+  LaunchScope ls(c, c.gemm_cls, flops, bytes);
   static int force = -2;
   if (force == -2) {
     const char *e = getenv("WF4DVAR_GEMM_CFG");   // tuning experiments only

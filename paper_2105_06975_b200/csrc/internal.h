@@ -29,9 +29,13 @@ struct Error {
   } while (0)
 
 // ---------------------------------------------------------------- profiling
-enum KClass { K_GEMM = 0, K_TRSM, K_MODEL, K_VEC, K_DOT, K_SCALAR, K_NCLASS };
-static const char *const kClassName[K_NCLASS] = {"gemm_dmma", "trsm_dmma", "model_stencil",
-                                                 "vector", "dot_reduce", "krylov_scalar"};
+// K_GEMM: covariance / dense-model products (a1, a2, a10, a12);  K_TRSM: triangular
+// panel solves (a7, a8);  K_TRSM_UPD: the DMMA GEMM coupling of a solved TRSM
+// super-block to the remaining rows (same k_gemm kernel, counted with the solve).
+enum KClass { K_GEMM = 0, K_TRSM, K_TRSM_UPD, K_MODEL, K_VEC, K_DOT, K_SCALAR, K_NCLASS };
+static const char *const kClassName[K_NCLASS] = {"gemm_dmma", "trsm_dmma", "trsm_update_dmma",
+                                                 "model_stencil", "vector", "dot_reduce",
+                                                 "krylov_scalar"};
 
 struct Prof {
   bool on = false;
@@ -116,6 +120,7 @@ struct Ctx {
   // counters (per-window constituent products, Tables 7.2-7.3 / S5-S7)
   int64_t n_R = 0, n_Rhat_inv = 0, n_D = 0, n_Dhat_inv = 0, n_M = 0, n_A = 0, n_P = 0;
   int64_t launches = 0;
+  int gemm_cls = K_GEMM;          // profiling class of the next launch_gemm
   Prof prof;
   std::string last_error;
   std::vector<void *> allocs;
@@ -164,9 +169,11 @@ struct Ctx {
 };
 
 // Run the enclosed launches on another stream of the context.
+// While profiling, everything stays on the main stream: per-launch event times of
+// concurrently running kernels would overlap and misstate each kernel's rate.
 struct OnStream {
   Ctx &c; cudaStream_t saved;
-  OnStream(Ctx &c_, cudaStream_t s) : c(c_), saved(c_.st) { c.st = s; }
+  OnStream(Ctx &c_, cudaStream_t s) : c(c_), saved(c_.st) { if (!c.prof.on) c.st = s; }
   ~OnStream() { c.st = saved; }
 };
 void fork(Ctx &c);   // aux streams wait for the work enqueued so far on c.st

@@ -262,7 +262,9 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
         q.M = rhi - rlo; q.N = P.ncols; q.K = hi - lo;
         q.alpha = -1.0; q.beta = 1.0;
       }
+      c.gemm_cls = K_TRSM_UPD;
       launch_gemm(c, g, np, 1);
+      c.gemm_cls = K_GEMM;
     }
     // after the first coupling every remaining row of Y is initialised: solve in place
     for (int i = 0; i < np; ++i) { cur[i].X = cur[i].Y; cur[i].ldx = cur[i].ldy; }
