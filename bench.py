@@ -56,6 +56,10 @@ def parse():
                     help="cap for the time-to-1e-8 solve (0 disables it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--shard", default="time", choices=["time", "batch"],
+                    help="N > 1: 'time' = the windows of ONE batch sharded over the ranks "
+                         "(NCCL halos + allreduce, strong scaling; SURVEY 8(e)); 'batch' = an "
+                         "independent batch per rank (no collective, weak scaling)")
     return ap.parse_args()
 
 
@@ -211,12 +215,22 @@ def main():
     cell = cell_of(args)
     cfgm = SC.CONFIGS[args.config]["m"]
     m = args.m or cfgm
-    prob = SC.make_problem(args.config, seed0=rank * m, m=m)
+    time_shard = ws > 1 and args.shard == "time"
+    prob = SC.make_problem(args.config, seed0=0 if time_shard else rank * m, m=m)
     stream = torch.cuda.Stream(device=dev)
     pc = {k: cell[k] for k in ("shape", "lhat", "k", "rhat")}
-    ctx = W.Context.from_problem(prob, pc, device=local, stream=stream.cuda_stream)
+    dkw = {}
+    if time_shard:
+        ids = [W.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(ids, src=0)
+        dkw = dict(rank=rank, world=ws, nccl_id=ids[0])
+    ctx = W.Context.from_problem(prob, pc, device=local, stream=stream.cuda_stream, **dkw)
     peak_fp64 = measure_dgemm_peak(torch, dev) if rank == 0 else None
-    b = torch.from_numpy(prob.rhs).to(dev)
+    rhs = prob.rhs
+    if time_shard:
+        rhs = W.local_windows(prob.rhs, prob.s, prob.p, prob.W, m, ctx.w_begin, ctx.w_end)
+    n_local = rhs.size
+    b = torch.from_numpy(rhs).to(dev)
     x = torch.empty_like(b)
     solver = cell["solver"]
     kw = dict(solver=solver, tol=1e-300, restart=50, mark_tol=1e-8)
@@ -248,7 +262,8 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         secs = float(t.item())
     steps = args.steps
-    value = ws * steps / secs
+    units = 1 if time_shard else ws       # A+P applies of the whole job per step
+    value = units * steps / secs
 
     # per-kernel-class rates: the same K steps again with the library's CUDA-event
     # instrumentation on (launches serialised on the library stream while profiling,
@@ -259,8 +274,8 @@ def main():
     ctx.profile_enable(False)
 
     # end-to-end: the public API with HOST buffers (H2D + A+P + D2H every step)
-    xh = torch.from_numpy(np.random.Generator(np.random.PCG64(5)).standard_normal(prob.n)).pin_memory()
-    yh = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+    xh = torch.from_numpy(np.random.Generator(np.random.PCG64(5)).standard_normal(n_local)).pin_memory()
+    yh = torch.empty(n_local, dtype=torch.float64).pin_memory()
     ctx.apply_AP_host(xh.numpy(), yh.numpy())
     barrier()
     t0 = time.perf_counter()
@@ -271,7 +286,7 @@ def main():
         t = torch.tensor([e2e_secs], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_secs = float(t.item())
-    e2e_val = ws * args.e2e_steps / e2e_secs
+    e2e_val = units * args.e2e_steps / e2e_secs
 
     # time-to-1e-8 (one real solve; reported, capped)
     tts = None
@@ -335,16 +350,18 @@ def main():
                           f"size (s={prob.s}, N={prob.N}), factorisations untimed, scaled x1/{m}")
     line = dict(metric="saddle-point A+P applies/sec (FP64)", value=value, unit="A+P applies/s",
                 n_gpus=ws, steps=steps, warmup=args.warmup, ms_per_step=secs / steps * 1e3,
-                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                higher_is_better=True, scaling="strong" if time_shard else "weak", vs_baseline=None, dtype="f64",
                 data="synthetic",
                 config=dict(workload=f"BASELINE.json configs[{args.config}]",
                             desc=SC.CONFIGS[args.config]["desc"], cell=cell, s=prob.s, p=prob.p,
                             N=prob.N, m=m, step="one batched Krylov iteration (1 A + 1 P apply)",
                             l2="inputs larger than L2 (no flush needed)",
-                            parallelism=f"independent batch per rank x{ws}"),
+                            parallelism=(f"time windows sharded over {ws} ranks (NCCL one-state "
+                                         f"halos + Krylov allreduce)") if time_shard else
+                                        f"independent batch per rank x{ws}"),
                 roofline=roof, step_roofline=step_roof, cpu_baseline=cpu,
-                e2e=dict(value=e2e_val, unit="A+P applies/s", h2d_bytes_per_step=prob.n * 8,
-                         d2h_bytes_per_step=prob.n * 8,
+                e2e=dict(value=e2e_val, unit="A+P applies/s", h2d_bytes_per_step=n_local * 8 * ws,
+                         d2h_bytes_per_step=n_local * 8 * ws,
                          how="wf4dvar_apply_AP_host: pinned host x -> device, A+P, y -> host"),
                 gpu_launches=launches, clocks=clk.summary(), time_to_1e8=tts, kernels=kernels,
                 counters=dict(n_apply_A=rep["n_apply_A"], n_apply_P=rep["n_apply_P"]))

@@ -117,10 +117,33 @@ typedef struct {
   double dhat_ridge;  /* 0 => D_hat = D; > 0 => D_hat = D + ridge I         */
 } wf4dvar_precond;
 
+/* Time-window sharding ("the model propagations M_i can be
+ * run in parallel", P:L253 the parallel-in-time L_M(k)).  With world > 1 rank g
+ * owns the contiguous global windows [w_begin, w_end) of wf4dvar_partition, all
+ * vectors are rank-local ((2s+p)*(w_end-w_begin)*m doubles, same segment layout),
+ * B, Q, R, H and the model data are passed in full on every rank.  Per A apply
+ * two one-state halos move ([s][m] doubles: x3 of the last window to rank+1 for L,
+ * x1 of the first window to rank-1 for L^T); L_hat chains that cross a rank
+ * boundary hand their running state over once per crossing (none when k divides
+ * every rank's w_begin); L_I uses an allgather of per-rank window sums; the
+ * Krylov inner products are summed over the ranks (allreduce of [nd][m] doubles).
+ * Every rank calls create / apply / solve / destroy in the same order. */
+typedef enum {
+  WF4DVAR_TRANSPORT_NONE = 0,  /* world must be 1                                          */
+  WF4DVAR_TRANSPORT_NCCL = 1,  /* one process per GPU; NCCL (libnccl.so.2, dlopen'ed)      */
+  WF4DVAR_TRANSPORT_LOCAL = 2  /* world ranks = host threads of one process sharing a
+                                  wf4dvar_local_group (single-device driving of the
+                                  sharded path; stream-ordered, no kernel waits on another) */
+} wf4dvar_transport;
+
 typedef struct {
-  int32_t rank, world; /* world == 1: single device (the only mode in v1)           */
+  int32_t rank, world; /* 0 <= rank < world; world <= N+1                           */
   int32_t device;      /* CUDA device ordinal                                       */
   void *stream;        /* cudaStream_t the library enqueues on (NULL = default)     */
+  int32_t transport;   /* wf4dvar_transport (ignored when world == 1)               */
+  const void *nccl_id; /* NCCL: the 128-byte ncclUniqueId rank 0 obtained from
+                          wf4dvar_nccl_unique_id, broadcast by the caller           */
+  void *local_group;   /* LOCAL: from wf4dvar_local_group_create(world)             */
 } wf4dvar_dist;
 
 typedef enum { WF4DVAR_MINRES = 0, WF4DVAR_GMRES = 1 } wf4dvar_solver;
@@ -188,6 +211,34 @@ wf4dvar_status wf4dvar_profile_read(wf4dvar_ctx ctx, wf4dvar_kstat *out, int32_t
                                     int32_t *n_out);
 /* Total number of kernel launches issued by this context so far. */
 int64_t wf4dvar_launch_count(wf4dvar_ctx ctx);
+
+/* ---- sharding helpers (host only; no device, no context needed) ---- */
+/* The contiguous balanced partition: rank g of `world` owns global windows
+   [w_begin, w_end), sizes differing by at most one (earlier ranks larger). */
+wf4dvar_status wf4dvar_partition(int32_t W, int32_t world, int32_t rank, int32_t *w_begin,
+                                 int32_t *w_end);
+/* Schedule of the L_hat^{-1} (transpose = 0) / L_hat^{-T} (transpose = 1) chain
+   substitution (Lemma 4.2) for chains of length k (k = N+1 for the
+   exact L) restricted to the windows [w_begin, w_end) of W: entry j (j = 1..)
+   updates the windows at chain position j -- forward z_w = r_w + M_w z_{w-1},
+   backward z_w = r_w + M_{w+1}^T z_{w+1} -- in nl launches of (first local
+   window, stride, count); recv = 1 means the neighbour's boundary state is
+   received into the halo first (forward from rank-1, backward from rank+1),
+   send = 1 that this rank's boundary window is sent the other way first.
+   Writes at most max_steps entries; *n_steps = the full count. */
+typedef struct {
+  int32_t j, recv, send, nl;
+  int32_t first[2], stride[2], count[2];
+} wf4dvar_chain_step;
+wf4dvar_status wf4dvar_chain_plan(int32_t W, int32_t k, int32_t w_begin, int32_t w_end,
+                                  int32_t transpose, wf4dvar_chain_step *out,
+                                  int32_t max_steps, int32_t *n_steps);
+/* NCCL: rank 0 fills out[128] with a fresh ncclUniqueId (to broadcast). */
+wf4dvar_status wf4dvar_nccl_unique_id(void *out128);
+/* LOCAL transport: one group shared by `world` contexts of this process. Destroy
+   it after every context that uses it. */
+wf4dvar_status wf4dvar_local_group_create(int32_t world, void **out);
+wf4dvar_status wf4dvar_local_group_destroy(void *group);
 
 const char *wf4dvar_last_error(wf4dvar_ctx ctx);
 /* Library build string (compile arch, version). */

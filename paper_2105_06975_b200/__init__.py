@@ -7,4 +7,5 @@ Importing this package loads libwf4dvar.so and raises if it is missing: there
 is no CPU fallback.
 """
 from ._lib import (Context, WF4DVarError, make_precond, version, EXPORTED,  # noqa: F401
-                   LIB_PATH)
+                   LIB_PATH, LocalGroup, partition, chain_plan, nccl_unique_id, local_windows,
+                   global_windows)

@@ -45,9 +45,18 @@ class Precond(C.Structure):
                 ("dhat_ridge", C.c_double)]
 
 
+TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
+
+
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("device", C.c_int32),
-                ("stream", C.c_void_p)]
+                ("stream", C.c_void_p), ("transport", C.c_int32), ("nccl_id", C.c_void_p),
+                ("local_group", C.c_void_p)]
+
+
+class ChainStep(C.Structure):
+    _fields_ = [("j", C.c_int32), ("recv", C.c_int32), ("send", C.c_int32), ("nl", C.c_int32),
+                ("first", C.c_int32 * 2), ("stride", C.c_int32 * 2), ("count", C.c_int32 * 2)]
 
 
 class SolveOpts(C.Structure):
@@ -84,6 +93,12 @@ _sig = {
     "wf4dvar_profile_enable": (C.c_int, [_ctx, C.c_int32]),
     "wf4dvar_profile_read": (C.c_int, [_ctx, C.POINTER(KStat), C.c_int32, _ip]),
     "wf4dvar_launch_count": (C.c_int64, [_ctx]),
+    "wf4dvar_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, _ip, _ip]),
+    "wf4dvar_chain_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(ChainStep), C.c_int32, _ip]),
+    "wf4dvar_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "wf4dvar_local_group_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
+    "wf4dvar_local_group_destroy": (C.c_int, [C.c_void_p]),
     "wf4dvar_last_error": (C.c_char_p, [_ctx]),
     "wf4dvar_version": (C.c_char_p, []),
 }
@@ -104,6 +119,85 @@ class WF4DVarError(RuntimeError):
 
 def version():
     return _lib.wf4dvar_version().decode()
+
+
+def partition(W, world, rank):
+    """Global windows [w_begin, w_end) owned by `rank` (host only)."""
+    b, e = C.c_int32(), C.c_int32()
+    st = _lib.wf4dvar_partition(int(W), int(world), int(rank), C.byref(b), C.byref(e))
+    if st != 0:
+        raise WF4DVarError(st, f"partition(W={W}, world={world}, rank={rank})")
+    return b.value, e.value
+
+
+def chain_plan(W, k, w_begin, w_end, transpose):
+    """The library's L_hat chain schedule for the local windows (host only)."""
+    n = C.c_int32()
+    st = _lib.wf4dvar_chain_plan(int(W), int(k), int(w_begin), int(w_end), int(transpose),
+                                 None, 0, C.byref(n))
+    if st != 0:
+        raise WF4DVarError(st, "chain_plan")
+    arr = (ChainStep * max(n.value, 1))()
+    _lib.wf4dvar_chain_plan(int(W), int(k), int(w_begin), int(w_end), int(transpose), arr,
+                            n.value, C.byref(n))
+    return [dict(j=a.j, recv=a.recv, send=a.send,
+                 launches=[(a.first[l], a.stride[l], a.count[l]) for l in range(a.nl)])
+            for a in arr[:n.value]]
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId (rank 0 creates it; the caller broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    st = _lib.wf4dvar_nccl_unique_id(buf)
+    if st != 0:
+        raise WF4DVarError(st, _lib.wf4dvar_last_error(None).decode())
+    return buf.raw
+
+
+class LocalGroup:
+    """In-process transport group: `world` contexts driven by `world` host threads."""
+
+    def __init__(self, world):
+        self._h = C.c_void_p()
+        st = _lib.wf4dvar_local_group_create(int(world), C.byref(self._h))
+        if st != 0:
+            raise WF4DVarError(st, "local_group_create")
+        self.world = int(world)
+
+    def close(self):
+        if self._h:
+            _lib.wf4dvar_local_group_destroy(self._h)
+            self._h = None
+
+
+def local_windows(vec, s, p, W, m, w_begin, w_end):
+    """Rank-local part [(2s+p)][w_begin:w_end][m] of a global library-layout vector
+    (argument marshalling for the sharded path; numpy or torch)."""
+    segs, off = [], 0
+    for ln in (s, p, s):
+        seg = vec[off:off + ln * W * m].reshape(ln, W, m)[:, w_begin:w_end, :]
+        segs.append(seg.reshape(-1))
+        off += ln * W * m
+    if hasattr(vec, "data_ptr"):
+        import torch
+        return torch.cat(segs).contiguous()
+    return np.ascontiguousarray(np.concatenate(segs))
+
+
+def global_windows(parts, s, p, m, bounds):
+    """Inverse of local_windows: assemble rank-local vectors (in rank order, with
+    their (w_begin, w_end)) into one global library-layout numpy vector."""
+    W = bounds[-1][1]
+    out = []
+    for si, ln in enumerate((s, p, s)):
+        blocks = []
+        for v, (b, e) in zip(parts, bounds):
+            v = np.asarray(v)
+            lw = e - b
+            offs = [0, s * lw * m, (s + p) * lw * m]
+            blocks.append(v[offs[si]:offs[si] + ln * lw * m].reshape(ln, lw, m))
+        out.append(np.concatenate(blocks, axis=1).reshape(-1))
+    return np.concatenate(out)
 
 
 def _ptr(a):
@@ -136,7 +230,7 @@ class Context:
 
     def __init__(self, s, p, N, m, B, Q, R, H_idx, model="heat", heat_r=0.25, M_dense=None,
                  l96_traj=None, l96_F=8.0, l96_dt=0.025, l96_nsub=5, precond=None, device=0,
-                 stream=None):
+                 stream=None, rank=0, world=1, nccl_id=None, local_group=None):
         keep = []
 
         def arr(a, dt=np.float64):
@@ -160,7 +254,19 @@ class Context:
             pr.l96_traj = _np_ptr(arr(l96_traj), C.c_double)
         pr.l96_F, pr.l96_dt, pr.l96_nsub = float(l96_F), float(l96_dt), int(l96_nsub)
         pc = precond if isinstance(precond, Precond) else make_precond(**(precond or {}))
-        d = Dist(0, 1, int(device), C.c_void_p(stream) if stream else None)
+        transport = TRANSPORT_NONE
+        idbuf = None
+        if world > 1:
+            if local_group is not None:
+                transport = TRANSPORT_LOCAL
+            else:
+                assert nccl_id is not None and len(nccl_id) == 128, "world > 1 needs nccl_id"
+                transport = TRANSPORT_NCCL
+                idbuf = C.create_string_buffer(bytes(nccl_id), 128)
+                keep.append(idbuf)
+        d = Dist(int(rank), int(world), int(device), C.c_void_p(stream) if stream else None,
+                 transport, C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                 local_group._h if local_group is not None else None)
         h = _ctx()
         st = _lib.wf4dvar_create(C.byref(pr), C.byref(pc), C.byref(d), C.byref(h))
         if st != 0:
@@ -168,6 +274,10 @@ class Context:
         self._h = h
         self.s, self.p, self.N, self.m = int(s), int(p), int(N), int(m)
         self.W = self.N + 1
+        self.rank, self.world = int(rank), int(world)
+        b, e = C.c_int32(), C.c_int32()
+        self._check(_lib.wf4dvar_local_windows(h, C.byref(b), C.byref(e)))
+        self.w_begin, self.w_end = b.value, e.value
         n = C.c_int64()
         self._check(_lib.wf4dvar_vector_len(h, C.byref(n)))
         self.n = n.value

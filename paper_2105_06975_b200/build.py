@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libwf4dvar.so")
-SOURCES = ["api.cu", "saddle.cu", "gemm.cu", "trsm.cu", "model.cu", "l96.cu", "vec.cu", "krylov.cu"]
+SOURCES = ["api.cu", "saddle.cu", "gemm.cu", "trsm.cu", "model.cu", "l96.cu", "vec.cu", "krylov.cu", "comm.cu"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 
@@ -33,7 +33,7 @@ def build(verbose=False, force=False):
     cmd = [_nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-Xptxas", "-v" if verbose else "-O3",
            "-o", LIB + ".tmp"] + srcs + [
-           "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcusolver", "-lcublas",
+           "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcusolver", "-lcublas", "-ldl",
            "-Xlinker", "-rpath=" + os.path.join(CUDA_HOME, "lib64")]
     if verbose:
         print(" ".join(cmd), flush=True)

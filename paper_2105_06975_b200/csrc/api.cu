@@ -83,9 +83,12 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     }
     WF_REQUIRE(p.model == WF4DVAR_M_DENSE || p.model == WF4DVAR_M_HEAT || p.model == WF4DVAR_M_L96,
                WF4DVAR_EINVAL, "unknown model");
+    int rank = 0, world = 1;
     if (dist) {
-      WF_REQUIRE(dist->world == 1 || dist->world == 0, WF4DVAR_EINVAL,
-                 "world > 1 (time-window sharding) is not in this build; run replicas per rank");
+      world = dist->world <= 0 ? 1 : dist->world;
+      rank = dist->rank;
+      WF_REQUIRE(rank >= 0 && rank < world, WF4DVAR_EINVAL, "dist: need 0 <= rank < world");
+      WF_REQUIRE(world <= p.N + 1, WF4DVAR_EINVAL, "dist: world must be <= N+1 (windows)");
       c.device = dist->device;
       c.st = (cudaStream_t)dist->stream;
     }
@@ -95,8 +98,23 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       WF_CUDA(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
-    c.s = p.s; c.p = p.p; c.N = p.N; c.W = p.N + 1; c.m = p.m; c.model = p.model;
+    c.s = p.s; c.p = p.p; c.N = p.N; c.WG = p.N + 1; c.m = p.m; c.model = p.model;
+    int wb = 0, we = c.WG;
+    wf::partition(c.WG, world, rank, &wb, &we);
+    c.w0 = wb;
+    c.W = we - wb;
     c.ncol = (int64_t)c.W * c.m;
+    if (world > 1) {
+      c.comm = wf::make_comm(*dist);
+      const size_t sm = (size_t)c.s * c.m;
+      c.halo_lo = c.alloc<double>(sm);
+      c.halo_hi = c.alloc<double>(sm);
+      c.pack_lo = c.alloc<double>(sm);
+      c.pack_hi = c.alloc<double>(sm);
+      c.gath = c.alloc<double>(sm * world);
+      WF_CUDA(cudaMemset(c.halo_lo, 0, sm * 8));
+      WF_CUDA(cudaMemset(c.halo_hi, 0, sm * 8));
+    }
     c.n = (int64_t)(2 * c.s + c.p) * c.ncol;
     c.B = c.alloc<double>((size_t)c.s * c.s);
     c.Q = c.alloc<double>((size_t)c.s * c.s);
@@ -151,6 +169,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
   }
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  delete c.comm;
+  c.comm = nullptr;
   for (void *p : c.allocs) cudaFree(p);
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : c.prof.pool) cudaEventDestroy(e);
@@ -165,8 +185,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
 wf4dvar_status wf4dvar_local_windows(wf4dvar_ctx ctx, int32_t *w_begin, int32_t *w_end) {
   return guarded(ctx, [&](Ctx &c) {
     WF_REQUIRE(w_begin && w_end, WF4DVAR_EINVAL, "NULL output");
-    *w_begin = 0;
-    *w_end = c.W;
+    *w_begin = c.w0;
+    *w_end = c.w0 + c.W;
   });
 }
 
@@ -285,6 +305,57 @@ wf4dvar_status wf4dvar_profile_read(wf4dvar_ctx ctx, wf4dvar_kstat *out, int32_t
 }
 
 int64_t wf4dvar_launch_count(wf4dvar_ctx ctx) { return ctx ? ctx->c.launches : -1; }
+
+wf4dvar_status wf4dvar_partition(int32_t W, int32_t world, int32_t rank, int32_t *w_begin,
+                                 int32_t *w_end) {
+  if (!w_begin || !w_end || W < 1 || world < 1 || world > W || rank < 0 || rank >= world)
+    return WF4DVAR_EINVAL;
+  int b, e;
+  wf::partition(W, world, rank, &b, &e);
+  *w_begin = b;
+  *w_end = e;
+  return WF4DVAR_OK;
+}
+
+wf4dvar_status wf4dvar_chain_plan(int32_t W, int32_t k, int32_t w_begin, int32_t w_end,
+                                  int32_t transpose, wf4dvar_chain_step *out, int32_t max_steps,
+                                  int32_t *n_steps) {
+  if (W < 1 || k < 1 || k > W || w_begin < 0 || w_end <= w_begin || w_end > W || !n_steps)
+    return WF4DVAR_EINVAL;
+  std::vector<wf::ChainStep> plan = wf::chain_plan(W, k, w_begin, w_end, transpose != 0);
+  *n_steps = (int32_t)plan.size();
+  for (int i = 0; i < (int)plan.size() && i < max_steps && out; ++i) {
+    const wf::ChainStep &s = plan[i];
+    out[i].j = s.j; out[i].recv = s.recv; out[i].send = s.send; out[i].nl = s.nl;
+    for (int l = 0; l < 2; ++l) {
+      out[i].first[l] = s.first[l]; out[i].stride[l] = s.stride[l]; out[i].count[l] = s.count[l];
+    }
+  }
+  return WF4DVAR_OK;
+}
+
+wf4dvar_status wf4dvar_nccl_unique_id(void *out128) {
+  if (!out128) return WF4DVAR_EINVAL;
+  try {
+    wf::nccl_unique_id(out128);
+  } catch (const Error &e) {
+    g_create_error = e.msg;
+    return e.st;
+  }
+  return WF4DVAR_OK;
+}
+
+wf4dvar_status wf4dvar_local_group_create(int32_t world, void **out) {
+  if (!out || world < 1) return WF4DVAR_EINVAL;
+  *out = wf::local_group_create(world);
+  return WF4DVAR_OK;
+}
+
+wf4dvar_status wf4dvar_local_group_destroy(void *group) {
+  if (!group) return WF4DVAR_EINVAL;
+  wf::local_group_destroy((wf::LocalGroup *)group);
+  return WF4DVAR_OK;
+}
 
 const char *wf4dvar_last_error(wf4dvar_ctx ctx) {
   if (!ctx) return g_create_error.c_str();

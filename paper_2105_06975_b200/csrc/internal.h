@@ -77,13 +77,52 @@ struct TrsmProb {
 
 struct Ctx;
 
+// ---------------------------------------------------------------- transport (comm.cu)
+// Stream-ordered collectives of the time-window-sharded path.
+struct Comm {
+  int rank = 0, world = 1;
+  struct P2P { void *buf; size_t count; int peer; bool send; };   // count in doubles
+  virtual ~Comm() {}
+  virtual void exchange(const std::vector<P2P> &ops, cudaStream_t st) = 0;
+  virtual void allreduce_sum(double *buf, size_t count, cudaStream_t st) = 0;
+  virtual void allgather(const double *send, double *recv, size_t count, cudaStream_t st) = 0;
+};
+struct LocalGroup;
+Comm *make_comm(const wf4dvar_dist &d);
+LocalGroup *local_group_create(int world);
+void local_group_destroy(LocalGroup *g);
+void nccl_unique_id(void *out128);
+
+// Contiguous balanced partition of W windows over `world` ranks.
+void partition(int W, int world, int rank, int *w_begin, int *w_end);
+
+// Schedule of one L_hat^{-1} (transpose = 0) or L_hat^{-T} (transpose = 1)
+// chain substitution with chains of length k over the global windows [0, WG),
+// restricted to the local windows [w0, w1): step j updates the windows at chain
+// position j (forward: w mod k == j; backward: j before the chain end); before the
+// step the rank receives the neighbour's boundary window (forward: from rank-1 into
+// the low halo; backward: from rank+1 into the high halo) and/or sends its own
+// boundary window the other way.  Launches are (local first window, stride, count).
+struct ChainStep {
+  int j, recv, send, nl;
+  int first[2], stride[2], count[2];
+};
+std::vector<ChainStep> chain_plan(int WG, int k, int w0, int w1, bool transpose);
+
 void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flops_hint = -1);
 void launch_trsm(Ctx &c, const TrsmProb *probs, int nprob, bool upper);
 
 // ---------------------------------------------------------------- context
 struct Ctx {
-  // problem
+  // problem.  W = number of LOCAL windows (the segment layout [len][W][m]); the
+  // rank owns global windows [w0, w0 + W) of WG = N + 1.
   int s = 0, p = 0, N = 0, W = 0, m = 0;
+  int w0 = 0, WG = 0;
+  Comm *comm = nullptr;           // world > 1 only
+  double *halo_lo = nullptr;      // [s][m]: state of global window w0 - 1 (from rank - 1)
+  double *halo_hi = nullptr;      // [s][m]: state of global window w0 + W (from rank + 1)
+  double *pack_lo = nullptr, *pack_hi = nullptr;   // [s][m] send staging
+  double *gath = nullptr;         // [world][s][m] L_I scan totals
   int model = 0;
   int64_t ncol = 0;   // W*m columns of every segment
   int64_t n = 0;      // (2s+p)*W*m
@@ -214,6 +253,11 @@ void scale_rows(Ctx &c, double *y, const double *x, const double *row_scale, int
 void lowrank_correct(Ctx &c, double *y, const double *x);
 void rhat_inv(Ctx &c, const double *x2, double *y2);
 void dhat_inv(Ctx &c, const double *x1, double *y1);
+
+// world > 1: in-place sum of per-RHS partial inner products over the ranks
+void allreduce(Ctx &c, double *buf, size_t count);
+// pack local window wl of an [s][W][m] segment into a contiguous [s][m] buffer
+void pack_window(Ctx &c, double *dst, const double *seg, int wl);
 
 void apply_A(Ctx &c, const double *x, double *y);
 void apply_P(Ctx &c, const double *x, double *y);

@@ -541,6 +541,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
     k_multidot_partial<<<grid, 256, 0, c.st>>>(V, n, nv, w, rows, m, RB, rpb, part, jmax);
     k_multidot_final<<<nblk((int64_t)nv * m, 8), 256, 0, c.st>>>(part, gy, nv, jmax, m, out);
     c.launches += 2;
+    allreduce(c, out, (size_t)nv * m);
   };
   auto multiaxpy = [&](int nv, double *w, const double *h, bool norm) {
     LaunchScope ls(c, K_VEC, 2.0 * nv * n, 8.0 * (nv + 2) * n);
@@ -550,6 +551,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
     if (norm) {
       k_multidot_final<<<nblk(m, 8), 256, 0, c.st>>>(part, gy, 1, 1, m, S.ww);
       c.launches++;
+      allreduce(c, S.ww, (size_t)m);
     }
   };
   auto norm2 = [&](const double *v) {

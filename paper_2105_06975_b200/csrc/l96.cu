@@ -27,10 +27,11 @@ struct L96Thread {
 
 struct L96Args {
   double *out;
-  const double *base, *in, *traj, *add2;
+  const double *base, *in, *traj, *add2, *halo;
   const int *row_map;
   double sign, F, dt;
   int s, W, m, nsub, w_first, w_step, nw, dir;
+  int w0, WG;   // global index of local window 0; global window count
 };
 
 template <int IPT>
@@ -113,8 +114,9 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
   const int r = blockIdx.x * 32 + lane;
   const int t = blockIdx.y;
   const int w = a.w_first + t * a.w_step;
-  const int ws = w + a.dir;
-  const bool has = ws >= 0 && ws < a.W;
+  const int ws = w + a.dir;                       // local source window
+  const bool has = a.w0 + ws >= 0 && a.w0 + ws < a.WG;   // global source exists
+  const bool from_halo = ws < 0 || ws >= a.W;      // owned by the neighbour rank
   const bool live = r < a.m;
   const int64_t ld = (int64_t)a.W * a.m;
   const int s = a.s;
@@ -122,13 +124,15 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
   double v[IPT];
   if (has) {
     // trajectory start state of the window pair: M_w uses traj[w-1], M_{w+1}^T uses traj[w]
-    const int tw = a.dir < 0 ? w - 1 : w;
+    const int tw = a.w0 + (a.dir < 0 ? w - 1 : w);
     double x[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
       int i = ty + 8 * k;
       x[k] = (live && i < s) ? a.traj[((int64_t)tw * s + i) * a.m + r] : 0.0;
-      v[k] = (live && i < s) ? a.in[i * ld + (int64_t)ws * a.m + r] : 0.0;
+      v[k] = (live && i < s) ? (from_halo ? a.halo[(int64_t)i * a.m + r]
+                                          : a.in[i * ld + (int64_t)ws * a.m + r])
+                             : 0.0;
     }
     if (a.dir < 0) {
       // forward tangent: nsub RK4 steps
@@ -216,6 +220,7 @@ void l96_step(Ctx &c, bool transpose, double sign, const double *in, const doubl
   L96Args a{};
   a.out = out; a.base = base; a.in = in; a.traj = c.traj; a.add2 = add2; a.row_map = row_map;
   a.sign = sign; a.F = c.l96_F; a.dt = c.l96_dt; a.s = c.s; a.W = c.W; a.m = c.m;
+  a.w0 = c.w0; a.WG = c.WG; a.halo = transpose ? c.halo_hi : c.halo_lo;
   a.nsub = c.l96_nsub; a.w_first = w_first; a.w_step = w_step; a.nw = nw;
   a.dir = transpose ? 1 : -1;
   dim3 grid((c.m + 31) / 32, nw), block(32, 8);

@@ -9,6 +9,7 @@
 // dropped tail is < 1e-17 relative (D = 22 at r = 0.25): a coalesced,
 // register-windowed 1-D stencil along the state index, one thread per
 // (window, RHS) column -- FP64-ALU/HBM balanced, no tensor cores (not a GEMM).
+#include <algorithm>
 #include <cmath>
 
 #include "internal.h"
@@ -23,14 +24,18 @@ __global__ void __launch_bounds__(128) k_heat_step(double *out, const double *ba
                                                    const double *in, const double *add2,
                                                    const int *row_map, const Taps taps, double sign,
                                                    int s, int W, int m, int w_first, int w_step,
-                                                   int nw, int dir) {
+                                                   int nw, int dir, const double *halo, int w0,
+                                                   int WG) {
   const int64_t ld = (int64_t)W * m;
   const int cc = blockIdx.x * blockDim.x + threadIdx.x;
   if (cc >= nw * m) return;
   const int tt = cc / m, r = cc - tt * m;
   const int w = w_first + tt * w_step;
-  const int ws = w + dir;   // dir = -1 (M_w in_{w-1}) or +1 (M_{w+1}^T in_{w+1})
-  const bool has = (ws >= 0 && ws < W);
+  const int ws = w + dir;   // dir = -1 (M_w in_{w-1}) or +1 (M_{w+1}^T in_{w+1}); local
+  const bool has = (w0 + ws >= 0 && w0 + ws < WG);   // the global source window exists
+  // a source outside the local windows belongs to the neighbour rank: its state
+  // was received into the [s][m] halo buffer
+  const bool from_halo = (ws < 0 || ws >= W);
   const int64_t col = (int64_t)w * m + r, cols = (int64_t)ws * m + r;
   const int i0 = blockIdx.y * TI;
   double v[TI + 2 * D];
@@ -40,7 +45,7 @@ __global__ void __launch_bounds__(128) k_heat_step(double *out, const double *ba
       int row = i0 - D + j;
       row = row < 0 ? row + s : (row >= s ? row - s : row);
       row = row < 0 ? row + s : (row >= s ? row - s : row);
-      v[j] = __ldg(in + row * ld + cols);
+      v[j] = from_halo ? __ldg(halo + (int64_t)row * m + r) : __ldg(in + row * ld + cols);
     }
   }
   // tap-outer / row-inner: TI independent accumulation chains advance together
@@ -107,7 +112,8 @@ static void heat_launch(Ctx &c, bool transpose, double sign, const double *in, c
   int cols = nw * c.m;
   dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
   k_heat_step<D, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, taps, sign, c.s, c.W,
-                                              c.m, w_first, w_step, nw, transpose ? 1 : -1);
+                                              c.m, w_first, w_step, nw, transpose ? 1 : -1,
+                                              transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
   WF_CUDA(cudaGetLastError());
 }
 
@@ -134,38 +140,53 @@ void model_step(Ctx &c, bool transpose, double sign, const double *in, const dou
     return;
   }
   if (c.model == WF4DVAR_M_DENSE || c.model == WF4DVAR_M_HEAT) {
-    // Windows without a source (w = 0 forward, w = N transposed) are a copy of base.
-    int t0 = 0, t1 = nw;
+    // Windows without a (global) source -- w = 0 forward, w = N transposed -- are a
+    // copy of base; a source owned by the neighbour rank comes from the halo.
+    const int dir = transpose ? 1 : -1;
     auto src_ok = [&](int t) {
-      int w = w_first + t * w_step, ws = w + (transpose ? 1 : -1);
-      return ws >= 0 && ws < c.W;
+      int ws = c.w0 + w_first + t * w_step + dir;
+      return ws >= 0 && ws < c.WG;
     };
+    auto src_halo = [&](int t) {
+      int ws = w_first + t * w_step + dir;
+      return ws < 0 || ws >= c.W;
+    };
+    auto mat = [&](int w) {   // M_w at Mdense[w-1]; M_{w+1}^T at MdenseT[w]  (global w)
+      return transpose ? c.MdenseT + (int64_t)(c.w0 + w) * s * s
+                       : c.Mdense + (int64_t)(c.w0 + w - 1) * s * s;
+    };
+    int t0 = 0, t1 = nw;
     for (int t = 0; t < nw; ++t) {
+      int w = w_first + t * w_step;
       if (!src_ok(t)) {
-        int w = w_first + t * w_step;
         if (out != base)
           WF_CUDA(cudaMemcpy2DAsync(out + (int64_t)w * m, ld * 8, base + (int64_t)w * m, ld * 8,
                                     m * 8, s, cudaMemcpyDeviceToDevice, c.st));
+      } else if (src_halo(t)) {
+        GemmProb g{};
+        g.A = mat(w); g.lda = s;
+        g.X = transpose ? c.halo_hi : c.halo_lo; g.ldx = m;
+        g.Y = out + (int64_t)w * m; g.ldy = ld;
+        g.Z = base + (int64_t)w * m; g.ldz = ld;
+        g.M = s; g.N = m; g.K = s; g.alpha = sign; g.beta = 1.0;
+        launch_gemm(c, &g, 1, 1);
       }
     }
-    while (t0 < t1 && !src_ok(t0)) ++t0;
-    while (t1 > t0 && !src_ok(t1 - 1)) --t1;
+    auto plain = [&](int t) { return src_ok(t) && !src_halo(t); };
+    while (t0 < t1 && !plain(t0)) ++t0;
+    while (t1 > t0 && !plain(t1 - 1)) --t1;
     if (t1 > t0) {
       int wf0 = w_first + t0 * w_step;
       GemmProb g{};
-      // M_w is stored at Mdense[w-1]; M_{w+1}^T at MdenseT[w]
-      g.A = transpose ? c.MdenseT + (int64_t)wf0 * s * s : c.Mdense + (int64_t)(wf0 - 1) * s * s;
+      g.A = mat(wf0);
       g.lda = s; g.sA = (int64_t)w_step * s * s;
-      g.X = in + (int64_t)(wf0 + (transpose ? 1 : -1)) * m; g.ldx = ld; g.sX = (int64_t)w_step * m;
+      g.X = in + (int64_t)(wf0 + dir) * m; g.ldx = ld; g.sX = (int64_t)w_step * m;
       g.Y = out + (int64_t)wf0 * m; g.ldy = ld; g.sY = (int64_t)w_step * m;
       g.Z = base + (int64_t)wf0 * m; g.ldz = ld; g.sZ = (int64_t)w_step * m;
       g.zrow = nullptr;
       g.M = s; g.N = m; g.K = s;
       g.alpha = sign; g.beta = 1.0;
       launch_gemm(c, &g, 1, t1 - t0);
-    }
-    for (int t = 0; t < nw; ++t) {
-      // nothing: all windows handled
     }
     if (add2) {
       // H^T scatter on every target window (only used with w_step == 1 over all windows)
@@ -180,39 +201,132 @@ void model_step(Ctx &c, bool transpose, double sign, const double *in, const dou
   throw Error{WF4DVAR_EINVAL, "model not supported by model_step"};
 }
 
+// out[i][w][r] += sum_{q in [qlo, qhi)} tot[q][i][r] for every local window w
+__global__ void k_add_totals(double *z, const double *tot, int qlo, int qhi, int s, int W, int m) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)s * m) return;
+  int64_t i = e / m, r = e % m;
+  double add = 0.0;
+  for (int q = qlo; q < qhi; ++q) add += tot[(int64_t)q * s * m + e];   // fixed rank order
+  if (add == 0.0 && qlo >= qhi) return;
+  double *p = z + i * (int64_t)W * m + r;
+  for (int w = 0; w < W; ++w) p[(int64_t)w * m] += add;
+}
+
+void pack_window(Ctx &c, double *dst, const double *seg, int wl) {
+  WF_CUDA(cudaMemcpy2DAsync(dst, (size_t)c.m * 8, seg + (int64_t)wl * c.m, (size_t)c.ncol * 8,
+                            (size_t)c.m * 8, c.s, cudaMemcpyDeviceToDevice, c.st));
+}
+
+void partition(int W, int world, int rank, int *w_begin, int *w_end) {
+  const int base = W / world, rem = W % world;
+  *w_begin = rank * base + std::min(rank, rem);
+  *w_end = *w_begin + base + (rank < rem ? 1 : 0);
+}
+
+std::vector<ChainStep> chain_plan(int WG, int k, int w0, int w1, bool transpose) {
+  std::vector<ChainStep> plan;
+  const int L = std::min(k, WG);   // longest chain
+  const int nfull = WG / k;
+  const int last_len = WG - nfull * k;
+  // backward position of w: distance to the end of its chain
+  auto pos_bwd = [&](int w) { return std::min((w / k + 1) * k, WG) - 1 - w; };
+  // first w >= lo with w mod k == res
+  auto first_congruent = [&](int lo, int res) { return lo + (((res - lo) % k) + k) % k; };
+  for (int j = 1; j < L; ++j) {
+    ChainStep st{};
+    st.j = j;
+    if (!transpose) {
+      // z_w = r_w + M_w z_{w-1} for w mod k == j
+      st.recv = (w0 > 0 && w0 % k == j) ? 1 : 0;
+      st.send = (w1 < WG && w1 % k == j) ? 1 : 0;
+      int wf = first_congruent(w0, j);
+      if (wf < w1) {
+        st.first[0] = wf - w0; st.stride[0] = k; st.count[0] = (w1 - 1 - wf) / k + 1;
+        st.nl = 1;
+      }
+    } else {
+      // z_w = r_w + M_{w+1}^T z_{w+1} for the windows j before their chain end
+      st.recv = (w1 < WG && pos_bwd(w1 - 1) == j) ? 1 : 0;
+      st.send = (w0 > 0 && pos_bwd(w0 - 1) == j) ? 1 : 0;
+      const int hi_full = std::min(w1, nfull * k);
+      int wf = first_congruent(w0, k - 1 - j);
+      if (wf < hi_full) {
+        st.first[st.nl] = wf - w0; st.stride[st.nl] = k;
+        st.count[st.nl] = (hi_full - 1 - wf) / k + 1;
+        st.nl++;
+      }
+      const int wr = WG - 1 - j;   // ragged last chain [nfull k, WG)
+      if (j < last_len && wr >= std::max(w0, nfull * k) && wr < w1) {
+        st.first[st.nl] = wr - w0; st.stride[st.nl] = 1; st.count[st.nl] = 1;
+        st.nl++;
+      }
+    }
+    plan.push_back(st);
+  }
+  return plan;
+}
+
+// L_I^{-1} / L_I^{-T}: window prefix / suffix sums, local scan plus,
+// across ranks, the sum of the other ranks' window totals (allgather, rank order).
+static void li_scan(Ctx &c, bool transpose, double *z) {
+  {
+    LaunchScope ls(c, K_MODEL, 0, (double)c.s * c.ncol * 16);
+    int64_t tot = (int64_t)c.s * c.m;
+    k_window_scan<<<(unsigned)((tot + 127) / 128), 128, 0, c.st>>>(z, c.s, c.W, c.m,
+                                                                   transpose ? -1 : 1);
+    WF_CUDA(cudaGetLastError());
+    c.launches++;
+  }
+  if (!c.comm) return;
+  double *mine = transpose ? c.pack_lo : c.pack_hi;
+  pack_window(c, mine, z, transpose ? 0 : c.W - 1);
+  const size_t cnt = (size_t)c.s * c.m;
+  c.comm->allgather(mine, c.gath, cnt, c.st);
+  const int rank = c.comm->rank, world = c.comm->world;
+  const int qlo = transpose ? rank + 1 : 0, qhi = transpose ? world : rank;
+  if (qlo >= qhi) return;
+  LaunchScope ls(c, K_MODEL, 0, (double)c.s * c.ncol * 16);
+  k_add_totals<<<(unsigned)((cnt + 127) / 128), 128, 0, c.st>>>(z, c.gath, qlo, qhi, c.s, c.W, c.m);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
+}
+
 void lhat_solve(Ctx &c, bool transpose, double *z) {
-  const int W = c.W, N = c.N;
   switch (c.pc.lhat) {
     case WF4DVAR_L0:
       return;
-    case WF4DVAR_LI: {
-      LaunchScope ls(c, K_MODEL, 0, (double)c.s * c.ncol * 16);
-      int64_t tot = (int64_t)c.s * c.m;
-      k_window_scan<<<(unsigned)((tot + 127) / 128), 128, 0, c.st>>>(z, c.s, W, c.m,
-                                                                     transpose ? -1 : 1);
-      WF_CUDA(cudaGetLastError());
-      c.launches++;
+    case WF4DVAR_LI:
+      li_scan(c, transpose, z);
       return;
-    }
     default: break;
   }
-  const int k = (c.pc.lhat == WF4DVAR_LEXACT) ? W : c.pc.k;
+  const int k = (c.pc.lhat == WF4DVAR_LEXACT) ? c.WG : c.pc.k;
   if (k <= 1) return;
-  if (!transpose) {
-    // chain step j: z_w = r_w + M_w z_{w-1} for w = ck + j (Lemma 4.2 substitution)
-    for (int j = 1; j < k && j <= N; ++j) {
-      int nw = (N - j) / k + 1;
-      model_step(c, false, 1.0, z, z, z, j, k, nw);
+  const std::vector<ChainStep> plan = chain_plan(c.WG, k, c.w0, c.w0 + c.W, transpose);
+  const size_t cnt = (size_t)c.s * c.m;
+  for (const ChainStep &st : plan) {
+    if (c.comm && (st.recv || st.send)) {
+      // chain hand-off across the rank boundary (Lemma 4.2's serial product)
+      std::vector<Comm::P2P> ops;
+      const int rank = c.comm->rank;
+      if (!transpose) {
+        if (st.send) {
+          pack_window(c, c.pack_hi, z, c.W - 1);
+          ops.push_back({c.pack_hi, cnt, rank + 1, true});
+        }
+        if (st.recv) ops.push_back({c.halo_lo, cnt, rank - 1, false});
+      } else {
+        if (st.send) {
+          pack_window(c, c.pack_lo, z, 0);
+          ops.push_back({c.pack_lo, cnt, rank - 1, true});
+        }
+        if (st.recv) ops.push_back({c.halo_hi, cnt, rank + 1, false});
+      }
+      c.comm->exchange(ops, c.st);
     }
-  } else {
-    // backward: z_w = r_w + M_{w+1}^T z_{w+1} while w+1 stays in w's chain
-    const int nfull = W / k, last_len = W - nfull * k;
-    for (int j = 1; j < k; ++j) {
-      // full chains: w = ck + (k-1-j)
-      if (nfull > 0) model_step(c, true, 1.0, z, z, z, k - 1 - j, k, nfull);
-      // ragged last chain [nfull*k, W): w = W-1-j
-      if (last_len > 0 && j < last_len) model_step(c, true, 1.0, z, z, z, W - 1 - j, 1, 1);
-    }
+    for (int l = 0; l < st.nl; ++l)
+      model_step(c, transpose, 1.0, z, z, z, st.first[l], st.stride[l], st.count[l]);
   }
 }
 

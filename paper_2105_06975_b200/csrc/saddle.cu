@@ -34,24 +34,36 @@ static void d_product(Ctx &c, const double *X, double *Y, const double *Z, doubl
   const int s = c.s, m = c.m;
   const int64_t ld = c.ncol;
   GemmProb g[2];
-  g[0] = gp(c.B, s, X, ld, Y, ld, Z, ld, s, m, s, alpha, beta);
-  g[1] = gp(c.Q, s, X + m, ld, Y + m, ld, Z ? Z + m : nullptr, ld, s, (int)(ld - m), s, alpha, beta);
-  launch_gemm(c, g, c.W > 1 ? 2 : 1, 1);
-  c.n_D += c.W;
+  if (c.w0 == 0) {   // this rank owns window 0 (B); Q on the rest
+    g[0] = gp(c.B, s, X, ld, Y, ld, Z, ld, s, m, s, alpha, beta);
+    g[1] = gp(c.Q, s, X + m, ld, Y + m, ld, Z ? Z + m : nullptr, ld, s, (int)(ld - m), s, alpha, beta);
+    launch_gemm(c, g, c.W > 1 ? 2 : 1, 1);
+  } else {
+    g[0] = gp(c.Q, s, X, ld, Y, ld, Z, ld, s, (int)ld, s, alpha, beta);
+    launch_gemm(c, g, 1, 1);
+  }
+  c.n_D += c.WG;
 }
 
 void dhat_inv(Ctx &c, const double *x1, double *y1) {
   const int s = c.s, m = c.m;
   const int64_t ld = c.ncol;
   TrsmProb f[2], b[2];
-  f[0] = TrsmProb{c.GB, s, x1, ld, y1, ld, s, m, 0};
-  f[1] = TrsmProb{c.GQ, s, x1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
-  b[0] = TrsmProb{c.GBt, s, y1, ld, y1, ld, s, m, 0};
-  b[1] = TrsmProb{c.GQt, s, y1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
-  int np = c.W > 1 ? 2 : 1;
+  int np;
+  if (c.w0 == 0) {
+    f[0] = TrsmProb{c.GB, s, x1, ld, y1, ld, s, m, 0};
+    f[1] = TrsmProb{c.GQ, s, x1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
+    b[0] = TrsmProb{c.GBt, s, y1, ld, y1, ld, s, m, 0};
+    b[1] = TrsmProb{c.GQt, s, y1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
+    np = c.W > 1 ? 2 : 1;
+  } else {
+    f[0] = TrsmProb{c.GQ, s, x1, ld, y1, ld, s, (int)ld, 0};
+    b[0] = TrsmProb{c.GQt, s, y1, ld, y1, ld, s, (int)ld, 0};
+    np = 1;
+  }
   launch_trsm(c, f, np, false);
   launch_trsm(c, b, np, true);
-  c.n_Dhat_inv += c.W;
+  c.n_Dhat_inv += c.WG;
 }
 
 void rhat_inv(Ctx &c, const double *x2, double *y2) {
@@ -67,7 +79,7 @@ void rhat_inv(Ctx &c, const double *x2, double *y2) {
   launch_trsm(c, &f, 1, false);
   launch_trsm(c, &b, 1, true);
   if (c.pc.rhat == WF4DVAR_RME) lowrank_correct(c, y2, x2);
-  c.n_Rhat_inv += c.W;
+  c.n_Rhat_inv += c.WG;
 }
 
 static int n_model_blocks(const Ctx &c) {
@@ -97,6 +109,24 @@ void apply_A(Ctx &c, const double *x, double *y) {
   const int64_t ld = c.ncol;
   const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
   double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  if (c.comm) {
+    // one-state halos: L needs x3 of global window w0-1 (rank-1's
+    // last), L^T needs x1 of window w0+W (rank+1's first)
+    const int rank = c.comm->rank, world = c.comm->world;
+    const size_t cnt = (size_t)s * c.m;
+    std::vector<Comm::P2P> ops;
+    if (rank + 1 < world) {
+      pack_window(c, c.pack_hi, x3, c.W - 1);
+      ops.push_back({c.pack_hi, cnt, rank + 1, true});
+      ops.push_back({c.halo_hi, cnt, rank + 1, false});
+    }
+    if (rank > 0) {
+      pack_window(c, c.pack_lo, x1, 0);
+      ops.push_back({c.pack_lo, cnt, rank - 1, true});
+      ops.push_back({c.halo_lo, cnt, rank - 1, false});
+    }
+    c.comm->exchange(ops, c.st);
+  }
   // the three output blocks are independent: c2 and c3 run on the aux streams
   fork(c);
   {
@@ -114,7 +144,7 @@ void apply_A(Ctx &c, const double *x, double *y) {
   model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
   d_product(c, x1, y1, y1, 1.0, 1.0);
   join(c);
-  c.n_R += c.W;
+  c.n_R += c.WG;
   c.n_M += 2 * c.N;
   c.n_A++;
 }

@@ -165,6 +165,11 @@ void reduce_final(Ctx &c, const double *part, int nparts, int nd, double *out) {
   k_dots_final<<<(nd * c.m + 7) / 8, 256, 0, c.st>>>(part, nparts, nd, c.m, out);
   WF_CUDA(cudaGetLastError());
   c.launches++;
+  allreduce(c, out, (size_t)nd * c.m);
+}
+
+void allreduce(Ctx &c, double *buf, size_t count) {
+  if (c.comm) c.comm->allreduce_sum(buf, count, c.st);
 }
 
 void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_t n, double *out) {

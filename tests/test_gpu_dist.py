@@ -1,0 +1,196 @@
+"""GPU: the time-window-sharded path on one device.
+
+world ranks are host threads of this process, each with its own context and
+stream, joined by the library's LOCAL transport (wf4dvar_local_group): the same
+sharded kernels, halo exchanges, chain hand-offs, L_I allgather and Krylov
+allreduces that the NCCL transport carries between GPUs, with stream-ordered
+device copies instead of NVLink messages (no kernel waits on another).
+
+Criteria: the sharded apply_A / apply_P, assembled from the
+ranks' local windows, equal the single-rank result to <= 1e-13 relative (the
+per-column arithmetic does not change with the partition) and the oracle to the
+parity tolerances; sharded solves reach the single-rank solution to 1e-9 with
+iteration counts within the rounding envelope.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from synth import configs as SC
+from synth.layout import to_paper_order
+
+from .helpers import OracleCols, rel_err_cols, seeded_vec
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def WF():
+    import paper_2105_06975_b200 as W
+    return W
+
+
+def run_ranks(world, fn):
+    """fn(rank) on `world` threads; returns the results in rank order."""
+    out, err = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            torch.cuda.set_device(0)
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
+class Sharded:
+    def __init__(self, prob, pc, world):
+        W = WF()
+        self.prob, self.world = prob, world
+        self.group = W.LocalGroup(world)
+        self.streams = [torch.cuda.Stream() for _ in range(world)]
+        self.ctx = [W.Context.from_problem(prob, pc, rank=r, world=world, local_group=self.group,
+                                           stream=self.streams[r].cuda_stream)
+                    for r in range(world)]
+        self.bounds = [(c.w_begin, c.w_end) for c in self.ctx]
+
+    def local(self, vec, r):
+        p = self.prob
+        b, e = self.bounds[r]
+        return torch.from_numpy(WF().local_windows(vec, p.s, p.p, p.W, p.m, b, e)).cuda()
+
+    def gather(self, parts):
+        p = self.prob
+        return WF().global_windows([t.cpu().numpy() for t in parts], p.s, p.p, p.m, self.bounds)
+
+    def apply(self, which, vec):
+        xs = [self.local(vec, r) for r in range(self.world)]
+        ys = [torch.empty_like(x) for x in xs]
+
+        def fn(r):
+            with torch.cuda.stream(self.streams[r]):
+                getattr(self.ctx[r], which)(xs[r], ys[r])
+            self.streams[r].synchronize()
+            return ys[r]
+        return self.gather(run_ranks(self.world, fn))
+
+    def solve(self, rhs, **kw):
+        bs = [self.local(rhs, r) for r in range(self.world)]
+        xs = [torch.empty_like(b) for b in bs]
+        reps = run_ranks(self.world, lambda r: self.ctx[r].solve(bs[r], xs[r], **kw))
+        return self.gather(xs), reps
+
+    def close(self):
+        for c in self.ctx:
+            c.close()
+        self.group.close()
+
+
+def single(prob, pc):
+    return WF().Context.from_problem(prob, pc)
+
+
+def apply1(ctx, which, vec):
+    x = torch.from_numpy(vec).cuda()
+    y = torch.empty_like(x)
+    getattr(ctx, which)(x, y)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+PROBS = {
+    "heat": lambda: SC.custom_problem(s=200, N=9, q=2, m=5, seed0=3),
+    "dense": lambda: SC.random_dense_problem(s=70, p=37, N=6, m=3, seed=1),
+    "l96": lambda: SC.make_problem(2, m=8, N=9),
+}
+CELLS = [
+    dict(shape="PD", lhat="LM", k=3, rhat="exact"),     # chains cross rank boundaries
+    dict(shape="PD", lhat="LM", k=5, rhat="me"),
+    dict(shape="PD", lhat="LI", k=1, rhat="rr"),        # L_I: allgather of totals
+    dict(shape="PI", lhat="L", k=1, rhat="exact"),      # exact L: rank-serial chain
+    dict(shape="PI", lhat="LM", k=2, rhat="block", block=5),
+    dict(shape="PD", lhat="L0", k=1, rhat="diag"),
+]
+
+
+@pytest.mark.parametrize("name", list(PROBS))
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_applies_match_single_rank_and_oracle(name, world):
+    prob = PROBS[name]()
+    ora = OracleCols(prob, cols=[0, prob.m - 1])
+    x = seeded_vec(prob.n, 11)
+    for pc in CELLS:
+        one = single(prob, pc)
+        sh = Sharded(prob, pc, world)
+        try:
+            for which in ("apply_A", "apply_P"):
+                y1 = apply1(one, which, x)
+                yg = sh.apply(which, x)
+                assert rel(yg, y1) <= 1e-13, (name, world, pc, which, rel(yg, y1))
+                ref = ora.apply_A(x) if which == "apply_A" else ora.apply_P(pc, x)
+                errs = rel_err_cols(yg, ref, prob)
+                tol = 1e-12 if which == "apply_A" else 1e-9
+                assert max(errs.values()) <= tol, (name, world, pc, which, errs)
+        finally:
+            sh.close()
+            one.close()
+
+
+@pytest.mark.parametrize("solver,pc", [
+    ("minres", dict(shape="PD", lhat="LM", k=3, rhat="exact")),
+    ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr")),
+])
+def test_sharded_solve_matches_single_rank(solver, pc):
+    prob = SC.custom_problem(s=200, N=9, q=2, m=5, seed0=3)
+    one = single(prob, pc)
+    b = torch.from_numpy(prob.rhs).cuda()
+    x1 = torch.empty_like(b)
+    r1 = one.solve(b, x1, solver=solver, tol=1e-10, maxit=3000, restart=50)
+    for world in (2, 4):
+        sh = Sharded(prob, pc, world)
+        try:
+            xg, reps = sh.solve(prob.rhs, solver=solver, tol=1e-10, maxit=3000, restart=50)
+            for rp in reps[1:]:   # every rank takes the same decisions
+                assert (rp["iters"] == reps[0]["iters"]).all()
+            assert all(reps[0]["converged"])
+            assert np.max(np.abs(reps[0]["iters"] - r1["iters"])) <= 3, (reps[0]["iters"], r1["iters"])
+            P1 = to_paper_order(x1.cpu().numpy(), prob.s, prob.p, prob.W, prob.m)
+            Pg = to_paper_order(xg, prob.s, prob.p, prob.W, prob.m)
+            for c in range(prob.m):
+                assert rel(Pg[c], P1[c]) <= 1e-9
+            assert reps[0]["n_apply_A"] == r1["n_apply_A"] or abs(
+                reps[0]["n_apply_A"] - r1["n_apply_A"]) <= 3
+        finally:
+            sh.close()
+    one.close()
+
+
+def test_sharded_c3_shape_aligned_chains():
+    """configs[3]'s structure scaled down (k = 4 dividing every rank's windows,
+    dense SOAR covariances, stride-4 observations), 4 ranks."""
+    prob = SC.custom_problem(s=256, N=15, q=4, m=4, seed0=9, Bp=(0.01, 1.0),
+                             Qp=(0.01, 0.1), Rp=(0.005, 0.05))
+    pc = dict(shape="PD", lhat="LM", k=4, rhat="exact")
+    one = single(prob, pc)
+    sh = Sharded(prob, pc, 4)
+    try:
+        x = seeded_vec(prob.n, 3)
+        for which in ("apply_A", "apply_P"):
+            assert rel(sh.apply(which, x), apply1(one, which, x)) <= 1e-13
+    finally:
+        sh.close()
+        one.close()
