@@ -214,6 +214,50 @@ static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int
   c.launches++;
 }
 
+// Recursive blocked TRSM over rows [lo, hi) (Elmroth-Gustavson style): solve one
+// half, couple it to the other half with ONE DMMA GEMM (K = half the range), solve
+// the other half.  Half the triangle's flops land in the top-level GEMM (K = n/2),
+// a quarter in K = n/4 GEMMs, ...; only ranges <= leaf rows go to the panel kernel.
+// src_x: the rows of this range still hold only X (no coupling wrote Y yet).
+static void trsm_rec(Ctx &c, const TrsmProb *probs, int np, bool upper, int lo, int hi, int leaf,
+                     bool src_x) {
+  auto with_src = [&](TrsmProb *cur, bool from_x) {
+    for (int i = 0; i < np; ++i) {
+      cur[i] = probs[i];
+      if (!from_x) { cur[i].X = cur[i].Y; cur[i].ldx = cur[i].ldy; }
+    }
+  };
+  TrsmProb cur[2];
+  if (hi - lo <= leaf) {
+    with_src(cur, src_x);
+    trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
+    return;
+  }
+  // split at a multiple of the 64-row tile, near the middle
+  int mid = lo + (((hi - lo) / 2 + TB - 1) / TB) * TB;
+  if (mid >= hi) mid = lo + (hi - lo) / 2;
+  const int f_lo = upper ? mid : lo, f_hi = upper ? hi : mid;     // solved first
+  const int s_lo = upper ? lo : mid, s_hi = upper ? mid : hi;     // coupled, solved second
+  trsm_rec(c, probs, np, upper, f_lo, f_hi, leaf, src_x);
+  GemmProb g[2];
+  for (int i = 0; i < np; ++i) {
+    const TrsmProb &P = probs[i];
+    GemmProb &q = g[i];
+    q = GemmProb{};
+    q.A = P.G + (int64_t)s_lo * P.ldg + f_lo; q.lda = P.ldg;
+    q.X = P.Y + (int64_t)f_lo * P.ldy; q.ldx = P.ldy;
+    q.Y = P.Y + (int64_t)s_lo * P.ldy; q.ldy = P.ldy;
+    if (src_x) { q.Z = P.X + (int64_t)s_lo * P.ldx; q.ldz = P.ldx; }
+    else { q.Z = q.Y; q.ldz = P.ldy; }
+    q.M = s_hi - s_lo; q.N = P.ncols; q.K = f_hi - f_lo;
+    q.alpha = -1.0; q.beta = 1.0;
+  }
+  c.gemm_cls = K_TRSM_UPD;
+  launch_gemm(c, g, np, 1);
+  c.gemm_cls = K_GEMM;
+  trsm_rec(c, probs, np, upper, s_lo, s_hi, leaf, false);
+}
+
 void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   TrsmProb probs[2];
   int np = 0;
@@ -224,6 +268,15 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   const int blk = probs[0].blk;
   if (blk > 0) {   // block-diagonal factor: independent segments
     trsm_segments(c, probs, np, upper, 0, blk, n);
+    return;
+  }
+  static int leaf_env = -1;
+  if (leaf_env < 0) {
+    const char *e = getenv("WF4DVAR_TRSM_LEAF");   // tuning experiments only (0 = blocked)
+    leaf_env = e ? atoi(e) : 256;
+  }
+  if (leaf_env > 0 && n > leaf_env) {
+    trsm_rec(c, probs, np, upper, 0, n, leaf_env, true);
     return;
   }
   static int sb_env = -1;
