@@ -4,6 +4,7 @@
 // D x1 (B on window-0 columns, Q on the rest -- two groups in one launch),
 // R x2 + H x3 (the H gather is the zrow epilogue), D c1 inside S_hat^{-1} and
 // P_I, and dense-M_w model products (batched over windows).
+#include <algorithm>
 #include <cstdlib>
 
 #include "dmma.cuh"
@@ -15,6 +16,7 @@ struct GemmLaunch {
   GemmProb p[2];
   int tiles0;       // tiles of group 0 (per batch)
   int tm[2], tn[2];
+  int gm;           // raster group height (M-tiles sharing each X panel in L2)
 };
 
 template <class C, bool V16>
@@ -25,9 +27,10 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
   if (tile >= L.tiles0) { tile -= L.tiles0; gi = 1; }
   const GemmProb &P = L.p[gi];
   const int b = blockIdx.z;
-  // grouped raster: 8 M-tiles per group share X panels in L2
+  // grouped raster: GM M-tiles per group share X panels in L2 while the group's A
+  // rows stay resident (ncu r01b: GM = 8 re-read X 8x from DRAM at configs[3])
   const int tm_all = L.tm[gi], tn_all = L.tn[gi];
-  constexpr int GM = 8;
+  const int GM = L.gm;
   int group = tile / (GM * tn_all);
   int first_m = group * GM;
   int gsize = min(tm_all - first_m, GM);
@@ -107,6 +110,23 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     tiles += t;
   }
   if (nprob == 1) L.tiles0 = tiles;
+  // raster group height: one wave of resident CTAs (~2 per SM) touches gm A row
+  // panels and (2*148/gm) X column panels; pick the gm minimising that L2 footprint
+  // (~sqrt(2*148*BN/BM)), capped at the M-tiles of the problem
+  {
+    static int gm_env = -2;
+    if (gm_env == -2) {
+      const char *e = getenv("WF4DVAR_GEMM_GM");   // tuning experiments only
+      gm_env = e ? atoi(e) : -1;
+    }
+    int best = 1;
+    double best_fp = 1e300;
+    for (int g = 1; g <= 64; g *= 2) {
+      double fp = (double)g * C::BM + std::max(1.0, 2.0 * 148 / g) * C::BN;
+      if (fp <= best_fp) { best_fp = fp; best = g; }
+    }
+    L.gm = std::max(1, std::min(gm_env > 0 ? gm_env : best, L.tm[0]));
+  }
   size_t smem = C::SMEM_DOUBLES * sizeof(double);
   dim3 grid(tiles, 1, batch);
   if (v16) {
