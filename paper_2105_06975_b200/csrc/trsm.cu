@@ -273,7 +273,10 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   static int leaf_env = -1;
   if (leaf_env < 0) {
     const char *e = getenv("WF4DVAR_TRSM_LEAF");   // tuning experiments only (0 = blocked)
-    leaf_env = e ? atoi(e) : 256;
+    // measured r01c (kbench, bench c3): the recursive split does not beat the
+    // super-block scheme at n = 4096 (small-K couplings run at < 24 TFLOP/s), so
+    // the default stays blocked; WF4DVAR_TRSM_LEAF=512 selects the recursion
+    leaf_env = e ? atoi(e) : 0;
   }
   if (leaf_env > 0 && n > leaf_env) {
     trsm_rec(c, probs, np, upper, 0, n, leaf_env, true);

@@ -150,30 +150,35 @@ def test_sharded_applies_match_single_rank_and_oracle(name, world):
             one.close()
 
 
-@pytest.mark.parametrize("solver,pc", [
-    ("minres", dict(shape="PD", lhat="LM", k=3, rhat="exact")),
-    ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr")),
+@pytest.mark.parametrize("solver,pc,restart,dit", [
+    ("minres", dict(shape="PD", lhat="LM", k=3, rhat="exact"), 50, 3),
+    # full GMRES: iteration counts are robust to the summation order of the
+    # rank-partitioned inner products ...
+    ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr"), 0, 3),
+    # ... restarted GMRES(50) is not (its stagnation plateaus move by tens of
+    # iterations under 1e-16 perturbations, SURVEY PROBE-3): solution only
+    ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr"), 50, None),
 ])
-def test_sharded_solve_matches_single_rank(solver, pc):
+def test_sharded_solve_matches_single_rank(solver, pc, restart, dit):
     prob = SC.custom_problem(s=200, N=9, q=2, m=5, seed0=3)
     one = single(prob, pc)
     b = torch.from_numpy(prob.rhs).cuda()
     x1 = torch.empty_like(b)
-    r1 = one.solve(b, x1, solver=solver, tol=1e-10, maxit=3000, restart=50)
+    r1 = one.solve(b, x1, solver=solver, tol=1e-10, maxit=1500, restart=restart)
+    assert all(r1["converged"])
     for world in (2, 4):
         sh = Sharded(prob, pc, world)
         try:
-            xg, reps = sh.solve(prob.rhs, solver=solver, tol=1e-10, maxit=3000, restart=50)
+            xg, reps = sh.solve(prob.rhs, solver=solver, tol=1e-10, maxit=1500, restart=restart)
             for rp in reps[1:]:   # every rank takes the same decisions
                 assert (rp["iters"] == reps[0]["iters"]).all()
             assert all(reps[0]["converged"])
-            assert np.max(np.abs(reps[0]["iters"] - r1["iters"])) <= 3, (reps[0]["iters"], r1["iters"])
+            if dit is not None:
+                assert np.max(np.abs(reps[0]["iters"] - r1["iters"])) <= dit, (reps[0]["iters"], r1["iters"])
             P1 = to_paper_order(x1.cpu().numpy(), prob.s, prob.p, prob.W, prob.m)
             Pg = to_paper_order(xg, prob.s, prob.p, prob.W, prob.m)
             for c in range(prob.m):
                 assert rel(Pg[c], P1[c]) <= 1e-9
-            assert reps[0]["n_apply_A"] == r1["n_apply_A"] or abs(
-                reps[0]["n_apply_A"] - r1["n_apply_A"]) <= 3
         finally:
             sh.close()
     one.close()
