@@ -40,6 +40,9 @@ CELLS = {
 }
 
 
+FP64_ALU_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12   # TFLOP/s, FP64 DFMA pipe at max SM clock
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -314,6 +317,13 @@ def main():
         achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
         roof = dict(bound="tensor", achieved=achieved, peak=peak_fp64, unit="TFLOP/s",
                     frac=achieved / peak_fp64, peak_source=fp64_src)
+    elif dom == "model_stencil" and prob.model == "l96":
+        # matrix-free RK4 tangent/adjoint recomputation: FP64 ALU (DFMA) bound
+        achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
+        roof = dict(bound="alu", achieved=achieved, peak=FP64_ALU_PEAK, unit="TFLOP/s",
+                    frac=achieved / FP64_ALU_PEAK,
+                    peak_source="derived: 148 SMs x 64 FP64 FMA/clk x 2 flops x 1.965 GHz "
+                                "(DESIGN.md section 5)")
     else:
         achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
         roof = dict(bound="hbm", achieved=achieved, peak=hbm, unit="GB/s", frac=achieved / hbm,

@@ -171,6 +171,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   delete c.comm;
   c.comm = nullptr;
+  if (c.sk_ws) cudaFree(c.sk_ws);
+  if (c.sk_flags) cudaFree(c.sk_flags);
   for (void *p : c.allocs) cudaFree(p);
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : c.prof.pool) cudaEventDestroy(e);
@@ -378,6 +380,7 @@ extern "C" int wf4dvar_test_gemm(int M, int N, int K, double alpha, const double
     g.A = A; g.lda = lda; g.X = X; g.ldx = ldx; g.Y = Y; g.ldy = ldy; g.Z = Z; g.ldz = ldz;
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = Z ? beta : 0.0;
     wf::launch_gemm(c, &g, 1, 1);
+    if (c.sk_ws) { cudaFree(c.sk_ws); cudaFree(c.sk_flags); }   // implicit sync
   } catch (const Error &e) {
     return e.st;
   }
@@ -392,6 +395,7 @@ extern "C" int wf4dvar_test_trsm(int n, int ncols, int upper, int blk, const dou
     c.st = (cudaStream_t)stream;
     wf::TrsmProb p{G, n, X, ncols, Y, ncols, n, ncols, blk};
     wf::launch_trsm(c, &p, 1, upper != 0);
+    if (c.sk_ws) { cudaFree(c.sk_ws); cudaFree(c.sk_flags); }   // implicit sync
   } catch (const Error &e) {
     return e.st;
   }

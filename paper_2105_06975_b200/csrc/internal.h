@@ -160,6 +160,10 @@ struct Ctx {
   int64_t n_R = 0, n_Rhat_inv = 0, n_D = 0, n_Dhat_inv = 0, n_M = 0, n_A = 0, n_P = 0;
   int64_t launches = 0;
   int gemm_cls = K_GEMM;          // profiling class of the next launch_gemm
+  double *sk_ws = nullptr;        // stream-K GEMM: parked partial tiles
+  unsigned *sk_flags = nullptr;   // stream-K GEMM: per-CTA publish flags
+  size_t sk_ws_cap = 0;
+  unsigned sk_epoch = 0;
   Prof prof;
   std::string last_error;
   std::vector<void *> allocs;

@@ -151,10 +151,10 @@ def test_sharded_applies_match_single_rank_and_oracle(name, world):
 
 
 @pytest.mark.parametrize("solver,pc,restart,dit", [
-    ("minres", dict(shape="PD", lhat="LM", k=3, rhat="exact"), 50, 3),
+    ("minres", dict(shape="PD", lhat="LM", k=3, rhat="exact"), 50, 1),
     # full GMRES: iteration counts are robust to the summation order of the
     # rank-partitioned inner products ...
-    ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr"), 0, 3),
+    ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr"), 0, 1),
     # ... restarted GMRES(50) is not (its stagnation plateaus move by tens of
     # iterations under 1e-16 perturbations, SURVEY PROBE-3): solution only
     ("gmres", dict(shape="PI", lhat="LM", k=4, rhat="rr"), 50, None),
@@ -166,6 +166,16 @@ def test_sharded_solve_matches_single_rank(solver, pc, restart, dit):
     x1 = torch.empty_like(b)
     r1 = one.solve(b, x1, solver=solver, tol=1e-10, maxit=1500, restart=restart)
     assert all(r1["converged"])
+    # rounding envelope of the single-rank counts (RHS perturbed at 1e-15 relative):
+    # the sharded path sums its inner products in another order, which is exactly
+    # such a perturbation
+    rng = np.random.default_rng(0)
+    lo, hi = r1["iters"].copy(), r1["iters"].copy()
+    for _ in range(4):
+        bp = torch.from_numpy(prob.rhs * (1 + 1e-15 * rng.standard_normal(prob.n))).cuda()
+        xp = torch.empty_like(bp)
+        it = one.solve(bp, xp, solver=solver, tol=1e-10, maxit=1500, restart=restart)["iters"]
+        lo, hi = np.minimum(lo, it), np.maximum(hi, it)
     for world in (2, 4):
         sh = Sharded(prob, pc, world)
         try:
@@ -174,7 +184,8 @@ def test_sharded_solve_matches_single_rank(solver, pc, restart, dit):
                 assert (rp["iters"] == reps[0]["iters"]).all()
             assert all(reps[0]["converged"])
             if dit is not None:
-                assert np.max(np.abs(reps[0]["iters"] - r1["iters"])) <= dit, (reps[0]["iters"], r1["iters"])
+                itg = reps[0]["iters"]
+                assert ((itg >= lo - dit) & (itg <= hi + dit)).all(), (itg, lo, hi)
             P1 = to_paper_order(x1.cpu().numpy(), prob.s, prob.p, prob.W, prob.m)
             Pg = to_paper_order(xg, prob.s, prob.p, prob.W, prob.m)
             for c in range(prob.m):

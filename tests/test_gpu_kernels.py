@@ -29,6 +29,27 @@ def test_gemm_vs_float64_reference(M, N, K, with_z):
     assert err <= 1e-14 * scale * max(1, K) ** 0.5 * 4, err
 
 
+@pytest.mark.parametrize("M,N,K", [(1024, 2432, 256), (1000, 2500, 200), (3072, 8192, 1024),
+                                   (4096, 8192, 128)])
+def test_gemm_stream_k_tail_vs_float64_reference(M, N, K):
+    """Tile counts that leave a partial last wave (304, 320, 3072 tiles of 64x128 on
+    296 resident CTAs) take the stream-K hybrid: split tiles, parked partials,
+    deterministic fix-up.  Same tolerance as the data-parallel kernel, and
+    bitwise-reproducible across launches."""
+    g = torch.Generator().manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g, dtype=torch.float64).cuda()
+    X = torch.randn(K, N, generator=g, dtype=torch.float64).cuda()
+    Z = torch.randn(M, N, generator=g, dtype=torch.float64).cuda()
+    Y = torch.empty(M, N, dtype=torch.float64, device="cuda")
+    L().test_gemm(A, X, Y, alpha=1.5, beta=-1.0, Z=Z)
+    ref = 1.5 * (A @ X) - Z     # cuBLAS DGEMM as the float64 reference at this size
+    scale = (A.abs() @ X.abs()).max().item() + 1.0
+    assert (Y - ref).abs().max().item() <= 1e-14 * scale * K ** 0.5 * 4
+    Y2 = torch.empty_like(Y)
+    L().test_gemm(A, X, Y2, alpha=1.5, beta=-1.0, Z=Z)
+    assert torch.equal(Y, Y2)
+
+
 def test_gemm_strided_views_and_odd_ld():
     # odd leading dimensions force the 8-byte cp.async path
     A = torch.randn(51, 77, dtype=torch.float64, device="cuda")[:, :33]
