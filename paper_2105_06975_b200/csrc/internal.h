@@ -1,6 +1,7 @@
 // Internal declarations of the wf4dvar CUDA library (not part of the C ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
@@ -223,12 +224,19 @@ void fork(Ctx &c);   // aux streams wait for the work enqueued so far on c.st
 void join(Ctx &c);   // c.st waits for the aux streams
 
 // RAII helper that brackets one launch with profiling events.
+// It also opens an NVTX range named after the kernel class (no-op unless a tool
+// such as ncu is attached: `ncu --nvtx --nvtx-include "gemm_dmma/"` then selects
+// exactly the launches of one class).
 struct LaunchScope {
   Ctx &c; int cls; cudaEvent_t ev = nullptr;
   LaunchScope(Ctx &c_, int cls_, double flops, double bytes) : c(c_), cls(cls_) {
+    nvtxRangePushA(kClassName[cls]);
     c.prof_begin(cls, flops, bytes, &ev);
   }
-  ~LaunchScope() { c.prof_end(cls, ev); }
+  ~LaunchScope() {
+    c.prof_end(cls, ev);
+    nvtxRangePop();
+  }
 };
 
 // ---------------------------------------------------------------- ops
