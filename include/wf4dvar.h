@@ -115,6 +115,18 @@ typedef struct {
   int32_t block;      /* R_BLOCK: uniform block size (last block ragged), Alg. 1
                          with every cut applied (reading A7)                         */
   double dhat_ridge;  /* 0 => D_hat = D; > 0 => D_hat = D + ridge I         */
+  /* R_BLOCK by Algorithm 1 in full, used when pvec != NULL (then
+     `block` is ignored): pvec[0..npvec) block sizes summing to p; every first
+     super-diagonal block with scaled Frobenius norm normvec(j) < block_tol is cut
+     (block_tol = +inf cuts all: uniform blocks); maxsize > 0 splits the largest
+     block in two if it is larger; numproc > 0 merges the two smallest adjacent
+     blocks if there are more than numproc blocks, or splits the largest if there
+     are fewer than numproc - 2 (readings A7, A25).  At most 512 blocks; pvec is
+     copied. */
+  const int32_t *pvec;
+  int32_t npvec;
+  double block_tol;
+  int32_t maxsize, numproc;
 } wf4dvar_precond;
 
 /* Time-window sharding ("the model propagations M_i can be
@@ -233,6 +245,14 @@ typedef struct {
 wf4dvar_status wf4dvar_chain_plan(int32_t W, int32_t k, int32_t w_begin, int32_t w_end,
                                   int32_t transpose, wf4dvar_chain_step *out,
                                   int32_t max_steps, int32_t *n_steps);
+/* Algorithm 1 block structure of R_block, host only: R [p*p] host
+   row-major, pvec / block_tol / maxsize / numproc as in wf4dvar_precond.  Writes
+   the block starts followed by p (at most max_out entries) to starts_out and the
+   entry count (number of blocks + 1) to *n_out.  This is the setup step
+   wf4dvar_create runs for R_BLOCK with pvec != NULL. */
+wf4dvar_status wf4dvar_rblock_plan(const double *R, int32_t p, const int32_t *pvec, int32_t npvec,
+                                   double block_tol, int32_t maxsize, int32_t numproc,
+                                   int32_t *starts_out, int32_t max_out, int32_t *n_out);
 /* NCCL: rank 0 fills out[128] with a fresh ncclUniqueId (to broadcast). */
 wf4dvar_status wf4dvar_nccl_unique_id(void *out128);
 /* LOCAL transport: one group shared by `world` contexts of this process. Destroy

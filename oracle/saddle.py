@@ -40,6 +40,12 @@ class Precond:
     T: float = -1.0
     block: int = 0
     ridge: float = 0.0
+    # Algorithm 1 in full: pvec / tol / maxsize / numproc (None = uniform
+    # `block` with every cut applied, reading A7)
+    pvec: tuple = None
+    block_tol: float = float("inf")
+    maxsize: int = 0
+    numproc: int = 0
 
 
 def selection_matrix(H_idx, s):
@@ -79,9 +85,15 @@ class Saddle:
         return np.concatenate(list(a) + list(b) + list(c))
 
     def rhat_matrix(self, pc):
-        key = ("Rhat", pc.rhat, pc.gamma, pc.T, pc.block)
+        key = ("Rhat", pc.rhat, pc.gamma, pc.T, pc.block,
+               tuple(pc.pvec) if pc.pvec is not None else None, pc.block_tol, pc.maxsize,
+               pc.numproc)
         if key not in self._cache:
-            self._cache[key] = RH.rhat(self.R, pc.rhat, pc.gamma, pc.T, pc.block)
+            if pc.rhat == "block" and pc.pvec is not None:
+                self._cache[key] = RH.r_block(self.R, list(pc.pvec), pc.block_tol,
+                                              pc.maxsize or None, pc.numproc or None)[0]
+            else:
+                self._cache[key] = RH.rhat(self.R, pc.rhat, pc.gamma, pc.T, pc.block)
         return self._cache[key]
 
     def _spd_solve(self, key, mat_fn, rhs):
@@ -145,7 +157,9 @@ class Saddle:
         return self.join(c1, c2, c3)
 
     def _rhat_inv(self, pc, x2):
-        key = ("cho_Rhat", pc.rhat, pc.gamma, pc.T, pc.block)
+        key = ("cho_Rhat", pc.rhat, pc.gamma, pc.T, pc.block,
+               tuple(pc.pvec) if pc.pvec is not None else None, pc.block_tol, pc.maxsize,
+               pc.numproc)
         self.counters["Rhat_inv"] += self.W
         return [self._spd_solve(key, lambda: self.rhat_matrix(pc), x2[w]) for w in range(self.W)]
 

@@ -8,4 +8,4 @@ is no CPU fallback.
 """
 from ._lib import (Context, WF4DVarError, make_precond, version, EXPORTED,  # noqa: F401
                    LIB_PATH, LocalGroup, partition, chain_plan, nccl_unique_id, local_windows,
-                   global_windows)
+                   global_windows, rblock_plan)

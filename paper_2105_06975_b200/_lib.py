@@ -42,7 +42,8 @@ class Problem(C.Structure):
 class Precond(C.Structure):
     _fields_ = [("shape", C.c_int32), ("lhat", C.c_int32), ("k", C.c_int32), ("rhat", C.c_int32),
                 ("gamma", C.c_double), ("T", C.c_double), ("block", C.c_int32),
-                ("dhat_ridge", C.c_double)]
+                ("dhat_ridge", C.c_double), ("pvec", _ip), ("npvec", C.c_int32),
+                ("block_tol", C.c_double), ("maxsize", C.c_int32), ("numproc", C.c_int32)]
 
 
 TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
@@ -97,6 +98,8 @@ _sig = {
     "wf4dvar_chain_plan": (C.c_int, [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                      C.POINTER(ChainStep), C.c_int32, _ip]),
     "wf4dvar_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "wf4dvar_rblock_plan": (C.c_int, [_dp, C.c_int32, _ip, C.c_int32, C.c_double, C.c_int32,
+                                      C.c_int32, _ip, C.c_int32, _ip]),
     "wf4dvar_local_group_create": (C.c_int, [C.c_int32, C.POINTER(C.c_void_p)]),
     "wf4dvar_local_group_destroy": (C.c_int, [C.c_void_p]),
     "wf4dvar_last_error": (C.c_char_p, [_ctx]),
@@ -143,6 +146,22 @@ def chain_plan(W, k, w_begin, w_end, transpose):
     return [dict(j=a.j, recv=a.recv, send=a.send,
                  launches=[(a.first[l], a.stride[l], a.count[l]) for l in range(a.nl)])
             for a in arr[:n.value]]
+
+
+def rblock_plan(R, pvec, block_tol=float("inf"), maxsize=0, numproc=0):
+    """Algorithm 1 block boundaries the library computes for R_block (host only):
+    list of (start, end) diagonal blocks."""
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    pv = np.ascontiguousarray(pvec, dtype=np.int32)
+    out = np.zeros(pv.size + 3, np.int32)
+    n = C.c_int32()
+    st = _lib.wf4dvar_rblock_plan(_np_ptr(R, C.c_double), int(R.shape[0]), _np_ptr(pv, C.c_int32),
+                                  int(pv.size), float(block_tol), int(maxsize), int(numproc),
+                                  _np_ptr(out, C.c_int32), int(out.size), C.byref(n))
+    if st != 0:
+        raise WF4DVarError(st, _lib.wf4dvar_last_error(None).decode())
+    e = out[:n.value].tolist()
+    return list(zip(e[:-1], e[1:]))
 
 
 def nccl_unique_id():
@@ -220,9 +239,18 @@ RHATS = {"diag": RDIAG, "block": RBLOCK, "rr": RRR, "me": RME, "exact": REXACT}
 
 
 def make_precond(shape="PD", lhat="LM", k=4, rhat="exact", gamma=-1.0, T=-1.0, block=0,
-                 ridge=0.0):
-    return Precond(SHAPES[shape], LHATS[lhat], int(k or 1), RHATS[rhat], float(gamma), float(T),
-                   int(block or 0), float(ridge))
+                 ridge=0.0, pvec=None, block_tol=float("inf"), maxsize=0, numproc=0):
+    pc = Precond(SHAPES[shape], LHATS[lhat], int(k or 1), RHATS[rhat], float(gamma), float(T),
+                 int(block or 0), float(ridge))
+    if pvec is not None:
+        arr = np.ascontiguousarray(pvec, dtype=np.int32)
+        pc._pvec_keep = arr            # the library copies it during create/set_precond
+        pc.pvec = _np_ptr(arr, C.c_int32)
+        pc.npvec = int(arr.size)
+    pc.block_tol = float(block_tol)
+    pc.maxsize = int(maxsize or 0)
+    pc.numproc = int(numproc or 0)
+    return pc
 
 
 class Context:

@@ -42,6 +42,20 @@ void Ctx::prof_end(int cls, cudaEvent_t a) {
 using wf::Ctx;
 using wf::Error;
 
+// copy the preconditioner description, including the caller's pvec array
+static void set_pc(Ctx &c, const wf4dvar_precond &pc) {
+  c.pc = pc;
+  c.pvec_store.clear();
+  if (pc.pvec) {
+    WF_REQUIRE(pc.npvec >= 1 && pc.npvec <= 512, WF4DVAR_EINVAL, "R_block: 1 <= npvec <= 512");
+    for (int j = 0; j < pc.npvec; ++j) {
+      WF_REQUIRE(pc.pvec[j] >= 1, WF4DVAR_EINVAL, "R_block: pvec entries must be >= 1");
+      c.pvec_store.push_back(pc.pvec[j]);
+    }
+    c.pc.pvec = c.pvec_store.data();
+  }
+}
+
 template <class F>
 static wf4dvar_status guarded(wf4dvar_ctx ctx, F &&f) {
   if (!ctx) return WF4DVAR_EINVAL;
@@ -112,29 +126,29 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       c.pack_lo = c.alloc<double>(sm);
       c.pack_hi = c.alloc<double>(sm);
       c.gath = c.alloc<double>(sm * world);
-      WF_CUDA(cudaMemset(c.halo_lo, 0, sm * 8));
-      WF_CUDA(cudaMemset(c.halo_hi, 0, sm * 8));
+      WF_CUDA(cudaMemsetAsync(c.halo_lo, 0, sm * 8, c.st));
+      WF_CUDA(cudaMemsetAsync(c.halo_hi, 0, sm * 8, c.st));
     }
     c.n = (int64_t)(2 * c.s + c.p) * c.ncol;
     c.B = c.alloc<double>((size_t)c.s * c.s);
     c.Q = c.alloc<double>((size_t)c.s * c.s);
     c.R = c.alloc<double>((size_t)c.p * c.p);
-    WF_CUDA(cudaMemcpy(c.B, p.B, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
-    WF_CUDA(cudaMemcpy(c.Q, p.Q, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
-    WF_CUDA(cudaMemcpy(c.R, p.R, (size_t)c.p * c.p * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, c.B, p.B, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, c.Q, p.Q, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, c.R, p.R, (size_t)c.p * c.p * 8, cudaMemcpyHostToDevice));
     c.H_idx = c.alloc<int>(c.p);
     c.H_inv = c.alloc<int>(c.s);
     std::vector<int> inv(c.s, -1);
     for (int j = 0; j < c.p; ++j) inv[p.H_idx[j]] = j;
-    WF_CUDA(cudaMemcpy(c.H_idx, p.H_idx, c.p * 4, cudaMemcpyHostToDevice));
-    WF_CUDA(cudaMemcpy(c.H_inv, inv.data(), c.s * 4, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, c.H_idx, p.H_idx, c.p * 4, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, c.H_inv, inv.data(), c.s * 4, cudaMemcpyHostToDevice));
     wf::setup_model(c, p);
     c.ws_seg = c.alloc<double>((size_t)c.s * c.ncol);
     // dot partials: gy <= 2*148 blocks x up to 4 dots x m
     c.dot_part_cap = 4 * 148 * 4 * std::max(c.m, 256) + 4096;
     c.dot_part = c.alloc<double>(c.dot_part_cap);
     WF_CUDA(cudaMallocHost((void **)&c.hpin, 16 * sizeof(int)));
-    c.pc = *pc;
+    set_pc(c, *pc);
     wf::setup_precond(c);
     WF_CUDA(cudaStreamSynchronize(c.st));
   } catch (const Error &e) {
@@ -154,7 +168,7 @@ wf4dvar_status wf4dvar_set_precond(wf4dvar_ctx ctx, const wf4dvar_precond *pc) {
   return guarded(ctx, [&](Ctx &c) {
     WF_REQUIRE(pc, WF4DVAR_EINVAL, "pc is NULL");
     WF_CUDA(cudaStreamSynchronize(c.st));
-    c.pc = *pc;
+    set_pc(c, *pc);
     wf::setup_precond(c);
   });
 }
@@ -336,6 +350,23 @@ wf4dvar_status wf4dvar_chain_plan(int32_t W, int32_t k, int32_t w_begin, int32_t
   return WF4DVAR_OK;
 }
 
+wf4dvar_status wf4dvar_rblock_plan(const double *R, int32_t p, const int32_t *pvec, int32_t npvec,
+                                   double block_tol, int32_t maxsize, int32_t numproc,
+                                   int32_t *starts_out, int32_t max_out, int32_t *n_out) {
+  if (!R || p < 1 || !pvec || npvec < 1 || !n_out) return WF4DVAR_EINVAL;
+  try {
+    std::vector<double> Rh(R, R + (size_t)p * p);
+    std::vector<int> pv(pvec, pvec + npvec);
+    std::vector<int> st = wf::algorithm1_blocks(Rh, p, pv, block_tol, maxsize, numproc);
+    *n_out = (int32_t)st.size();
+    for (int i = 0; i < (int)st.size() && i < max_out && starts_out; ++i) starts_out[i] = st[i];
+  } catch (const Error &e) {
+    g_create_error = e.msg;
+    return e.st;
+  }
+  return WF4DVAR_OK;
+}
+
 wf4dvar_status wf4dvar_nccl_unique_id(void *out128) {
   if (!out128) return WF4DVAR_EINVAL;
   try {
@@ -348,7 +379,7 @@ wf4dvar_status wf4dvar_nccl_unique_id(void *out128) {
 }
 
 wf4dvar_status wf4dvar_local_group_create(int32_t world, void **out) {
-  if (!out || world < 1) return WF4DVAR_EINVAL;
+  if (!out || world < 1 || world > 64) return WF4DVAR_EINVAL;
   *out = wf::local_group_create(world);
   return WF4DVAR_OK;
 }
@@ -374,13 +405,12 @@ extern "C" int wf4dvar_test_gemm(int M, int N, int K, double alpha, const double
                                  int64_t ldz, double *Y, int64_t ldy, void *stream) {
   if (M < 0 || N < 0 || K < 0 || !A || !X || !Y) return WF4DVAR_EINVAL;
   try {
-    Ctx c;
+    static thread_local Ctx c;   // persistent: keeps the stream-K workspace across calls
     c.st = (cudaStream_t)stream;
     wf::GemmProb g{};
     g.A = A; g.lda = lda; g.X = X; g.ldx = ldx; g.Y = Y; g.ldy = ldy; g.Z = Z; g.ldz = ldz;
     g.M = M; g.N = N; g.K = K; g.alpha = alpha; g.beta = Z ? beta : 0.0;
     wf::launch_gemm(c, &g, 1, 1);
-    if (c.sk_ws) { cudaFree(c.sk_ws); cudaFree(c.sk_flags); }   // implicit sync
   } catch (const Error &e) {
     return e.st;
   }
@@ -391,11 +421,10 @@ extern "C" int wf4dvar_test_trsm(int n, int ncols, int upper, int blk, const dou
                                  const double *X, double *Y, void *stream) {
   if (n <= 0 || ncols <= 0 || !G || !X || !Y || blk < 0) return WF4DVAR_EINVAL;
   try {
-    Ctx c;
+    static thread_local Ctx c;
     c.st = (cudaStream_t)stream;
     wf::TrsmProb p{G, n, X, ncols, Y, ncols, n, ncols, blk};
     wf::launch_trsm(c, &p, 1, upper != 0);
-    if (c.sk_ws) { cudaFree(c.sk_ws); cudaFree(c.sk_flags); }   // implicit sync
   } catch (const Error &e) {
     return e.st;
   }

@@ -123,12 +123,14 @@ void nccl_unique_id(void *out128) {
 }
 
 // ------------------------------------------------------------------ in-process group
-// out[i] = sum_{g < G} src[g][i], fixed rank order
-__global__ void k_sum_ranks(double *out, const double *const *src, int G, int64_t count) {
+// out[i] = sum_{g < G} src[g][i], fixed rank order (pointers passed by value)
+constexpr int kMaxLocalRanks = 64;
+struct RankPtrs { const double *p[kMaxLocalRanks]; };
+__global__ void k_sum_ranks(double *out, const RankPtrs src, int G, int64_t count) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= count) return;
   double v = 0.0;
-  for (int g = 0; g < G; ++g) v += src[g][i];
+  for (int g = 0; g < G; ++g) v += src.p[g][i];
   out[i] = v;
 }
 
@@ -161,16 +163,13 @@ cudaEvent_t record_new(cudaStream_t st) {
 struct LocalComm : Comm {
   LocalGroup *g;
   int64_t gen = 0;                 // collective generation (same sequence on every rank)
-  double **d_src = nullptr;        // device array of G source pointers (k_sum_ranks)
   double *tmp = nullptr;           // reduction result staging
   size_t tmp_cap = 0;
   LocalComm(int rank_, LocalGroup *grp) : g(grp) {
     rank = rank_;
     world = grp->world;
-    WF_CUDA(cudaMalloc(&d_src, sizeof(double *) * world));
   }
   ~LocalComm() override {
-    if (d_src) cudaFree(d_src);
     if (tmp) cudaFree(tmp);
   }
   void exchange(const std::vector<P2P> &ops, cudaStream_t st) override {
@@ -251,9 +250,9 @@ struct LocalComm : Comm {
     }
     std::unique_lock<std::mutex> lk(g->mu);
     auto &cl = post(lk, buf, st);
-    WF_CUDA(cudaMemcpyAsync(d_src, cl.ptr.data(), sizeof(double *) * world,
-                            cudaMemcpyHostToDevice, st));
-    k_sum_ranks<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(tmp, d_src, world, (int64_t)count);
+    RankPtrs rp{};
+    for (int q = 0; q < world; ++q) rp.p[q] = cl.ptr[q];
+    k_sum_ranks<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(tmp, rp, world, (int64_t)count);
     WF_CUDA(cudaGetLastError());
     finish(lk, cl, st);
     WF_CUDA(cudaMemcpyAsync(buf, tmp, count * 8, cudaMemcpyDeviceToDevice, st));
@@ -269,7 +268,10 @@ struct LocalComm : Comm {
 };
 }  // namespace
 
-LocalGroup *local_group_create(int world) { return new LocalGroup(world); }
+LocalGroup *local_group_create(int world) {
+  WF_REQUIRE(world >= 1 && world <= kMaxLocalRanks, WF4DVAR_EINVAL, "local group: 1 <= world <= 64");
+  return new LocalGroup(world);
+}
 void local_group_destroy(LocalGroup *g) { delete g; }
 
 Comm *make_comm(const wf4dvar_dist &d) {

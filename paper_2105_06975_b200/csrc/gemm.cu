@@ -144,34 +144,23 @@ __global__ void __launch_bounds__(C::NT) k_gemm_sk(const GemmLaunch L, const SkA
 #pragma unroll
       for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   };
-  // ---- data-parallel part
-  for (int tile = c; tile < S.dp_tiles; tile += S.G) {
-    int gi, m0, n0;
-    tile_coords<C>(L, tile, gi, m0, n0);
-    const GemmProb &P = L.p[gi];
-    zero();
-    tile_mainloop<C, V16>(smem, acc, P.A, P.lda, P.X, P.ldx, m0, n0, 0, P.K, P.M, P.N);
-    tile_epilogue<C>(P, m0, n0, acc);
-  }
-  // ---- stream-K part: iterations [it0, it1) of the sk tiles
+  // ---- stream-K part first: iterations [range_lo(c), range_lo(c+1)) of the sk
+  // tiles.  Every range spans >= nk iterations, so it holds at most: the END piece of
+  // a tile started by CTA c-1 (c finishes it), full tiles, and the START piece of a
+  // tile CTA c+1 finishes.  The start piece is computed and published FIRST, the
+  // finisher piece LAST, so a finisher never waits behind its neighbour's full tiles.
   const int64_t T = (int64_t)S.sk_tiles * S.nk;
   auto range_lo = [&](int cc) { return (int64_t)cc * T / S.G; };
-  int64_t it = range_lo(c);
-  const int64_t it1 = range_lo(c + 1);
-  while (it < it1) {
-    const int lt = (int)(it / S.nk);
-    const int kb = (int)(it - (int64_t)lt * S.nk);
-    const int64_t ke_full = it1 - (int64_t)lt * S.nk;
-    const int ke = ke_full < S.nk ? (int)ke_full : S.nk;
+  const int64_t it0 = range_lo(c), it1 = range_lo(c + 1);
+  auto piece = [&](int lt, int kb, int ke) {
     int gi, m0, n0;
     tile_coords<C>(L, S.dp_tiles + lt, gi, m0, n0);
     const GemmProb &P = L.p[gi];
     zero();
     tile_mainloop<C, V16>(smem, acc, P.A, P.lda, P.X, P.ldx, m0, n0, kb * C::BK,
                           min(P.K, ke * C::BK), P.M, P.N);
-    const int64_t tile_lo = (int64_t)lt * S.nk;
     if (ke < S.nk) {
-      // start (or middle) piece: park the accumulators, publish
+      // start piece: park the accumulators, publish
       double *slot = S.ws + (int64_t)c * C::NT * NACC;
       int q = 0;
 #pragma unroll
@@ -183,33 +172,50 @@ __global__ void __launch_bounds__(C::NT) k_gemm_sk(const GemmLaunch L, const SkA
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) atomicExch(S.flags + c, S.epoch);
-    } else {
-      if (kb > 0) {
-        // finisher: add the parked pieces of the CTAs that started this tile in a
-        // fixed order (decreasing CTA index: c-1, c-2, ..., c0) -- deterministic,
-        // and without a second accumulator array (register budget)
-        int c0 = c;
-        while (c0 > 0 && range_lo(c0) > tile_lo) --c0;
-        for (int cc = c - 1; cc >= c0; --cc) {
-          if (threadIdx.x == 0) {
-            while (atomicAdd(S.flags + cc, 0u) != S.epoch) __nanosleep(128);
-          }
-          __syncthreads();
-          __threadfence();
-          const double *slot = S.ws + (int64_t)cc * C::NT * NACC;
-          int q = 0;
-#pragma unroll
-          for (int i = 0; i < C::FM; ++i)
-#pragma unroll
-            for (int j = 0; j < C::FN; ++j)
-#pragma unroll
-              for (int h = 0; h < 2; ++h, ++q)
-                acc[i][j][h] += __ldcg(slot + (int64_t)q * C::NT + threadIdx.x);
-        }
-      }
-      tile_epilogue<C>(P, m0, n0, acc);
+      return;
     }
-    it = tile_lo + ke;
+    if (kb > 0) {
+      // finisher: add the parked start piece(s) in a fixed order (c-1, c-2, ...)
+      const int64_t tile_lo = (int64_t)lt * S.nk;
+      int c0 = c;
+      while (c0 > 0 && range_lo(c0) > tile_lo) --c0;
+      for (int cc = c - 1; cc >= c0; --cc) {
+        if (threadIdx.x == 0) {
+          while (atomicAdd(S.flags + cc, 0u) != S.epoch) __nanosleep(64);
+        }
+        __syncthreads();
+        __threadfence();
+        const double *slot = S.ws + (int64_t)cc * C::NT * NACC;
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+          for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h, ++q)
+              acc[i][j][h] += __ldcg(slot + (int64_t)q * C::NT + threadIdx.x);
+      }
+    }
+    tile_epilogue<C>(P, m0, n0, acc);
+  };
+  const int lt_first = (int)(it0 / S.nk), kb_first = (int)(it0 - (int64_t)lt_first * S.nk);
+  const int lt_last = (int)((it1 - 1) / S.nk);
+  const int ke_last = (int)(it1 - (int64_t)lt_last * S.nk);
+  const bool first_is_end = kb_first > 0;              // finisher piece
+  const bool last_is_start = ke_last < S.nk;           // published piece
+  if (last_is_start && !(lt_last == lt_first && first_is_end))
+    piece(lt_last, lt_last == lt_first ? kb_first : 0, ke_last);
+  for (int lt = lt_first + (first_is_end ? 1 : 0); lt <= lt_last - (last_is_start ? 1 : 0); ++lt)
+    piece(lt, 0, S.nk);
+  if (first_is_end) piece(lt_first, kb_first, lt_last == lt_first ? ke_last : S.nk);
+  // ---- data-parallel part
+  for (int tile = c; tile < S.dp_tiles; tile += S.G) {
+    int gi, m0, n0;
+    tile_coords<C>(L, tile, gi, m0, n0);
+    const GemmProb &P = L.p[gi];
+    zero();
+    tile_mainloop<C, V16>(smem, acc, P.A, P.lda, P.X, P.ldx, m0, n0, 0, P.K, P.M, P.N);
+    tile_epilogue<C>(P, m0, n0, acc);
   }
 }
 

@@ -74,6 +74,7 @@ struct TrsmProb {
   double *Y;       int64_t ldy;
   int n, ncols;   // triangle order, number of right-hand-side columns
   int blk;        // 0 = dense triangle, else block-diagonal block size
+  const std::vector<int> *segs = nullptr;   // else: block-diagonal with these block starts
 };
 
 struct Ctx;
@@ -147,6 +148,8 @@ struct Ctx {
   double *GB = nullptr, *GBt = nullptr, *GQ = nullptr, *GQt = nullptr;  // chol(D_hat) & transposes
   double *GR = nullptr, *GRt = nullptr;                                  // chol(R_hat base)
   double *Rdiag_inv = nullptr;                                           // [p]
+  std::vector<int> rblk_starts;   // R_block (Algorithm 1): block starts + p (empty = uniform)
+  std::vector<int> pvec_store;    // copy of the caller's pvec (pc.pvec points here)
   double *U_me = nullptr, *Kinv_me = nullptr; int r_me = 0;              // Woodbury
   double gamma_used = 0, T_used = 0;
   // workspaces (n doubles each unless noted)
@@ -211,6 +214,17 @@ struct Ctx {
   void prof_begin(int cls, double flops, double bytes, cudaEvent_t *ev);
   void prof_end(int cls, cudaEvent_t ev);
 };
+
+// Setup copies: ordered on the context stream and complete on return.  (A plain
+// cudaMemcpy from pageable host memory may return before the DMA lands and is
+// ordered only on the legacy default stream, so a later kernel on a non-blocking
+// library stream could read a half-written buffer.)
+inline cudaError_t memcpy_sync(Ctx &c, void *dst, const void *src, size_t bytes,
+                               cudaMemcpyKind kind) {
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, c.st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(c.st);
+}
 
 // Run the enclosed launches on another stream of the context.
 // While profiling, everything stays on the main stream: per-launch event times of
@@ -288,6 +302,8 @@ void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_
           double *out);
 
 void setup_precond(Ctx &c);
+std::vector<int> algorithm1_blocks(const std::vector<double> &R, int p, const std::vector<int> &pvec,
+                                   double tol, int maxsize, int numproc);
 void free_precond(Ctx &c);
 void setup_model(Ctx &c, const wf4dvar_problem &p);
 

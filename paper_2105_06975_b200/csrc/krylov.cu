@@ -264,9 +264,9 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
     }
     std::vector<int> it(m), act(m);
     std::vector<double> rel(m);
-    WF_CUDA(cudaMemcpy(it.data(), S.iters, m * 4, cudaMemcpyDeviceToHost));
-    WF_CUDA(cudaMemcpy(act.data(), S.active, m * 4, cudaMemcpyDeviceToHost));
-    WF_CUDA(cudaMemcpy(rel.data(), S.relres, m * 8, cudaMemcpyDeviceToHost));
+    WF_CUDA(memcpy_sync(c, it.data(), S.iters, m * 4, cudaMemcpyDeviceToHost));
+    WF_CUDA(memcpy_sync(c, act.data(), S.active, m * 4, cudaMemcpyDeviceToHost));
+    WF_CUDA(memcpy_sync(c, rel.data(), S.relres, m * 8, cudaMemcpyDeviceToHost));
     for (int r = 0; r < m; ++r) {
       if (rep->iters) rep->iters[r] = it[r];
       if (rep->relres) rep->relres[r] = rel[r];
@@ -274,7 +274,7 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
     }
     if (rep->history) {
       std::vector<double> hh((size_t)(o.maxit + 1) * m, std::nan(""));
-      WF_CUDA(cudaMemcpy(hh.data(), S.hist, (size_t)(j + 1) * m * 8, cudaMemcpyDeviceToHost));
+      WF_CUDA(memcpy_sync(c, hh.data(), S.hist, (size_t)(j + 1) * m * 8, cudaMemcpyDeviceToHost));
       memcpy(rep->history, hh.data(), hh.size() * 8);
     }
   }
@@ -617,9 +617,9 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
   int active_left = 0;
   std::vector<int> act(m), it(m);
   std::vector<double> rel(m);
-  WF_CUDA(cudaMemcpy(act.data(), S.active, m * 4, cudaMemcpyDeviceToHost));
-  WF_CUDA(cudaMemcpy(it.data(), S.iters, m * 4, cudaMemcpyDeviceToHost));
-  WF_CUDA(cudaMemcpy(rel.data(), S.relres, m * 8, cudaMemcpyDeviceToHost));
+  WF_CUDA(memcpy_sync(c, act.data(), S.active, m * 4, cudaMemcpyDeviceToHost));
+  WF_CUDA(memcpy_sync(c, it.data(), S.iters, m * 4, cudaMemcpyDeviceToHost));
+  WF_CUDA(memcpy_sync(c, rel.data(), S.relres, m * 8, cudaMemcpyDeviceToHost));
   for (int r = 0; r < m; ++r) active_left += act[r];
   if (rep) {
     float ms = 0;
@@ -638,7 +638,7 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
     }
     if (rep->history) {
       std::vector<double> hh((size_t)(o.maxit + 1) * m);
-      WF_CUDA(cudaMemcpy(hh.data(), S.hist, hh.size() * 8, cudaMemcpyDeviceToHost));
+      WF_CUDA(memcpy_sync(c, hh.data(), S.hist, hh.size() * 8, cudaMemcpyDeviceToHost));
       for (int r = 0; r < m; ++r)
         for (size_t i = (size_t)it[r] + 1; i <= (size_t)o.maxit; ++i) hh[i * m + r] = std::nan("");
       memcpy(rep->history, hh.data(), hh.size() * 8);

@@ -366,8 +366,8 @@ void setup_model(Ctx &c, const wf4dvar_problem &p) {
       c.Mdense = c.alloc<double>((size_t)N * s * s);
       c.MdenseT = c.alloc<double>((size_t)N * s * s);
       for (int w = 0; w < N; ++w) {
-        WF_CUDA(cudaMemcpy(c.Mdense + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
-        WF_CUDA(cudaMemcpy(c.MdenseT + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
+        WF_CUDA(memcpy_sync(c, c.Mdense + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
+        WF_CUDA(memcpy_sync(c, c.MdenseT + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
       }
     }
   } else if (c.model == WF4DVAR_M_DENSE) {
@@ -379,8 +379,8 @@ void setup_model(Ctx &c, const wf4dvar_problem &p) {
       const double *Mw = p.M_dense + (size_t)w * s * s;
       for (int i = 0; i < s; ++i)
         for (int j = 0; j < s; ++j) Tm[(size_t)j * s + i] = Mw[(size_t)i * s + j];
-      WF_CUDA(cudaMemcpy(c.Mdense + (size_t)w * s * s, Mw, (size_t)s * s * 8, cudaMemcpyHostToDevice));
-      WF_CUDA(cudaMemcpy(c.MdenseT + (size_t)w * s * s, Tm.data(), Tm.size() * 8, cudaMemcpyHostToDevice));
+      WF_CUDA(memcpy_sync(c, c.Mdense + (size_t)w * s * s, Mw, (size_t)s * s * 8, cudaMemcpyHostToDevice));
+      WF_CUDA(memcpy_sync(c, c.MdenseT + (size_t)w * s * s, Tm.data(), Tm.size() * 8, cudaMemcpyHostToDevice));
     }
   } else if (c.model == WF4DVAR_M_L96) {
     WF_REQUIRE(p.l96_traj != nullptr || N == 0, WF4DVAR_EINVAL, "l96_traj is NULL");
@@ -390,7 +390,7 @@ void setup_model(Ctx &c, const wf4dvar_problem &p) {
     c.l96_F = p.l96_F; c.l96_dt = p.l96_dt; c.l96_nsub = p.l96_nsub;
     c.traj = c.alloc<double>((size_t)std::max(N, 1) * s * c.m);
     if (N > 0)
-      WF_CUDA(cudaMemcpy(c.traj, p.l96_traj, (size_t)N * s * c.m * 8, cudaMemcpyHostToDevice));
+      WF_CUDA(memcpy_sync(c, c.traj, p.l96_traj, (size_t)N * s * c.m * 8, cudaMemcpyHostToDevice));
   } else {
     throw Error{WF4DVAR_EINVAL, "unknown model kind"};
   }

@@ -76,6 +76,10 @@ void rhat_inv(Ctx &c, const double *x2, double *y2) {
   int blk = (c.pc.rhat == WF4DVAR_RBLOCK) ? c.pc.block : 0;
   TrsmProb f{c.GR, p, x2, ld, y2, ld, p, (int)ld, blk};
   TrsmProb b{c.GRt, p, y2, ld, y2, ld, p, (int)ld, blk};
+  if (c.pc.rhat == WF4DVAR_RBLOCK && !c.rblk_starts.empty()) {
+    f.segs = &c.rblk_starts;
+    b.segs = &c.rblk_starts;
+  }
   launch_trsm(c, &f, 1, false);
   launch_trsm(c, &b, 1, true);
   if (c.pc.rhat == WF4DVAR_RME) lowrank_correct(c, y2, x2);
@@ -274,6 +278,60 @@ void free_precond(Ctx &c) {
   c.r_me = 0;
 }
 
+// Algorithm 1, host side (setup, untimed).  pst = block starts of
+// pvec; normvec(j) = ||R(pst_j:pst_{j+1}-1, pst_{j+1}:pst_{j+2}-1)||_F /
+// sqrt(pvec_j pvec_{j+1}); every j with normvec(j) < tol cuts R at pst_{j+1}.
+// Then (readings A7/A25): one split of the largest block into two
+// halves (first half ceil(size/2)) if it exceeds maxsize; if there are more blocks
+// than numproc, the adjacent pair with the smallest combined size is merged (its
+// cross coupling restored from R), else if fewer than numproc - 2, the largest
+// block is split.  maxsize / numproc <= 0 disable those steps.
+// Returns the block starts followed by p.
+std::vector<int> algorithm1_blocks(const std::vector<double> &R, int p, const std::vector<int> &pvec,
+                                   double tol, int maxsize, int numproc) {
+  const int pn = (int)pvec.size();
+  std::vector<int> pst(pn + 1, 0);
+  for (int j = 0; j < pn; ++j) pst[j + 1] = pst[j] + pvec[j];
+  WF_REQUIRE(pst[pn] == p, WF4DVAR_EINVAL, "R_block: sum(pvec) must equal p");
+  std::vector<int> edges = {0};
+  for (int j = 0; j + 1 < pn; ++j) {
+    double fro = 0.0;
+    for (int i = pst[j]; i < pst[j + 1]; ++i)
+      for (int k = pst[j + 1]; k < pst[j + 2]; ++k) fro += R[(size_t)i * p + k] * R[(size_t)i * p + k];
+    const double normvec = std::sqrt(fro) / std::sqrt((double)pvec[j] * pvec[j + 1]);
+    if (normvec < tol) edges.push_back(pst[j + 1]);
+  }
+  edges.push_back(p);
+  auto split_largest = [&]() {
+    int bi = 0;
+    for (int b = 1; b + 1 < (int)edges.size(); ++b)
+      if (edges[b + 1] - edges[b] > edges[bi + 1] - edges[bi]) bi = b;
+    const int a = edges[bi], e = edges[bi + 1];
+    const int mid = a + (e - a + 1) / 2;
+    if (mid > a && mid < e) edges.insert(edges.begin() + bi + 1, mid);
+  };
+  int nb = (int)edges.size() - 1;
+  if (maxsize > 0) {
+    int big = 0;
+    for (int b = 0; b < nb; ++b) big = std::max(big, edges[b + 1] - edges[b]);
+    if (big > maxsize) split_largest();
+  }
+  nb = (int)edges.size() - 1;
+  if (numproc > 0) {
+    if (nb > numproc) {
+      int bi = 0, best = 1 << 30;
+      for (int b = 0; b + 1 < nb; ++b) {
+        const int sz = edges[b + 2] - edges[b];
+        if (sz < best) { best = sz; bi = b; }
+      }
+      edges.erase(edges.begin() + bi + 1);
+    } else if (nb < numproc - 2) {
+      split_largest();
+    }
+  }
+  return edges;
+}
+
 void setup_precond(Ctx &c) {
   const wf4dvar_precond &pc = c.pc;
   const int s = c.s, p = c.p;
@@ -282,7 +340,7 @@ void setup_precond(Ctx &c) {
   WF_REQUIRE(pc.rhat >= WF4DVAR_RDIAG && pc.rhat <= WF4DVAR_REXACT, WF4DVAR_EINVAL, "bad rhat");
   if (pc.lhat == WF4DVAR_LM)
     WF_REQUIRE(pc.k >= 1 && pc.k <= c.N + 1, WF4DVAR_EINVAL, "L_M(k) needs 1 <= k <= N+1");
-  if (pc.rhat == WF4DVAR_RBLOCK)
+  if (pc.rhat == WF4DVAR_RBLOCK && !pc.pvec)
     WF_REQUIRE(pc.block >= 1 && pc.block <= p, WF4DVAR_EINVAL, "R_block needs 1 <= block <= p");
   WF_REQUIRE(pc.dhat_ridge >= 0, WF4DVAR_EINVAL, "dhat_ridge must be >= 0");
   free_precond(c);
@@ -295,11 +353,11 @@ void setup_precond(Ctx &c) {
     for (int which = 0; which < 2; ++which) {
       const double *src = which == 0 ? c.B : c.Q;
       h.resize((size_t)s * s);
-      WF_CUDA(cudaMemcpy(h.data(), src, h.size() * 8, cudaMemcpyDeviceToHost));
+      WF_CUDA(memcpy_sync(c, h.data(), src, h.size() * 8, cudaMemcpyDeviceToHost));
       for (int i = 0; i < s; ++i) h[(size_t)i * s + i] += pc.dhat_ridge;
       double *tmp = nullptr;
       WF_CUDA(cudaMalloc(&tmp, h.size() * 8));
-      WF_CUDA(cudaMemcpy(tmp, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+      WF_CUDA(memcpy_sync(c, tmp, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
       try {
         chol(c, sv, tmp, s, which == 0 ? c.GB : c.GQ, which == 0 ? c.GBt : c.GQt,
              which == 0 ? "B_hat" : "Q_hat");
@@ -309,7 +367,7 @@ void setup_precond(Ctx &c) {
   }
   // ---- R_hat
   std::vector<double> Rh((size_t)p * p);
-  WF_CUDA(cudaMemcpy(Rh.data(), c.R, Rh.size() * 8, cudaMemcpyDeviceToHost));
+  WF_CUDA(memcpy_sync(c, Rh.data(), c.R, Rh.size() * 8, cudaMemcpyDeviceToHost));
   if (pc.rhat == WF4DVAR_RDIAG) {
     std::vector<double> dinv(p);
     for (int i = 0; i < p; ++i) {
@@ -317,11 +375,24 @@ void setup_precond(Ctx &c) {
       dinv[i] = 1.0 / Rh[(size_t)i * p + i];
     }
     c.Rdiag_inv = c.alloc<double>(p);
-    WF_CUDA(cudaMemcpy(c.Rdiag_inv, dinv.data(), p * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, c.Rdiag_inv, dinv.data(), p * 8, cudaMemcpyHostToDevice));
     return;
   }
   const char *name = "R";
-  if (pc.rhat == WF4DVAR_RBLOCK) {
+  c.rblk_starts.clear();
+  if (pc.rhat == WF4DVAR_RBLOCK && pc.pvec) {
+    // Algorithm 1 in full: blocks of R_block from pvec / tol / maxsize /
+    // numproc; R_block keeps R inside every retained block (including the higher
+    // super-diagonals of merged blocks) and zeros every coupling across a cut.
+    name = "R_block";
+    c.rblk_starts = algorithm1_blocks(Rh, p, c.pvec_store, pc.block_tol, pc.maxsize, pc.numproc);
+    std::vector<int> owner(p);
+    for (size_t b = 0; b + 1 < c.rblk_starts.size(); ++b)
+      for (int i = c.rblk_starts[b]; i < c.rblk_starts[b + 1]; ++i) owner[i] = (int)b;
+    for (int i = 0; i < p; ++i)
+      for (int j = 0; j < p; ++j)
+        if (owner[i] != owner[j]) Rh[(size_t)i * p + j] = 0.0;
+  } else if (pc.rhat == WF4DVAR_RBLOCK) {
     // Algorithm 1 with uniform pvec and every cut applied: block diagonal of R
     name = "R_block";
     for (int i = 0; i < p; ++i)
@@ -330,7 +401,7 @@ void setup_precond(Ctx &c) {
   }
   double *Rdev = nullptr;
   WF_CUDA(cudaMalloc(&Rdev, Rh.size() * 8));
-  WF_CUDA(cudaMemcpy(Rdev, Rh.data(), Rh.size() * 8, cudaMemcpyHostToDevice));
+  WF_CUDA(memcpy_sync(c, Rdev, Rh.data(), Rh.size() * 8, cudaMemcpyHostToDevice));
   try {
     if (pc.rhat == WF4DVAR_RRR || pc.rhat == WF4DVAR_RME) {
       std::vector<double> lam, V;
@@ -340,7 +411,7 @@ void setup_precond(Ctx &c) {
         name = "R_RR";
         c.gamma_used = pc.gamma >= 0 ? pc.gamma : lam[0];
         for (int i = 0; i < p; ++i) Rh[(size_t)i * p + i] += c.gamma_used;
-        WF_CUDA(cudaMemcpy(Rdev, Rh.data(), Rh.size() * 8, cudaMemcpyHostToDevice));
+        WF_CUDA(memcpy_sync(c, Rdev, Rh.data(), Rh.size() * 8, cudaMemcpyHostToDevice));
       } else {
         // Algorithm 3 via Woodbury on chol(R): eigenvalues below T raised to T.
         name = "R (R_ME base)";
@@ -395,8 +466,8 @@ void setup_precond(Ctx &c) {
           c.U_me = c.alloc<double>(U.size());
           c.Kinv_me = c.alloc<double>(Kinv.size());
           c.ws_lr = c.alloc<double>((size_t)r * c.ncol);
-          WF_CUDA(cudaMemcpy(c.U_me, U.data(), U.size() * 8, cudaMemcpyHostToDevice));
-          WF_CUDA(cudaMemcpy(c.Kinv_me, Kinv.data(), Kinv.size() * 8, cudaMemcpyHostToDevice));
+          WF_CUDA(memcpy_sync(c, c.U_me, U.data(), U.size() * 8, cudaMemcpyHostToDevice));
+          WF_CUDA(memcpy_sync(c, c.Kinv_me, Kinv.data(), Kinv.size() * 8, cudaMemcpyHostToDevice));
         }
       }
     }

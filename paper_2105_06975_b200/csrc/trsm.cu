@@ -30,10 +30,14 @@ template <int NB>
 using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, TRSM_STAGES>,
                                           TileCfg<64, NB, 16, 32, NB / 2, TRSM_STAGES>>::type;
 
+constexpr int kMaxSegTab = 512;   // variable block-diagonal factors (Algorithm 1 R_block)
+
 struct TrsmLaunch {
   TrsmProb p[2];
   int panels0;
   int seg_lo, seg_len, seg_hi;   // segment j covers [seg_lo + j*seg_len, min(.. + seg_len, seg_hi))
+  int ntab;                      // > 0: segment j covers [tab[j], tab[j+1]) instead
+  int tab[kMaxSegTab + 1];
 };
 
 template <int NB, bool UPPER, bool V16>
@@ -49,8 +53,8 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   if (panel >= L.panels0) { panel -= L.panels0; gi = 1; }
   const TrsmProb &P = L.p[gi];
   const int c0 = panel * NB;
-  const int slo = L.seg_lo + blockIdx.y * L.seg_len;
-  const int shi = min(L.seg_hi, slo + L.seg_len);
+  const int slo = L.ntab ? L.tab[blockIdx.y] : L.seg_lo + blockIdx.y * L.seg_len;
+  const int shi = L.ntab ? L.tab[blockIdx.y + 1] : min(L.seg_hi, slo + L.seg_len);
   if (slo >= shi) return;
   const int ntile = (shi - slo + TB - 1) / TB;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -172,15 +176,28 @@ static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
 
 // one k_trsm launch over segments [seg_lo + j*seg_len ...) of every problem
 static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int seg_lo,
-                          int seg_len, int seg_hi) {
+                          int seg_len, int seg_hi, const std::vector<int> *tab = nullptr) {
   TrsmLaunch L{};
   int total_cols = 0;
   bool v16 = (seg_len % 2 == 0) && (seg_lo % 2 == 0);
   double flops = 0, bytes = 0;
-  const int nseg = (seg_hi - seg_lo + seg_len - 1) / seg_len;
+  int nseg = (seg_hi - seg_lo + seg_len - 1) / seg_len;
   // algorithmic work: each segment of length l is a triangle of l^2/2 FMAs per column
   const int last = seg_hi - seg_lo - (nseg - 1) * seg_len;
-  const double tri = (double)(nseg - 1) * seg_len * seg_len + (double)last * last;
+  double tri = (double)(nseg - 1) * seg_len * seg_len + (double)last * last;
+  if (tab) {
+    nseg = (int)tab->size() - 1;
+    WF_REQUIRE(nseg >= 1 && nseg <= kMaxSegTab, WF4DVAR_EINVAL, "too many R_block blocks");
+    L.ntab = nseg;
+    tri = 0;
+    for (int j = 0; j <= nseg; ++j) {
+      L.tab[j] = (*tab)[j];
+      v16 = v16 && ((*tab)[j] % 2 == 0);
+      if (j < nseg) tri += (double)((*tab)[j + 1] - (*tab)[j]) * ((*tab)[j + 1] - (*tab)[j]);
+    }
+    seg_lo = (*tab)[0];
+    seg_hi = (*tab)[nseg];
+  }
   for (int i = 0; i < np; ++i) {
     L.p[i] = probs[i];
     total_cols += probs[i].ncols;
@@ -191,6 +208,7 @@ static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int
           (probs[i].ldg % 2 == 0) && (probs[i].ldy % 2 == 0);
   }
   L.seg_lo = seg_lo; L.seg_len = seg_len; L.seg_hi = seg_hi;
+  if (tab) { L.seg_lo = 0; L.seg_len = 1; }
   // panel width: as wide as possible while still filling the SMs
   const int ctas_per_col = nseg;
   int NB = 64;
@@ -266,6 +284,10 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   if (!np) return;
   const int n = probs[0].n;
   const int blk = probs[0].blk;
+  if (probs[0].segs) {   // variable block-diagonal factor (Algorithm 1): independent segments
+    trsm_segments(c, probs, np, upper, 0, 1, n, probs[0].segs);
+    return;
+  }
   if (blk > 0) {   // block-diagonal factor: independent segments
     trsm_segments(c, probs, np, upper, 0, blk, n);
     return;

@@ -209,3 +209,59 @@ def random_dense_problem(s, p, N, m, seed=0):
                    B=B, Q=Q, R=R, H_idx=H_idx, M_dense=M)
     prob.rhs = rng.standard_normal((2 * s + p) * W * m)
     return prob
+
+
+def paper_block_R(pvec, pcorr=None, seed=0, density=0.3, L=0.6, maxval=None, sigma=0.4,
+                  min_eig=0.41):
+    """The paper's block-structured synthetic R_i, reading A26:
+      * diagonal block k (size pvec_k): Hadamard product of a sparse random matrix
+        (entries U(0,1), density `density`) and a compact-support SOAR matrix on the
+        block's index circle (P:L566-568's modified SOAR with theta = pi / maxval,
+        standard SOAR form, reading A2; entries beyond maxval zero);
+      * off-diagonal block (k, l), k < l: sparse random entries in (0, pcorr_kl)
+        (pcorr_kl = 0: uncorrelated), density `density`;
+      * R = (diag blocks + upper off-diagonal blocks) + transpose ("adding the diagonal
+        blocks and upper half of the matrix and then symmetrising"; the diagonal
+        blocks therefore count twice);
+      * if lambda_min(R) < 1 the spectrum is shifted so that lambda_min = 0.41.
+    pcorr defaults to U(0, 0.3) per off-diagonal block pair.  Input data only."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    pvec = [int(v) for v in pvec]
+    p = sum(pvec)
+    st = np.concatenate([[0], np.cumsum(pvec)]).astype(int)
+    nb = len(pvec)
+    if pcorr is None:
+        pcorr = rng.uniform(0.0, 0.3, size=nb * (nb - 1) // 2)
+    U = np.zeros((p, p))
+    for k, n in enumerate(pvec):
+        mv = maxval or max(2, n // 2)
+        i = np.arange(n)
+        lag = np.abs(i[:, None] - i[None, :])
+        lag = np.minimum(lag, n - lag)
+        d = 2.0 * np.abs(np.sin(lag * (np.pi / mv) / 2.0))
+        soar = sigma * (1.0 + d / L) * np.exp(-d / L)
+        soar[lag > mv] = 0.0
+        rnd = rng.uniform(0.0, 1.0, size=(n, n)) * (rng.uniform(size=(n, n)) < density)
+        np.fill_diagonal(rnd, 1.0)
+        U[st[k]:st[k + 1], st[k]:st[k + 1]] = rnd * soar
+    q = 0
+    for k in range(nb):
+        for l in range(k + 1, nb):
+            blk = rng.uniform(0.0, 1.0, size=(pvec[k], pvec[l])) * pcorr[q]
+            blk *= rng.uniform(size=blk.shape) < density
+            U[st[k]:st[k + 1], st[l]:st[l + 1]] = blk
+            q += 1
+    R = U + U.T
+    lmin = np.linalg.eigvalsh(R)[0]
+    if lmin < 1.0:
+        R = R + (min_eig - lmin) * np.eye(p)
+    return R
+
+
+def with_R(prob, R):
+    """Copy of a problem with another observation covariance (same H, model, RHS
+    recipe except that observation noise keeps the original R draw)."""
+    import copy
+    q = copy.copy(prob)
+    q.R = np.array(R, dtype=np.float64)
+    return q

@@ -12,7 +12,10 @@ def oracle_precond(pc):
     d = dict(pc)
     return Precond(shape=d.get("shape", "PD"), lhat=d.get("lhat", "LM"), k=d.get("k", 4) or 1,
                    rhat=d.get("rhat", "exact"), gamma=d.get("gamma", -1.0), T=d.get("T", -1.0),
-                   block=d.get("block", 0), ridge=d.get("ridge", 0.0))
+                   block=d.get("block", 0), ridge=d.get("ridge", 0.0),
+                   pvec=tuple(d["pvec"]) if d.get("pvec") is not None else None,
+                   block_tol=d.get("block_tol", float("inf")), maxsize=d.get("maxsize", 0),
+                   numproc=d.get("numproc", 0))
 
 
 class OracleCols:
