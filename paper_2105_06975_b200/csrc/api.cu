@@ -2,6 +2,7 @@
 // lifetime, profiling bookkeeping; every compute step is a kernel launched
 // from saddle.cu / model.cu / gemm.cu / trsm.cu / vec.cu / krylov.cu.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -107,8 +108,15 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       c.st = (cudaStream_t)dist->stream;
     }
     WF_CUDA(cudaSetDevice(c.device));
+    if (const char *e = getenv("WF4DVAR_AUX_PRIORITY")) c.aux_priority = atoi(e) != 0;
     for (int i = 0; i < 2; ++i) {
-      WF_CUDA(cudaStreamCreateWithFlags(&c.aux[i], cudaStreamNonBlocking));
+      // the aux streams carry the latency-bound triangular solves (D_hat^{-1},
+      // R_hat^{-1}): highest priority, so their CTAs take SM slots as soon as
+      // co-running GEMM CTAs retire and the GEMMs fill the idle tensor pipes
+      int lo_pri = 0, hi_pri = 0;
+      WF_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+      WF_CUDA(cudaStreamCreateWithPriority(&c.aux[i], cudaStreamNonBlocking,
+                                           c.aux_priority ? hi_pri : 0));
       WF_CUDA(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));

@@ -132,6 +132,7 @@ struct Ctx {
   // fork/join streams: the three independent blocks of A and of P_D run concurrently
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  bool aux_priority = true;       // env WF4DVAR_AUX_PRIORITY=0 disables (experiments)
   int device = 0;
   // device data
   double *B = nullptr, *Q = nullptr, *R = nullptr;

@@ -167,13 +167,13 @@ void apply_P(Ctx &c, const double *x, double *y) {
     }
     {
       OnStream os(c, c.aux[1]);
-      double *t = c.ws_seg;
-      copy(c, t, x3, (int64_t)s * ld);
-      lhat_solve(c, true, t);                  // L_hat^{-T} x3
-      d_product(c, t, y3, nullptr, 1.0, 0.0);  // D (exact D)
-      lhat_solve(c, false, y3);                // L_hat^{-1}
+      dhat_inv(c, x1, y1);                     // latency-bound TRSM chain: priority stream
     }
-    dhat_inv(c, x1, y1);
+    double *t = c.ws_seg;
+    copy(c, t, x3, (int64_t)s * ld);
+    lhat_solve(c, true, t);                    // L_hat^{-T} x3
+    d_product(c, t, y3, nullptr, 1.0, 0.0);    // D (exact D)
+    lhat_solve(c, false, y3);                  // L_hat^{-1}
   } else {
     {
       OnStream os(c, c.aux[0]);
