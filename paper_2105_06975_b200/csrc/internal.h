@@ -144,6 +144,8 @@ struct Ctx {
   // heat stencil
   int heat_D = 0;                 // half width (0 => dense path)
   double heat_taps[65];           // taps[d + D], d in [-D, D]
+  double heat_rho = 0, heat_gain = 0;   // recursive-filter form: M = gain * (1-rho S)^-1 (1-rho S^-1)^-1
+  bool heat_iir = true;           // recursions (default) or the 2D+1-tap stencil
   // preconditioner
   wf4dvar_precond pc{};
   double *GB = nullptr, *GBt = nullptr, *GQ = nullptr, *GQt = nullptr;  // chol(D_hat) & transposes
