@@ -75,7 +75,11 @@ struct TrsmProb {
   int n, ncols;   // triangle order, number of right-hand-side columns
   int blk;        // 0 = dense triangle, else block-diagonal block size
   const std::vector<int> *segs = nullptr;   // else: block-diagonal with these block starts
+  const double *dpack = nullptr;            // optional setup pack of the diagonal tiles
 };
+struct Ctx;
+// pack of the 64x64 diagonal tiles of an n x n triangular factor (ld = n), setup time
+double *make_diag_pack(Ctx &c, const double *G, int n, bool upper);
 
 struct Ctx;
 
@@ -150,6 +154,8 @@ struct Ctx {
   wf4dvar_precond pc{};
   double *GB = nullptr, *GBt = nullptr, *GQ = nullptr, *GQt = nullptr;  // chol(D_hat) & transposes
   double *GR = nullptr, *GRt = nullptr;                                  // chol(R_hat base)
+  double *PB = nullptr, *PBt = nullptr, *PQ = nullptr, *PQt = nullptr;  // diagonal-tile packs
+  double *PR = nullptr, *PRt = nullptr;
   double *Rdiag_inv = nullptr;                                           // [p]
   std::vector<int> rblk_starts;   // R_block (Algorithm 1): block starts + p (empty = uniform)
   std::vector<int> pvec_store;    // copy of the caller's pvec (pc.pvec points here)

@@ -55,10 +55,12 @@ void dhat_inv(Ctx &c, const double *x1, double *y1) {
     f[1] = TrsmProb{c.GQ, s, x1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
     b[0] = TrsmProb{c.GBt, s, y1, ld, y1, ld, s, m, 0};
     b[1] = TrsmProb{c.GQt, s, y1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
+    f[0].dpack = c.PB; f[1].dpack = c.PQ; b[0].dpack = c.PBt; b[1].dpack = c.PQt;
     np = c.W > 1 ? 2 : 1;
   } else {
     f[0] = TrsmProb{c.GQ, s, x1, ld, y1, ld, s, (int)ld, 0};
     b[0] = TrsmProb{c.GQt, s, y1, ld, y1, ld, s, (int)ld, 0};
+    f[0].dpack = c.PQ; b[0].dpack = c.PQt;
     np = 1;
   }
   launch_trsm(c, f, np, false);
@@ -76,6 +78,8 @@ void rhat_inv(Ctx &c, const double *x2, double *y2) {
   int blk = (c.pc.rhat == WF4DVAR_RBLOCK) ? c.pc.block : 0;
   TrsmProb f{c.GR, p, x2, ld, y2, ld, p, (int)ld, blk};
   TrsmProb b{c.GRt, p, y2, ld, y2, ld, p, (int)ld, blk};
+  f.dpack = c.PR;
+  b.dpack = c.PRt;
   if (c.pc.rhat == WF4DVAR_RBLOCK && !c.rblk_starts.empty()) {
     f.segs = &c.rblk_starts;
     b.segs = &c.rblk_starts;
@@ -274,6 +278,8 @@ static void dev_free(Ctx &c, double *&ptr) {
 void free_precond(Ctx &c) {
   dev_free(c, c.GB); dev_free(c, c.GBt); dev_free(c, c.GQ); dev_free(c, c.GQt);
   dev_free(c, c.GR); dev_free(c, c.GRt); dev_free(c, c.Rdiag_inv);
+  dev_free(c, c.PB); dev_free(c, c.PBt); dev_free(c, c.PQ); dev_free(c, c.PQt);
+  dev_free(c, c.PR); dev_free(c, c.PRt);
   dev_free(c, c.U_me); dev_free(c, c.Kinv_me); dev_free(c, c.ws_lr);
   c.r_me = 0;
 }
@@ -364,6 +370,10 @@ void setup_precond(Ctx &c) {
       } catch (...) { cudaFree(tmp); throw; }
       cudaFree(tmp);
     }
+    c.PB = make_diag_pack(c, c.GB, s, false);
+    c.PBt = make_diag_pack(c, c.GBt, s, true);
+    c.PQ = make_diag_pack(c, c.GQ, s, false);
+    c.PQt = make_diag_pack(c, c.GQt, s, true);
   }
   // ---- R_hat
   std::vector<double> Rh((size_t)p * p);
@@ -474,6 +484,8 @@ void setup_precond(Ctx &c) {
     c.GR = c.alloc<double>((size_t)p * p);
     c.GRt = c.alloc<double>((size_t)p * p);
     chol(c, sv, Rdev, p, c.GR, c.GRt, name);
+    c.PR = make_diag_pack(c, c.GR, p, false);
+    c.PRt = make_diag_pack(c, c.GRt, p, true);
   } catch (...) { cudaFree(Rdev); throw; }
   cudaFree(Rdev);
 }

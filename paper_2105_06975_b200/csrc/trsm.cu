@@ -30,7 +30,8 @@ template <int NB>
 using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, TRSM_STAGES>,
                                           TileCfg<64, NB, 16, 32, NB / 2, TRSM_STAGES>>::type;
 
-constexpr int kMaxSegTab = 512;   // variable block-diagonal factors (Algorithm 1 R_block)
+constexpr int kMaxSegTab = 512;
+constexpr int kDiagPack = TB * (TB + 1) + TB;   // doubles per packed diagonal tile   // variable block-diagonal factors (Algorithm 1 R_block)
 
 struct TrsmLaunch {
   TrsmProb p[2];
@@ -68,6 +69,15 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   for (int it = 0; it < ntile; ++it) {
     const int ti = UPPER ? (ntile - 1 - it) : it;
     const int r0 = slo + ti * TB, r1 = min(shi, r0 + TB), nr = r1 - r0;
+    // ---- setup-time pack of this diagonal tile (ncu r01g: building it in-kernel from
+    // strided global loads + reciprocals was the top stall of k_trsm): one contiguous
+    // 33 KB cp.async copy straight into sG|sD, overlapped with the tile GEMM below
+    const double *dpk = (P.dpack && (r0 % TB) == 0) ? P.dpack + (int64_t)(r0 / TB) * kDiagPack
+                                                      : nullptr;
+    if (dpk) {
+      for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(sG + e, dpk + e, 16);
+      cp_async_commit();
+    }
     // ---- in-segment off-diagonal update: acc = G[r0:r1, K] * Y[K, panel]
     const int kbeg = UPPER ? r1 : slo;
     const int kend = UPPER ? shi : r0;
@@ -96,14 +106,18 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
     // ---- diagonal tile, transposed and masked:
     //   sG[c][r] = G[r0 + r][r0 + c] for r strictly below (lower) / above (upper) c, else 0;
     //   sD[r] = 1 / G[r0 + r][r0 + r]   (identity padding of a ragged last tile).
-    // Consecutive threads read consecutive columns of one row (coalesced).
-    for (int e = tid; e < TB * TB; e += 128) {
-      int r = e / TB, cc = e % TB;
-      double v = 0.0;
-      if (r < nr && cc < nr) v = G[(int64_t)(r0 + r) * P.ldg + r0 + cc];
-      if (r == cc) sD[r] = (r < nr) ? 1.0 / v : 1.0;
-      bool keep = UPPER ? (r < cc) : (r > cc);
-      sG[cc * (TB + 1) + r] = keep ? v : 0.0;
+    if (dpk) {
+      cp_async_wait<0>();   // the pack copy issued before the tile GEMM has landed
+    } else {
+      // no setup pack: build it here (consecutive threads read consecutive columns)
+      for (int e = tid; e < TB * TB; e += 128) {
+        int r = e / TB, cc = e % TB;
+        double v = 0.0;
+        if (r < nr && cc < nr) v = G[(int64_t)(r0 + r) * P.ldg + r0 + cc];
+        if (r == cc) sD[r] = (r < nr) ? 1.0 / v : 1.0;
+        bool keep = UPPER ? (r < cc) : (r > cc);
+        sG[cc * (TB + 1) + r] = keep ? v : 0.0;
+      }
     }
     __syncthreads();
     // ---- substitution: warp w solves columns w, w+4, ...; lane holds rows lane, lane+32.
@@ -155,9 +169,34 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
         if (lane + 32 < nr) Y[(int64_t)(r0 + lane + 32) * P.ldy + c0 + cc] = v1[q];
       }
     }
-    __threadfence();
-    __syncthreads();
+    __syncthreads();   // Y rows visible to the whole CTA (next tile's cp.async reads)
   }
+}
+
+// Setup: pack every 64x64 diagonal tile of a triangular factor as the kernel wants it
+// in shared memory: transposed and strictly masked (sG[c][r], stride 65) followed by
+// the 64 reciprocal diagonal entries (identity padding past n).
+__global__ void k_pack_diag(const double *G, int n, int upper, double *pack) {
+  const int t = blockIdx.x;
+  const int r0 = t * TB, nr = min(TB, n - r0);
+  double *pk = pack + (int64_t)t * kDiagPack;
+  for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+    int r = e / TB, cc = e % TB;
+    double v = (r < nr && cc < nr) ? G[(int64_t)(r0 + r) * n + r0 + cc] : 0.0;
+    if (r == cc) pk[TB * (TB + 1) + r] = (r < nr) ? 1.0 / v : 1.0;
+    bool keep = upper ? (r < cc) : (r > cc);
+    pk[cc * (TB + 1) + r] = keep ? v : 0.0;
+  }
+  for (int e = threadIdx.x; e < TB; e += blockDim.x) pk[e * (TB + 1) + TB] = 0.0;   // pad col
+}
+
+double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
+  const int nt = (n + TB - 1) / TB;
+  double *pk = c.alloc<double>((size_t)nt * kDiagPack);
+  k_pack_diag<<<nt, 256, 0, c.st>>>(G, n, upper ? 1 : 0, pk);
+  WF_CUDA(cudaGetLastError());
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  return pk;
 }
 
 template <int NB, bool UPPER>
