@@ -432,6 +432,20 @@ extern "C" int wf4dvar_test_trsm(int n, int ncols, int upper, int blk, const dou
     static thread_local Ctx c;
     c.st = (cudaStream_t)stream;
     wf::TrsmProb p{G, n, X, ncols, Y, ncols, n, ncols, blk};
+    // the production path uses setup-time diagonal-tile packs: build (and cache per
+    // factor) one here too, so kernel tests and micro-benchmarks exercise it
+    static thread_local const double *pk_G = nullptr;
+    static thread_local int pk_n = -1, pk_up = -1;
+    static thread_local double *pk = nullptr;
+    if (G != pk_G || n != pk_n || upper != pk_up) {
+      if (pk) {
+        cudaFree(pk);
+        c.allocs.clear();
+      }
+      pk = wf::make_diag_pack(c, G, n, upper != 0);
+      pk_G = G; pk_n = n; pk_up = upper;
+    }
+    p.dpack = pk;
     wf::launch_trsm(c, &p, 1, upper != 0);
   } catch (const Error &e) {
     return e.st;
