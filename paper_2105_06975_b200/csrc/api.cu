@@ -432,19 +432,18 @@ extern "C" int wf4dvar_test_trsm(int n, int ncols, int upper, int blk, const dou
     static thread_local Ctx c;
     c.st = (cudaStream_t)stream;
     wf::TrsmProb p{G, n, X, ncols, Y, ncols, n, ncols, blk};
-    // the production path uses setup-time diagonal-tile packs: build (and cache per
-    // factor) one here too, so kernel tests and micro-benchmarks exercise it
-    static thread_local const double *pk_G = nullptr;
-    static thread_local int pk_n = -1, pk_up = -1;
+    // the production path uses setup-time diagonal-tile packs: rebuild one on the same
+    // stream for every call (an address-keyed cache could go stale when the caller
+    // reuses memory), into a per-thread buffer grown on demand
     static thread_local double *pk = nullptr;
-    if (G != pk_G || n != pk_n || upper != pk_up) {
-      if (pk) {
-        cudaFree(pk);
-        c.allocs.clear();
-      }
-      pk = wf::make_diag_pack(c, G, n, upper != 0);
-      pk_G = G; pk_n = n; pk_up = upper;
+    static thread_local size_t pk_cap = 0;
+    const size_t need = (size_t)((n + 63) / 64) * (64 * 65 + 64);
+    if (need > pk_cap) {
+      if (pk) cudaFree(pk);
+      WF_CUDA(cudaMalloc(&pk, need * 8));
+      pk_cap = need;
     }
+    wf::fill_diag_pack(c, G, n, upper != 0, pk);
     p.dpack = pk;
     wf::launch_trsm(c, &p, 1, upper != 0);
   } catch (const Error &e) {

@@ -80,6 +80,7 @@ struct TrsmProb {
 struct Ctx;
 // pack of the 64x64 diagonal tiles of an n x n triangular factor (ld = n), setup time
 double *make_diag_pack(Ctx &c, const double *G, int n, bool upper);
+void fill_diag_pack(Ctx &c, const double *G, int n, bool upper, double *pack);   // async
 
 struct Ctx;
 

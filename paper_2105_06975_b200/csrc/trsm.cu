@@ -190,11 +190,16 @@ __global__ void k_pack_diag(const double *G, int n, int upper, double *pack) {
   for (int e = threadIdx.x; e < TB; e += blockDim.x) pk[e * (TB + 1) + TB] = 0.0;   // pad col
 }
 
+void fill_diag_pack(Ctx &c, const double *G, int n, bool upper, double *pk) {
+  const int nt = (n + TB - 1) / TB;
+  k_pack_diag<<<nt, 256, 0, c.st>>>(G, n, upper ? 1 : 0, pk);
+  WF_CUDA(cudaGetLastError());
+}
+
 double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
   const int nt = (n + TB - 1) / TB;
   double *pk = c.alloc<double>((size_t)nt * kDiagPack);
-  k_pack_diag<<<nt, 256, 0, c.st>>>(G, n, upper ? 1 : 0, pk);
-  WF_CUDA(cudaGetLastError());
+  fill_diag_pack(c, G, n, upper, pk);
   WF_CUDA(cudaStreamSynchronize(c.st));
   return pk;
 }
