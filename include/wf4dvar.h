@@ -80,8 +80,12 @@ typedef enum {
   WF4DVAR_M_DENSE = 0, /* M_dense[w-1] given as dense s x s row-major              */
   WF4DVAR_M_HEAT = 1,  /* M = (I - r Lap)^{-1}, Lap = periodic second difference
                           (BJ.c0-c4); applied as its exact circulant stencil        */
-  WF4DVAR_M_L96 = 2    /* tangent linear of l96_nsub RK4 steps of Lorenz-96
+  WF4DVAR_M_L96 = 2,   /* tangent linear of l96_nsub RK4 steps of Lorenz-96
                            along l96_traj, recomputed matrix-free      */
+  WF4DVAR_M_HEAT_EXPLICIT = 3 /* the paper's own heat model: M = M_dt^n,
+                          M_dt = forward-Euler Dirichlet step (first/last rows zero,
+                          interior (r, 1-2r, r)), n = heat_nsteps <= 8 per window,
+                          r = heat_r; applied as n fused 3-point sweeps          */
 } wf4dvar_model;
 
 typedef struct {
@@ -96,6 +100,13 @@ typedef struct {
   const double *l96_traj;  /* L96: [N][s][m] host, start state of window w-1 for M_w */
   double l96_F, l96_dt;    /* L96: forcing, RK4 step                                */
   int32_t l96_nsub;        /* L96: RK4 steps per window                             */
+  int32_t heat_nsteps;     /* HEAT_EXPLICIT: model steps per window, 1..8            */
+  /* General observation operator H_i (e.g. the paper's 5-point smoothed
+     observations): CSR p x s, host, same for every window.  When H_rowptr != NULL
+     it replaces H_idx (which may then be NULL); column indices in [0, s). */
+  const int32_t *H_rowptr; /* [p+1]                                                  */
+  const int32_t *H_col;    /* [H_rowptr[p]]                                           */
+  const double *H_val;     /* [H_rowptr[p]]                                           */
 } wf4dvar_problem;
 
 typedef enum { WF4DVAR_PD = 0, WF4DVAR_PI = 1 } wf4dvar_shape;

@@ -3,6 +3,9 @@
 heat_M      BJ.c0: "M_i = one implicit-Euler heat step (I - r*Lap)^-1 with the
             second-difference periodic Laplacian" (reading A12: Lap unscaled,
             circulant(-2; 1, 1)).  Plain definition: dense inverse.
+heat_explicit_M  NEXT-1: the paper's own heat model, explicit
+            forward-Euler Dirichlet step M_dt raised to the number of
+            model steps per window (Supp. P:L1134).
 l96_*       dx_i/dt = (x_{i+1}-x_{i-2})x_{i-1} - x_i + F,
             periodic, integrated with RK4 (BJ.c2: dt = 0.025, 5 substeps per
             window).  The tangent linear model is the exact derivative of the
@@ -24,6 +27,27 @@ def heat_lap(s):
 def heat_M(s, r):
     """M = (I - r Lap)^{-1}, dense (the definition)."""
     return np.linalg.inv(np.eye(s) - r * heat_lap(s))
+
+
+def heat_dirichlet_step(s, r):
+    """M_dt of the explicit Dirichlet heat model (Supp. P:L1119-1131):
+    forward Euler + centred second differences, first and last rows zero,
+    interior rows (r, 1-2r, r) on columns i-1, i, i+1 (columns 0 and s-1 carry
+    coefficient 0, as the printed matrix shows)."""
+    M = np.zeros((s, s))
+    for i in range(1, s - 1):
+        M[i, i] = 1.0 - 2.0 * r
+        if i - 1 >= 1:
+            M[i, i - 1] = r
+        if i + 1 <= s - 2:
+            M[i, i + 1] = r
+    return M
+
+
+def heat_explicit_M(s, r, nsteps):
+    """M between observation times = M_dt raised to the number of model steps per
+    window (Supp. P:L1134: "given by M_dt raised to the appropriate power")."""
+    return np.linalg.matrix_power(heat_dirichlet_step(s, r), nsteps)
 
 
 def l96_rhs(x, F=8.0):
@@ -88,6 +112,9 @@ def model_matrices(prob, col=0):
     """Dense [M_1..M_N] for RHS/problem column `col` of a synth.Problem."""
     if prob.model == "heat":
         M = heat_M(prob.s, prob.heat_r)
+        return [M] * prob.N
+    if prob.model == "heat_explicit":
+        M = heat_explicit_M(prob.s, prob.heat_r, prob.heat_nsteps)
         return [M] * prob.N
     if prob.model == "dense":
         return [prob.M_dense[w] for w in range(prob.N)]

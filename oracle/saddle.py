@@ -54,6 +54,23 @@ def selection_matrix(H_idx, s):
     return H
 
 
+def csr_matrix(rowptr, col, val, s):
+    """Dense H_i from CSR arrays (general observation operator)."""
+    p = len(rowptr) - 1
+    H = np.zeros((p, s))
+    for j in range(p):
+        for k in range(rowptr[j], rowptr[j + 1]):
+            H[j, col[k]] += val[k]
+    return H
+
+
+def obs_matrix(prob):
+    """H_i of a synth.Problem: CSR when given (prob.H_csr), else the selection H_idx."""
+    if getattr(prob, "H_csr", None) is not None:
+        return csr_matrix(*prob.H_csr, prob.s)
+    return selection_matrix(prob.H_idx, prob.s)
+
+
 class Saddle:
     """One right-hand side's saddle system (M_w may depend on the column)."""
 
@@ -62,7 +79,7 @@ class Saddle:
         self.s, self.p, self.N = prob.s, prob.p, prob.N
         self.W = prob.N + 1
         self.B, self.Q, self.R = prob.B, prob.Q, prob.R
-        self.Hi = selection_matrix(prob.H_idx, prob.s)
+        self.Hi = obs_matrix(prob)
         self.Ms = Ms if Ms is not None else model_matrices(prob, col)
         self.counters = dict(R=0, Rhat_inv=0, D=0, Dhat_inv=0, M=0)
         self._cache = {}

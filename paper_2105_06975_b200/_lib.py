@@ -20,7 +20,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 # ---------------------------------------------------------------- structs
-M_DENSE, M_HEAT, M_L96 = 0, 1, 2
+M_DENSE, M_HEAT, M_L96, M_HEAT_EXPLICIT = 0, 1, 2, 3
 PD, PI = 0, 1
 L0, LI, LM, LEXACT = 0, 1, 2, 3
 RDIAG, RBLOCK, RRR, RME, REXACT = 0, 1, 2, 3, 4
@@ -36,7 +36,8 @@ class Problem(C.Structure):
     _fields_ = [("s", C.c_int32), ("p", C.c_int32), ("N", C.c_int32), ("m", C.c_int32),
                 ("B", _dp), ("Q", _dp), ("R", _dp), ("H_idx", _ip), ("model", C.c_int32),
                 ("M_dense", _dp), ("heat_r", C.c_double), ("l96_traj", _dp),
-                ("l96_F", C.c_double), ("l96_dt", C.c_double), ("l96_nsub", C.c_int32)]
+                ("l96_F", C.c_double), ("l96_dt", C.c_double), ("l96_nsub", C.c_int32),
+                ("heat_nsteps", C.c_int32), ("H_rowptr", _ip), ("H_col", _ip), ("H_val", _dp)]
 
 
 class Precond(C.Structure):
@@ -258,7 +259,8 @@ class Context:
 
     def __init__(self, s, p, N, m, B, Q, R, H_idx, model="heat", heat_r=0.25, M_dense=None,
                  l96_traj=None, l96_F=8.0, l96_dt=0.025, l96_nsub=5, precond=None, device=0,
-                 stream=None, rank=0, world=1, nccl_id=None, local_group=None):
+                 stream=None, rank=0, world=1, nccl_id=None, local_group=None, heat_nsteps=1,
+                 H_csr=None):
         keep = []
 
         def arr(a, dt=np.float64):
@@ -273,8 +275,15 @@ class Context:
         pr = Problem()
         pr.s, pr.p, pr.N, pr.m = int(s), int(p), int(N), int(m)
         pr.B, pr.Q, pr.R = _np_ptr(Bh, C.c_double), _np_ptr(Qh, C.c_double), _np_ptr(Rh, C.c_double)
-        pr.H_idx = _np_ptr(Hh, C.c_int32)
-        pr.model = {"dense": M_DENSE, "heat": M_HEAT, "l96": M_L96}[model]
+        if Hh is not None:
+            pr.H_idx = _np_ptr(Hh, C.c_int32)
+        if H_csr is not None:
+            rp, cl, vl = arr(H_csr[0], np.int32), arr(H_csr[1], np.int32), arr(H_csr[2])
+            pr.H_rowptr, pr.H_col, pr.H_val = (_np_ptr(rp, C.c_int32), _np_ptr(cl, C.c_int32),
+                                               _np_ptr(vl, C.c_double))
+        pr.heat_nsteps = int(heat_nsteps)
+        pr.model = {"dense": M_DENSE, "heat": M_HEAT, "l96": M_L96,
+                    "heat_explicit": M_HEAT_EXPLICIT}[model]
         pr.heat_r = float(heat_r)
         if M_dense is not None:
             pr.M_dense = _np_ptr(arr(M_dense), C.c_double)
@@ -316,7 +325,9 @@ class Context:
                    model=prob.model, heat_r=getattr(prob, "heat_r", 0.25),
                    M_dense=getattr(prob, "M_dense", None), l96_traj=getattr(prob, "traj", None),
                    l96_F=getattr(prob, "F", 8.0), l96_dt=getattr(prob, "dt", 0.025),
-                   l96_nsub=getattr(prob, "nsub", 5), precond=precond, **kw)
+                   l96_nsub=getattr(prob, "nsub", 5), precond=precond,
+                   heat_nsteps=getattr(prob, "heat_nsteps", 1),
+                   H_csr=getattr(prob, "H_csr", None), **kw)
 
     def _check(self, st):
         if st != 0:

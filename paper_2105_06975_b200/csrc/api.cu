@@ -91,13 +91,22 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     const wf4dvar_problem &p = *prob;
     WF_REQUIRE(p.s >= 1 && p.p >= 1 && p.N >= 0 && p.m >= 1, WF4DVAR_EINVAL, "bad s/p/N/m");
     WF_REQUIRE(p.p <= p.s, WF4DVAR_EINVAL, "p must be <= s");
-    WF_REQUIRE(p.B && p.Q && p.R && p.H_idx, WF4DVAR_EINVAL, "B/Q/R/H_idx must be non-NULL");
-    for (int j = 0; j < p.p; ++j) {
-      WF_REQUIRE(p.H_idx[j] >= 0 && p.H_idx[j] < p.s, WF4DVAR_EINVAL, "H_idx out of range");
-      if (j) WF_REQUIRE(p.H_idx[j] > p.H_idx[j - 1], WF4DVAR_EINVAL, "H_idx not strictly increasing");
+    WF_REQUIRE(p.B && p.Q && p.R && (p.H_idx || p.H_rowptr), WF4DVAR_EINVAL,
+               "B/Q/R and H_idx or H_rowptr must be non-NULL");
+    if (p.H_rowptr) {
+      WF_REQUIRE(p.H_col && p.H_val && p.H_rowptr[0] == 0, WF4DVAR_EINVAL, "bad CSR H");
+      for (int j = 0; j < p.p; ++j)
+        WF_REQUIRE(p.H_rowptr[j + 1] >= p.H_rowptr[j], WF4DVAR_EINVAL, "CSR H rowptr not monotone");
+      for (int k = 0; k < p.H_rowptr[p.p]; ++k)
+        WF_REQUIRE(p.H_col[k] >= 0 && p.H_col[k] < p.s, WF4DVAR_EINVAL, "CSR H column out of range");
+    } else {
+      for (int j = 0; j < p.p; ++j) {
+        WF_REQUIRE(p.H_idx[j] >= 0 && p.H_idx[j] < p.s, WF4DVAR_EINVAL, "H_idx out of range");
+        if (j) WF_REQUIRE(p.H_idx[j] > p.H_idx[j - 1], WF4DVAR_EINVAL, "H_idx not strictly increasing");
+      }
     }
-    WF_REQUIRE(p.model == WF4DVAR_M_DENSE || p.model == WF4DVAR_M_HEAT || p.model == WF4DVAR_M_L96,
-               WF4DVAR_EINVAL, "unknown model");
+    WF_REQUIRE(p.model == WF4DVAR_M_DENSE || p.model == WF4DVAR_M_HEAT || p.model == WF4DVAR_M_L96 ||
+               p.model == WF4DVAR_M_HEAT_EXPLICIT, WF4DVAR_EINVAL, "unknown model");
     int rank = 0, world = 1;
     if (dist) {
       world = dist->world <= 0 ? 1 : dist->world;
@@ -144,12 +153,39 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     WF_CUDA(memcpy_sync(c, c.B, p.B, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
     WF_CUDA(memcpy_sync(c, c.Q, p.Q, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
     WF_CUDA(memcpy_sync(c, c.R, p.R, (size_t)c.p * c.p * 8, cudaMemcpyHostToDevice));
-    c.H_idx = c.alloc<int>(c.p);
-    c.H_inv = c.alloc<int>(c.s);
-    std::vector<int> inv(c.s, -1);
-    for (int j = 0; j < c.p; ++j) inv[p.H_idx[j]] = j;
-    WF_CUDA(memcpy_sync(c, c.H_idx, p.H_idx, c.p * 4, cudaMemcpyHostToDevice));
-    WF_CUDA(memcpy_sync(c, c.H_inv, inv.data(), c.s * 4, cudaMemcpyHostToDevice));
+    if (p.H_rowptr) {
+      // general H_i: CSR and its transpose (built here, host side)
+      c.H_general = true;
+      const int nnz = p.H_rowptr[c.p];
+      std::vector<int> trp(c.s + 1, 0), tcol(nnz);
+      std::vector<double> tval(nnz);
+      for (int k = 0; k < nnz; ++k) trp[p.H_col[k] + 1]++;
+      for (int i = 0; i < c.s; ++i) trp[i + 1] += trp[i];
+      std::vector<int> fill(trp.begin(), trp.end() - 1);
+      for (int j = 0; j < c.p; ++j)
+        for (int k = p.H_rowptr[j]; k < p.H_rowptr[j + 1]; ++k) {
+          int dst = fill[p.H_col[k]]++;
+          tcol[dst] = j;
+          tval[dst] = p.H_val[k];
+        }
+      c.Hrp = c.alloc<int>(c.p + 1); c.Hcol = c.alloc<int>(nnz); c.Hval = c.alloc<double>(nnz);
+      c.HTrp = c.alloc<int>(c.s + 1); c.HTcol = c.alloc<int>(nnz); c.HTval = c.alloc<double>(nnz);
+      WF_CUDA(memcpy_sync(c, c.Hrp, p.H_rowptr, (c.p + 1) * 4, cudaMemcpyHostToDevice));
+      if (nnz) {
+        WF_CUDA(memcpy_sync(c, c.Hcol, p.H_col, nnz * 4, cudaMemcpyHostToDevice));
+        WF_CUDA(memcpy_sync(c, c.Hval, p.H_val, nnz * 8, cudaMemcpyHostToDevice));
+        WF_CUDA(memcpy_sync(c, c.HTcol, tcol.data(), nnz * 4, cudaMemcpyHostToDevice));
+        WF_CUDA(memcpy_sync(c, c.HTval, tval.data(), nnz * 8, cudaMemcpyHostToDevice));
+      }
+      WF_CUDA(memcpy_sync(c, c.HTrp, trp.data(), (c.s + 1) * 4, cudaMemcpyHostToDevice));
+    } else {
+      c.H_idx = c.alloc<int>(c.p);
+      c.H_inv = c.alloc<int>(c.s);
+      std::vector<int> inv(c.s, -1);
+      for (int j = 0; j < c.p; ++j) inv[p.H_idx[j]] = j;
+      WF_CUDA(memcpy_sync(c, c.H_idx, p.H_idx, c.p * 4, cudaMemcpyHostToDevice));
+      WF_CUDA(memcpy_sync(c, c.H_inv, inv.data(), c.s * 4, cudaMemcpyHostToDevice));
+    }
     wf::setup_model(c, p);
     c.ws_seg = c.alloc<double>((size_t)c.s * c.ncol);
     // dot partials: gy <= 2*148 blocks x up to 4 dots x m

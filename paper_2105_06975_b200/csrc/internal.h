@@ -142,6 +142,12 @@ struct Ctx {
   // device data
   double *B = nullptr, *Q = nullptr, *R = nullptr;
   int *H_idx = nullptr, *H_inv = nullptr;
+  // general CSR H_i and its transpose (H^T as CSR over the s state rows)
+  int *Hrp = nullptr, *Hcol = nullptr, *HTrp = nullptr, *HTcol = nullptr;
+  double *Hval = nullptr, *HTval = nullptr;
+  bool H_general = false;
+  int heat_nsteps = 1;
+  double heat_r = 0;
   double *Mdense = nullptr;       // [N][s][s]
   double *MdenseT = nullptr;      // [N][s][s] transposes
   double *traj = nullptr;         // [N][s][m]
@@ -294,6 +300,10 @@ void dhat_inv(Ctx &c, const double *x1, double *y1);
 void allreduce(Ctx &c, double *buf, size_t count);
 // pack local window wl of an [s][W][m] segment into a contiguous [s][m] buffer
 void pack_window(Ctx &c, double *dst, const double *seg, int wl);
+
+// y[i][c] (+)= sum_k val[k] x[col[k]][c] over rows i < nrows, all ld columns (CSR)
+void csr_apply(Ctx &c, double *y, const double *x, const int *rowptr, const int *col,
+               const double *val, int nrows, bool accumulate);
 
 void apply_A(Ctx &c, const double *x, double *y);
 void apply_P(Ctx &c, const double *x, double *y);

@@ -137,6 +137,81 @@ __global__ void __launch_bounds__(128) k_heat_iir(double *out, const double *bas
   }
 }
 
+// The paper's own heat model: M = M_dt^NS, M_dt the forward-Euler
+// Dirichlet step (rows 0 and s-1 zero; interior (r, 1-2r, r), the boundary columns
+// carrying coefficient 0).  M_dt is symmetric, so M^T = M.  One thread per (window,
+// RHS) column and TI consecutive rows; the NS sweeps run in registers on the rows
+// [i0 - NS, i0 + TI + NS) (the light cone of the chunk), boundary and out-of-range
+// rows held at zero.
+template <int NS, int TI>
+__global__ void __launch_bounds__(128) k_heat_explicit(double *out, const double *base,
+                                                       const double *in, const double *add2,
+                                                       const int *row_map, double r, double sign,
+                                                       int s, int W, int m, int w_first,
+                                                       int w_step, int nw, int dir,
+                                                       const double *halo, int w0, int WG) {
+  const int64_t ld = (int64_t)W * m;
+  const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cc >= nw * m) return;
+  const int tt = cc / m, rr = cc - tt * m;
+  const int w = w_first + tt * w_step;
+  const int ws = w + dir;
+  const bool has = (w0 + ws >= 0 && w0 + ws < WG);
+  const bool from_halo = (ws < 0 || ws >= W);
+  const int64_t col = (int64_t)w * m + rr;
+  const double *src = from_halo ? halo + rr : in + (int64_t)ws * m + rr;
+  const int64_t sld = from_halo ? (int64_t)m : ld;
+  const int i0 = blockIdx.y * TI;
+  constexpr int L = TI + 2 * NS;
+  double v[L];
+  if (has) {
+#pragma unroll
+    for (int j = 0; j < L; ++j) {
+      const int i = i0 - NS + j;
+      v[j] = (i >= 1 && i <= s - 2) ? __ldg(src + (int64_t)i * sld) : 0.0;
+    }
+    const double d = 1.0 - 2.0 * r;
+#pragma unroll
+    for (int st = 0; st < NS; ++st) {
+      double prev = v[st];
+#pragma unroll
+      for (int j = st + 1; j < L - 1 - st; ++j) {
+        const int i = i0 - NS + j;
+        const double nv = (i >= 1 && i <= s - 2) ? fma(r, prev + v[j + 1], d * v[j]) : 0.0;
+        prev = v[j];
+        v[j] = nv;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 0; o < TI; ++o) {
+    const int i = i0 + o;
+    if (i < s) {
+      double val = base[i * ld + col];
+      if (has) val = fma(sign, v[NS + o], val);
+      if (add2) {
+        int j = row_map[i];
+        if (j >= 0) val += add2[(int64_t)j * ld + col];
+      }
+      out[i * ld + col] = val;
+    }
+  }
+}
+
+template <int NS>
+static void heat_explicit_launch(Ctx &c, bool transpose, double sign, const double *in,
+                                 const double *base, double *out, int w_first, int w_step,
+                                 int nw, const double *add2, const int *row_map) {
+  constexpr int TI = 32;
+  int cols = nw * c.m;
+  dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
+  k_heat_explicit<NS, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_r, sign,
+                                                   c.s, c.W, c.m, w_first, w_step, nw,
+                                                   transpose ? 1 : -1,
+                                                   transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+  WF_CUDA(cudaGetLastError());
+}
+
 // z_w += z_{w-1} (forward, w ascending) or z_w += z_{w+1} (backward): L_I^{-1} / L_I^{-T}
 __global__ void k_window_scan(double *z, int rows, int W, int m, int dir) {
   const int64_t ld = (int64_t)W * m;
@@ -199,6 +274,22 @@ void model_step(Ctx &c, bool transpose, double sign, const double *in, const dou
   const int64_t ld = c.ncol;
   if (c.model == WF4DVAR_M_L96) {
     l96_step(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map);
+    return;
+  }
+  if (c.model == WF4DVAR_M_HEAT_EXPLICIT) {
+    double elems = (double)nw * s * m;
+    LaunchScope ls(c, K_MODEL, elems * 4.0 * c.heat_nsteps, elems * 8.0 * 3);
+    switch (c.heat_nsteps) {
+      case 1: heat_explicit_launch<1>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 2: heat_explicit_launch<2>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 3: heat_explicit_launch<3>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 4: heat_explicit_launch<4>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 5: heat_explicit_launch<5>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 6: heat_explicit_launch<6>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      case 7: heat_explicit_launch<7>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+      default: heat_explicit_launch<8>(c, transpose, sign, in, base, out, w_first, w_step, nw, add2, row_map); break;
+    }
+    c.launches++;
     return;
   }
   if (c.model == WF4DVAR_M_HEAT && c.heat_D > 0 && c.heat_iir) {
@@ -461,6 +552,14 @@ void setup_model(Ctx &c, const wf4dvar_problem &p) {
         WF_CUDA(memcpy_sync(c, c.MdenseT + (size_t)w * s * s, M.data(), M.size() * 8, cudaMemcpyHostToDevice));
       }
     }
+  } else if (c.model == WF4DVAR_M_HEAT_EXPLICIT) {
+    WF_REQUIRE(p.heat_r > 0 && p.heat_r <= 0.5, WF4DVAR_EINVAL,
+               "HEAT_EXPLICIT needs 0 < heat_r <= 1/2 (P:L1132 stability)");
+    WF_REQUIRE(p.heat_nsteps >= 1 && p.heat_nsteps <= 8, WF4DVAR_EINVAL,
+               "HEAT_EXPLICIT needs 1 <= heat_nsteps <= 8");
+    WF_REQUIRE(s >= 3, WF4DVAR_EINVAL, "HEAT_EXPLICIT needs s >= 3");
+    c.heat_r = p.heat_r;
+    c.heat_nsteps = p.heat_nsteps;
   } else if (c.model == WF4DVAR_M_DENSE) {
     WF_REQUIRE(p.M_dense != nullptr, WF4DVAR_EINVAL, "M_dense is NULL");
     c.Mdense = c.alloc<double>((size_t)N * s * s);

@@ -138,15 +138,26 @@ void apply_A(Ctx &c, const double *x, double *y) {
   // the three output blocks are independent: c2 and c3 run on the aux streams
   fork(c);
   {
-    // c2 = R x2 + H x3 (gather in the epilogue)
+    // c2 = R x2 + H x3 (selection H: gather in the epilogue; general H: CSR first)
     OnStream os(c, c.aux[0]);
-    GemmProb g = gp(c.R, p, x2, ld, y2, ld, x3, ld, p, (int)ld, p, 1.0, 1.0, c.H_idx);
-    launch_gemm(c, &g, 1, 1);
+    if (c.H_general) {
+      csr_apply(c, y2, x3, c.Hrp, c.Hcol, c.Hval, p, false);
+      GemmProb g = gp(c.R, p, x2, ld, y2, ld, y2, ld, p, (int)ld, p, 1.0, 1.0);
+      launch_gemm(c, &g, 1, 1);
+    } else {
+      GemmProb g = gp(c.R, p, x2, ld, y2, ld, x3, ld, p, (int)ld, p, 1.0, 1.0, c.H_idx);
+      launch_gemm(c, &g, 1, 1);
+    }
   }
   {
-    // c3 = L^T x1 + H^T x2
+    // c3 = L^T x1 + H^T x2 (selection H: scatter fused into the model pass)
     OnStream os(c, c.aux[1]);
-    model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W, x2, c.H_inv);
+    if (c.H_general) {
+      model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W);
+      csr_apply(c, y3, x2, c.HTrp, c.HTcol, c.HTval, s, true);
+    } else {
+      model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W, x2, c.H_inv);
+    }
   }
   // c1 = L x3 + D x1
   model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);

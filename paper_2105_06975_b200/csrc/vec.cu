@@ -168,6 +168,29 @@ void reduce_final(Ctx &c, const double *part, int nparts, int nd, double *out) {
   allreduce(c, out, (size_t)nd * c.m);
 }
 
+// y[i][col] (+)= sum_k val[k] x[col_k][col]: one thread per (row, column), columns
+// fastest (coalesced across the W m columns of a segment)
+__global__ void k_csr_apply(double *y, const double *x, const int *rowptr, const int *col,
+                            const double *val, int nrows, int64_t ld, int accumulate) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)nrows * ld) return;
+  const int64_t i = e / ld, cc = e - i * ld;
+  double v = accumulate ? y[e] : 0.0;
+  for (int k = rowptr[i]; k < rowptr[i + 1]; ++k) v = fma(val[k], x[(int64_t)col[k] * ld + cc], v);
+  y[e] = v;
+}
+
+void csr_apply(Ctx &c, double *y, const double *x, const int *rowptr, const int *col,
+               const double *val, int nrows, bool accumulate) {
+  const int64_t tot = (int64_t)nrows * c.ncol;
+  if (tot == 0) return;
+  LaunchScope ls(c, K_VEC, 0, 8.0 * 2 * tot);
+  k_csr_apply<<<(unsigned)((tot + 255) / 256), 256, 0, c.st>>>(y, x, rowptr, col, val, nrows,
+                                                               c.ncol, accumulate ? 1 : 0);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
+}
+
 void allreduce(Ctx &c, double *buf, size_t count) {
   if (c.comm) c.comm->allreduce_sum(buf, count, c.st);
 }

@@ -62,6 +62,8 @@ class Problem:
     M_dense: Optional[np.ndarray] = None  # dense model: [N][s][s] (M_w for w=1..N)
     rhs: Optional[np.ndarray] = None      # flat library layout, (2s+p)*W*m
     extra: dict = field(default_factory=dict)
+    heat_nsteps: int = 1                  # heat_explicit: model steps per window
+    H_csr: Optional[tuple] = None         # (rowptr, col, val): general H_i (replaces H_idx)
 
     @property
     def W(self):
@@ -265,3 +267,99 @@ def with_R(prob, R):
     q = copy.copy(prob)
     q.R = np.array(R, dtype=np.float64)
     return q
+
+
+# ---------------------------------------------------------------- NEXT-1 workload
+def modified_soar_row(s, L, maxval, sigma):
+    """First row of the paper's circulant modified-SOAR matrix (reading
+    A2 for the parenthesis): c_i = sigma (1 + d_i/L) exp(-d_i/L),
+    d_i = 2|sin(i theta/2)|, theta = pi/maxval, on the circular lag i; entries with
+    circular lag >= maxval are zero (reading A29: maxval sets the number of
+    non-zeros)."""
+    i = np.arange(s)
+    lag = np.minimum(i, s - i)
+    d = 2.0 * np.abs(np.sin(lag * (np.pi / maxval) / 2.0))
+    row = sigma * (1.0 + d / L) * np.exp(-d / L)
+    row[lag >= maxval] = 0.0
+    return row
+
+
+def modified_soar_matrix(s, L, maxval, sigma, rng):
+    row = modified_soar_row(s, L, maxval, sigma)
+    C = np.array([np.roll(row, k) for k in range(s)])
+    lmin = np.linalg.eigvalsh(C)[0]
+    if lmin < 0:   # P:L570: delta = |lambda_min| + psi, psi ~ U[0, 0.5]
+        C = C + (abs(lmin) + rng.uniform(0.0, 0.5)) * np.eye(s)
+    return C
+
+
+def smoothed_H_csr(s):
+    """p = s/2 observations of alternate state variables, each smoothed equally over
+    5 adjacent state variables with entries 1/5 (reading A28: observed
+    variables 1, 3, 5, ...; the 5-point window is clipped at the boundary)."""
+    rowptr, col, val = [0], [], []
+    for c in range(1, s, 2):
+        for k in range(c - 2, c + 3):
+            if 0 <= k < s:
+                col.append(k)
+                val.append(0.2)
+        rowptr.append(len(col))
+    return (np.array(rowptr, np.int32), np.array(col, np.int32), np.array(val, np.float64))
+
+
+def paper_heat_problem(s=200, N=7, m=2, nsteps=1, r=0.4, seed0=0, pvec=None,
+                       B=(0.6, 100, 0.4), Q=(0.5, 120, 0.2), with_rhs=True):
+    """NEXT-1: the paper's own heat workload -- explicit Dirichlet
+    forward-Euler model (r = 0.4), 5-point smoothed observations of
+    alternate variables, modified-SOAR B and Q with the delta fix
+    (P:L566-570; (L, maxval, sigma) = (0.6, 100, 0.4) and (0.5, 120, 0.2)), the
+    block-structured R_i (paper_block_R).  Input data only."""
+    from .layout import pack as _pack
+    rng0 = np.random.Generator(np.random.PCG64(10_000 + seed0))
+    Bm = modified_soar_matrix(s, *B, rng0)
+    Qm = modified_soar_matrix(s, *Q, rng0)
+    Hc = smoothed_H_csr(s)
+    p = len(Hc[0]) - 1
+    if pvec is None:
+        pvec = uniform_blocks(p, max(2, p // 5))
+    Rm = paper_block_R(pvec, seed=20_000 + seed0)
+    Hd = np.zeros((p, s))
+    for j in range(p):
+        Hd[j, Hc[1][Hc[0][j]:Hc[0][j + 1]]] = Hc[2][Hc[0][j]:Hc[0][j + 1]]
+    Mdt = np.zeros((s, s))
+    for i in range(1, s - 1):
+        Mdt[i, i] = 1 - 2 * r
+        if i > 1:
+            Mdt[i, i - 1] = r
+        if i < s - 2:
+            Mdt[i, i + 1] = r
+    Mw = np.linalg.matrix_power(Mdt, nsteps)   # truth/forecast propagation (synthesis)
+    prob = Problem(name=f"paper_heat_s{s}_N{N}_m{m}", model="heat_explicit", s=s, p=p, N=N,
+                   m=m, B=Bm, Q=Qm, R=Rm, H_idx=np.arange(p, dtype=np.int32), heat_r=r,
+                   heat_nsteps=nsteps, H_csr=Hc)
+    prob.extra = dict(pvec=list(pvec))
+    if not with_rhs:
+        return prob
+    W = N + 1
+    rngs = [np.random.Generator(np.random.PCG64(seed0 + j)) for j in range(m)]
+    cB, cQ, cR = np.linalg.cholesky(Bm), np.linalg.cholesky(Qm), np.linalg.cholesky(Rm)
+    x0t = _gaussian(rngs, cB, s)
+    truth = [x0t]
+    for w in range(1, W):
+        truth.append(Mw @ truth[-1] + _gaussian(rngs, cQ, s))
+    y = [Hd @ truth[w] + _gaussian(rngs, cR, p) for w in range(W)]
+    xb = x0t + _gaussian(rngs, cB, s)
+    guess = [xb]
+    for w in range(1, W):
+        guess.append(Mw @ guess[-1])
+    eta = np.zeros((s, W, m))
+    nu = np.stack([y[w] - Hd @ guess[w] for w in range(W)], axis=1)
+    prob.rhs = _pack(eta, nu, np.zeros((s, W, m)))
+    return prob
+
+
+def uniform_blocks(p, b):
+    pv = [b] * (p // b)
+    if p % b:
+        pv.append(p % b)
+    return pv
