@@ -187,6 +187,10 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       WF_CUDA(memcpy_sync(c, c.H_inv, inv.data(), c.s * 4, cudaMemcpyHostToDevice));
     }
     wf::setup_model(c, p);
+    // CUDA graphs for launch-bound sizes (per-iteration GPU work well under the
+    // ~50 launches' overhead); WF4DVAR_GRAPHS=0/1 forces
+    c.use_graphs = c.n <= (int64_t)8 << 20;
+    if (const char *e = getenv("WF4DVAR_GRAPHS")) c.use_graphs = atoi(e) != 0;
     c.ws_seg = c.alloc<double>((size_t)c.s * c.ncol);
     // dot partials: gy <= 2*148 blocks x up to 4 dots x m
     c.dot_part_cap = 4 * 148 * 4 * std::max(c.m, 256) + 4096;
@@ -227,6 +231,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
   }
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  c.drop_graphs();
+  if (c.own_st) { cudaStreamSynchronize(c.own_st); cudaStreamDestroy(c.own_st); }
   delete c.comm;
   c.comm = nullptr;
   if (c.sk_ws) cudaFree(c.sk_ws);

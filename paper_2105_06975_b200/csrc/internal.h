@@ -179,6 +179,28 @@ struct Ctx {
   // counters (per-window constituent products, Tables 7.2-7.3 / S5-S7)
   int64_t n_R = 0, n_Rhat_inv = 0, n_D = 0, n_Dhat_inv = 0, n_M = 0, n_A = 0, n_P = 0;
   int64_t launches = 0;
+  struct Counters {
+    int64_t v[8];
+    Counters operator-(const Counters &o) const { Counters r; for (int i = 0; i < 8; ++i) r.v[i] = v[i] - o.v[i]; return r; }
+    Counters operator+(const Counters &o) const { Counters r; for (int i = 0; i < 8; ++i) r.v[i] = v[i] + o.v[i]; return r; }
+  };
+  Counters counters() const { return Counters{{n_R, n_Rhat_inv, n_D, n_Dhat_inv, n_M, n_A, n_P, launches}}; }
+  void set_counters(const Counters &k) {
+    n_R = k.v[0]; n_Rhat_inv = k.v[1]; n_D = k.v[2]; n_Dhat_inv = k.v[3]; n_M = k.v[4];
+    n_A = k.v[5]; n_P = k.v[6]; launches = k.v[7];
+  }
+  // CUDA graphs of the MINRES iteration (launch-bound sizes), cached across solves
+  bool use_graphs = false;
+  cudaStream_t own_st = nullptr;  // library stream for graph capture when st is the legacy stream
+  cudaGraphExec_t mg_exec[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  Counters mg_delta[6];
+  const void *mg_key[4] = {nullptr, nullptr, nullptr, nullptr};
+  double mg_tol = -1, mg_mark = -1;
+  void drop_graphs() {
+    for (auto &e : mg_exec)
+      if (e) { cudaGraphExecDestroy(e); e = nullptr; }
+    for (auto &k : mg_key) k = nullptr;
+  }
   int gemm_cls = K_GEMM;          // profiling class of the next launch_gemm
   double *sk_ws = nullptr;        // stream-K GEMM: parked partial tiles
   unsigned *sk_flags = nullptr;   // stream-K GEMM: per-CTA publish flags

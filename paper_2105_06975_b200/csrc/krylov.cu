@@ -139,7 +139,10 @@ __global__ void k_minres_s2(MinresS S, int m) {
 }
 
 // after the update and rr = r . r: shift scalars, convergence, history
-__global__ void k_minres_s3(MinresS S, int m, int j, double tol, double mark_tol) {
+// (the iteration number lives on the device, flags[3], so that a captured CUDA
+// graph of the iteration stays valid for every j)
+__global__ void k_minres_s3(MinresS S, int m, double tol, double mark_tol) {
+  const int j = S.flags[3] + 1;
   int cnt = 0, below_mark = 1;
   for (int r = threadIdx.x; r < m; r += blockDim.x) {
     if (S.active[r]) {
@@ -162,6 +165,7 @@ __global__ void k_minres_s3(MinresS S, int m, int j, double tol, double mark_tol
   if (threadIdx.x == 0) {
     S.flags[0] = cnt;
     if (below_mark && S.flags[2] < 0) S.flags[2] = j;
+    S.flags[3] = j;
   }
 }
 
@@ -214,26 +218,66 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   bool indef = false;
   const int ce = std::max(1, o.check_every);
   int *hpin = c.hpin;
-  for (j = 1; j <= o.maxit; ++j) {
-    apply_A(c, z, q);
-    { const double *a[1] = {q}, *bb[1] = {z}; dots(c, 1, a, bb, n, S.dots); }
+  // one MINRES iteration on the current rotation of the work vectors
+  auto body = [&](double *vp_, double *v_, double *vn_, double *z_, double *zn_, double *wp_,
+                  double *w_, double *awp_, double *aw_) {
+    apply_A(c, z_, q);
+    { const double *a[1] = {q}, *bb[1] = {z_}; dots(c, 1, a, bb, n, S.dots); }
     k_minres_s1<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
-    k_lin3<<<nblk(n, 256), 256, 0, c.st>>>(vn, q, S.cv, v, S.cv + m, vp, S.cv + 2 * m, n, m);
+    k_lin3<<<nblk(n, 256), 256, 0, c.st>>>(vn_, q, S.cv, v_, S.cv + m, vp_, S.cv + 2 * m, n, m);
     c.launches += 2;
-    apply_P(c, vn, zn);
-    { const double *a[1] = {zn}, *bb[1] = {vn}; dots(c, 1, a, bb, n, S.dots); }
+    apply_P(c, vn_, zn_);
+    { const double *a[1] = {zn_}, *bb[1] = {vn_}; dots(c, 1, a, bb, n, S.dots); }
     k_minres_s2<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
     {
       const RedGrid rg = red_grid(c, n);
       LaunchScope ls(c, K_VEC, 10.0 * n, 8.0 * 12 * n);
-      k_minres_update<<<dim3(rg.gx, rg.gy), 256, 0, c.st>>>(z, q, wp, w, awp, aw, x, res, S.coef,
-                                                            rg.rows, m, rg.RB, rg.rpb, c.dot_part);
+      k_minres_update<<<dim3(rg.gx, rg.gy), 256, 0, c.st>>>(z_, q, wp_, w_, awp_, aw_, x, res,
+                                                            S.coef, rg.rows, m, rg.RB, rg.rpb,
+                                                            c.dot_part);
       c.launches += 2;
       reduce_final(c, c.dot_part, rg.gy, 1, S.dots);   // ||r_j||^2
     }
-    k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, j, o.tol, o.mark_tol);
+    k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, o.tol, o.mark_tol);
     c.launches++;
     WF_CUDA(cudaGetLastError());
+  };
+  // Launch-bound sizes replay the iteration as a CUDA graph (one per phase of the
+  // 6-periodic buffer rotation, captured on first use, cached across solves with the
+  // same buffers); not while profiling (per-launch events) nor with a transport.
+  const bool graphs = c.use_graphs && !c.prof.on && !c.comm;
+  if (graphs) {
+    const void *key[4] = {b, x, c.kws, S.hist};
+    if (memcmp(key, c.mg_key, sizeof(key)) != 0 || c.mg_tol != o.tol || c.mg_mark != o.mark_tol) {
+      c.drop_graphs();
+      memcpy(c.mg_key, key, sizeof(key));
+      c.mg_tol = o.tol;
+      c.mg_mark = o.mark_tol;
+    }
+  }
+  for (j = 1; j <= o.maxit; ++j) {
+    const int phase = (j - 1) % 6;
+    if (graphs && j > 6) {
+      // phases repeat every 6 iterations: j > 6 means this phase already ran eagerly
+      // (all lazy allocations and kernel attributes are done) -> capture once, replay
+      if (!c.mg_exec[phase]) {
+        // capture does not execute: record the counter increments of one iteration
+        // (launches, per-window constituent products) and add them on every replay
+        cudaGraph_t g = nullptr;
+        const Ctx::Counters before = c.counters();
+        WF_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+        body(vp, v, vn, z, zn, wp, w, awp, aw);
+        WF_CUDA(cudaStreamEndCapture(c.st, &g));
+        c.mg_delta[phase] = c.counters() - before;
+        c.set_counters(before);
+        WF_CUDA(cudaGraphInstantiate(&c.mg_exec[phase], g, 0));
+        cudaGraphDestroy(g);
+      }
+      WF_CUDA(cudaGraphLaunch(c.mg_exec[phase], c.st));
+      c.set_counters(c.counters() + c.mg_delta[phase]);
+    } else {
+      body(vp, v, vn, z, zn, wp, w, awp, aw);
+    }
     WF_CUDA(cudaEventRecord(c.iter_event(j), c.st));
     // rotate: v_prev <- v, v <- v_new, z <- z_new, w_prev <- w, w <- w_new(in wp), same for Aw
     std::swap(vp, v); std::swap(v, vn);     // vp=old v, v=vn, vn=old vp (free)
@@ -347,10 +391,18 @@ __global__ void __launch_bounds__(256) k_multiaxpy(const double *V, int64_t n, i
     for (int64_t row = row0 + u; row < row1; row += U) {
       int64_t f = row * m + r;
       double v = w[f];
-      for (int i = 0; i < nv; ++i) {
-        double hi = h[i * m + r];
-        if (hi != 0.0) v = fma(-V[(int64_t)i * n + f], hi, v);
+      // batches of 8 independent basis loads in flight (ncu r01i: the one-at-a-time
+      // dependent load+FMA chain ran this HBM-bound kernel at 28% of bandwidth);
+      // the fixed i order keeps the result deterministic
+      int i = 0;
+      for (; i + 8 <= nv; i += 8) {
+        double vv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) vv[k] = __ldcs(V + (int64_t)(i + k) * n + f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v = fma(-vv[k], __ldg(h + (i + k) * m + r), v);
       }
+      for (; i < nv; ++i) v = fma(-__ldcs(V + (int64_t)i * n + f), __ldg(h + i * m + r), v);
       w[f] = v;
       nn = fma(v, v, nn);
     }
@@ -657,6 +709,24 @@ void solve(Ctx &c, const double *rhs, double *x, const wf4dvar_solve_opts &o, wf
     rep->n_Rhat_inv = c.n_Rhat_inv - Ri0; rep->n_D = c.n_D - D0; rep->n_Dhat_inv = c.n_Dhat_inv - Di0;
     rep->n_M = c.n_M - M0;
   };
+  // Stream capture is illegal on the legacy default stream: a graph-eligible solve
+  // issued there runs on a library-owned stream, ordered after / before the caller's
+  // stream by events (the call is synchronous either way).
+  cudaStream_t user = c.st;
+  const bool own = c.use_graphs && !c.prof.on && !c.comm && o.solver == WF4DVAR_MINRES &&
+                   user == nullptr;
+  if (own) {
+    if (!c.own_st) WF_CUDA(cudaStreamCreateWithFlags(&c.own_st, cudaStreamNonBlocking));
+    WF_CUDA(cudaEventRecord(c.ev_fork, user));
+    WF_CUDA(cudaStreamWaitEvent(c.own_st, c.ev_fork, 0));
+    c.st = c.own_st;
+  }
+  auto restore = [&]() {
+    if (!own) return;
+    cudaEventRecord(c.ev_fork, c.own_st);
+    cudaStreamWaitEvent(user, c.ev_fork, 0);
+    c.st = user;
+  };
   try {
     if (o.solver == WF4DVAR_MINRES) {
       WF_REQUIRE(c.pc.shape == WF4DVAR_PD, WF4DVAR_EINVAL, "MINRES needs the SPD preconditioner P_D");
@@ -664,7 +734,8 @@ void solve(Ctx &c, const double *rhs, double *x, const wf4dvar_solve_opts &o, wf
     } else {
       gmres(c, rhs, x, o, rep);
     }
-  } catch (...) { fill(); throw; }
+  } catch (...) { restore(); fill(); throw; }
+  restore();
   fill();
 }
 

@@ -41,18 +41,18 @@ __device__ __forceinline__ void l96_rhs(const double (&x)[IPT], double (&f)[IPT]
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
     int i = ty + 8 * k;
-    if (i < s) bx[i * 32 + lane] = x[k];
+    if (i < s) bx[i * 4 + lane] = x[k];
   }
-  __syncthreads();
+  __syncwarp();
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
     int i = ty + 8 * k;
     if (i < s) {
       int ip = i + 1 == s ? 0 : i + 1, im1 = i == 0 ? s - 1 : i - 1, im2 = i >= 2 ? i - 2 : i - 2 + s;
-      f[k] = (bx[ip * 32 + lane] - bx[im2 * 32 + lane]) * bx[im1 * 32 + lane] - x[k] + F;
+      f[k] = (bx[ip * 4 + lane] - bx[im2 * 4 + lane]) * bx[im1 * 4 + lane] - x[k] + F;
     }
   }
-  __syncthreads();
+  __syncwarp();
 }
 
 // Ju = J(x) u, with x already resident in bx (written by l96_rhs of the same stage is
@@ -64,9 +64,9 @@ __device__ __forceinline__ void l96_jac(const double (&x)[IPT], const double (&u
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
     int i = ty + 8 * k;
-    if (i < s) { bx[i * 32 + lane] = x[k]; bu[i * 32 + lane] = u[k]; }
+    if (i < s) { bx[i * 4 + lane] = x[k]; bu[i * 4 + lane] = u[k]; }
   }
-  __syncthreads();
+  __syncwarp();
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
     int i = ty + 8 * k;
@@ -74,15 +74,15 @@ __device__ __forceinline__ void l96_jac(const double (&x)[IPT], const double (&u
       int ip1 = i + 1 == s ? 0 : i + 1, ip2 = i + 2 >= s ? i + 2 - s : i + 2;
       int im1 = i == 0 ? s - 1 : i - 1, im2 = i >= 2 ? i - 2 : i - 2 + s;
       if (!transpose) {
-        Ju[k] = (bu[ip1 * 32 + lane] - bu[im2 * 32 + lane]) * bx[im1 * 32 + lane] +
-                (bx[ip1 * 32 + lane] - bx[im2 * 32 + lane]) * bu[im1 * 32 + lane] - u[k];
+        Ju[k] = (bu[ip1 * 4 + lane] - bu[im2 * 4 + lane]) * bx[im1 * 4 + lane] +
+                (bx[ip1 * 4 + lane] - bx[im2 * 4 + lane]) * bu[im1 * 4 + lane] - u[k];
       } else {
-        Ju[k] = bx[im2 * 32 + lane] * bu[im1 * 32 + lane] - bx[ip1 * 32 + lane] * bu[ip2 * 32 + lane] +
-                (bx[ip2 * 32 + lane] - bx[im1 * 32 + lane]) * bu[ip1 * 32 + lane] - u[k];
+        Ju[k] = bx[im2 * 4 + lane] * bu[im1 * 4 + lane] - bx[ip1 * 4 + lane] * bu[ip2 * 4 + lane] +
+                (bx[ip2 * 4 + lane] - bx[im1 * 4 + lane]) * bu[ip1 * 4 + lane] - u[k];
       }
     }
   }
-  __syncthreads();
+  __syncwarp();
 }
 
 // nonlinear stage states of one RK4 step from x (x1 = x)
@@ -110,8 +110,15 @@ template <int IPT, int NSUB_MAX>
 __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
   __shared__ double bx[L96Thread<IPT>::S_MAX * 32];
   __shared__ double bu[L96Thread<IPT>::S_MAX * 32];
-  const int lane = threadIdx.x, ty = threadIdx.y;
-  const int r = blockIdx.x * 32 + lane;
+  // 4 problems per warp, 8 lanes per problem (lane = 8 p + ty): the periodic
+  // neighbour exchange stays inside the warp (warp-private shared memory, __syncwarp
+  // instead of __syncthreads; layout [i][4] -> every access is 32 consecutive doubles)
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int wp = tid >> 5, lw = tid & 31;
+  const int lane = lw >> 3, ty = lw & 7;    // lane = problem within the warp
+  const int r = blockIdx.x * 32 + wp * 4 + lane;
+  double *const bxw = bx + wp * (L96Thread<IPT>::S_MAX * 4);
+  double *const buw = bu + wp * (L96Thread<IPT>::S_MAX * 4);
   const int t = blockIdx.y;
   const int w = a.w_first + t * a.w_step;
   const int ws = w + a.dir;                       // local source window
@@ -138,17 +145,17 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
       // forward tangent: nsub RK4 steps
       for (int st = 0; st < a.nsub; ++st) {
         double x2[IPT], x3[IPT], x4[IPT], xn[IPT], d1[IPT], d2[IPT], d3[IPT], d4[IPT], u[IPT];
-        rk4_stages<IPT>(x, x2, x3, x4, xn, bx, s, ty, lane, a.F, h);
-        l96_jac<IPT>(x, v, d1, bx, bu, s, ty, lane, false);
+        rk4_stages<IPT>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
+        l96_jac<IPT>(x, v, d1, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) u[k] = v[k] + 0.5 * h * d1[k];
-        l96_jac<IPT>(x2, u, d2, bx, bu, s, ty, lane, false);
+        l96_jac<IPT>(x2, u, d2, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) u[k] = v[k] + 0.5 * h * d2[k];
-        l96_jac<IPT>(x3, u, d3, bx, bu, s, ty, lane, false);
+        l96_jac<IPT>(x3, u, d3, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) u[k] = v[k] + h * d3[k];
-        l96_jac<IPT>(x4, u, d4, bx, bu, s, ty, lane, false);
+        l96_jac<IPT>(x4, u, d4, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
           v[k] = v[k] + (h / 6.0) * (d1[k] + 2.0 * d2[k] + 2.0 * d3[k] + d4[k]);
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
 #pragma unroll
           for (int k = 0; k < IPT; ++k) xs[st][k] = x[k];
           if (st + 1 < a.nsub) {
-            rk4_stages<IPT>(x, x2, x3, x4, xn, bx, s, ty, lane, a.F, h);
+            rk4_stages<IPT>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
 #pragma unroll
             for (int k = 0; k < IPT; ++k) x[k] = xn[k];
           }
@@ -177,21 +184,21 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
           double x1[IPT], x2[IPT], x3[IPT], x4[IPT], xn[IPT], lu[IPT], ld1[IPT], ld2[IPT], ld3[IPT];
 #pragma unroll
           for (int k = 0; k < IPT; ++k) x1[k] = xs[st][k];
-          rk4_stages<IPT>(x1, x2, x3, x4, xn, bx, s, ty, lane, a.F, h);
+          rk4_stages<IPT>(x1, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
           // lambda_d4 = h/6 l ; lambda_u4 = J4^T lambda_d4
           double lv[IPT], tmp[IPT];
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] = v[k]; tmp[k] = (h / 6.0) * v[k]; }
-          l96_jac<IPT>(x4, tmp, lu, bx, bu, s, ty, lane, true);
+          l96_jac<IPT>(x4, tmp, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld3[k] = (h / 3.0) * v[k] + h * lu[k]; }
-          l96_jac<IPT>(x3, ld3, lu, bx, bu, s, ty, lane, true);
+          l96_jac<IPT>(x3, ld3, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld2[k] = (h / 3.0) * v[k] + 0.5 * h * lu[k]; }
-          l96_jac<IPT>(x2, ld2, lu, bx, bu, s, ty, lane, true);
+          l96_jac<IPT>(x2, ld2, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld1[k] = (h / 6.0) * v[k] + 0.5 * h * lu[k]; }
-          l96_jac<IPT>(x1, ld1, lu, bx, bu, s, ty, lane, true);
+          l96_jac<IPT>(x1, ld1, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) v[k] = lv[k] + lu[k];
         }

@@ -287,6 +287,7 @@ static void dev_free(Ctx &c, double *&ptr) {
 }
 
 void free_precond(Ctx &c) {
+  c.drop_graphs();   // captured iterations hold pointers to the old factors
   dev_free(c, c.GB); dev_free(c, c.GBt); dev_free(c, c.GQ); dev_free(c, c.GQt);
   dev_free(c, c.GR); dev_free(c, c.GRt); dev_free(c, c.Rdiag_inv);
   dev_free(c, c.PB); dev_free(c, c.PBt); dev_free(c, c.PQ); dev_free(c, c.PQt);
