@@ -38,6 +38,19 @@ def launches(path):
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v
+    # NVTX class (the library's LaunchScope ranges) when captured with --nvtx
+    ncol = next((i for i, c in enumerate(h) if "Push/Pop_Range" in c), None)
+    byclass = collections.OrderedDict()
+    if ncol is not None:
+        for r in rows[hdr + 1:]:
+            if len(r) < len(h):
+                continue
+            rng = r[ncol].strip()
+            # '<tid>  "<default domain>:<range>:none:..."' -> <range>
+            rng = rng.split('"')[1].split(":")[1] if '"' in rng else "(no range)"
+            a = byclass.setdefault(rng, [0, 0.0])
+            a[0] += 1
+            a[1] += float(r[vi].replace(",", ""))
     tot = sum(v[1] for v in agg.values())
     print(f"# ncu launch list ({path}): gpu__time_duration.sum, --clock-control none")
     print("# cold-cache, serialised per launch: compare SHARES, not absolutes")
@@ -45,6 +58,10 @@ def launches(path):
     print(f"{'kernel':40s} {'launches':>8s} {'ms':>10s} {'share':>7s}")
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"{k:40s} {v[0]:8d} {v[1] / 1e6:10.3f} {100 * v[1] / tot:6.1f}%")
+    if byclass:
+        print("# by library kernel class (NVTX range)")
+        for k, v in sorted(byclass.items(), key=lambda x: -x[1][1]):
+            print(f"{k[:40]:40s} {v[0]:8d} {v[1] / 1e6:10.3f} {100 * v[1] / tot:6.1f}%")
 
 
 def full(path):
