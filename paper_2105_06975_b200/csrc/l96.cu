@@ -231,8 +231,14 @@ void l96_step(Ctx &c, bool transpose, double sign, const double *in, const doubl
   a.nsub = c.l96_nsub; a.w_first = w_first; a.w_step = w_step; a.nw = nw;
   a.dir = transpose ? 1 : -1;
   dim3 grid((c.m + 31) / 32, nw), block(32, 8);
-  // ~ per problem and substep: 4 rhs (5 flops/i) + 4 Jacobian products (~8 flops/i)
-  double flops = (double)nw * c.m * c.l96_nsub * c.s * (transpose ? 4 * 5 * 2 + 4 * 9 : 4 * 5 + 4 * 9);
+  // flops per state element and RK4 substep, counted from the kernel's arithmetic:
+  //   nonlinear stages: 4 tendencies x 4 + stage states 3 x 2 + update 7      = 29
+  //   tangent:  4 Jacobian products x 6 + stage tangents 3 x 2 + update 7      = 37
+  //   adjoint:  4 transposed products x 7 + adjoint stage combinations 14      = 42,
+  //             plus the stages recomputed twice (start states, then per substep)
+  const double nl = 29.0, tl = 37.0, ad = 42.0, ns = c.l96_nsub;
+  const double per = transpose ? (nl * (2.0 * ns - 1.0) + ad * ns) : (nl + tl) * ns;
+  double flops = (double)nw * c.m * c.s * per;
   LaunchScope ls(c, K_MODEL, flops, (double)nw * c.m * c.s * 8 * 4);
   if (c.s <= 40) k_l96_step<5, 8><<<grid, block, 0, c.st>>>(a);
   else k_l96_step<8, 8><<<grid, block, 0, c.st>>>(a);
