@@ -293,7 +293,7 @@ class Context:
         pc = precond if isinstance(precond, Precond) else make_precond(**(precond or {}))
         transport = TRANSPORT_NONE
         idbuf = None
-        if world > 1:
+        if world > 1 or nccl_id is not None or local_group is not None:
             if local_group is not None:
                 transport = TRANSPORT_LOCAL
             else:

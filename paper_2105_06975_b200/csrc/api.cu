@@ -135,7 +135,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     c.w0 = wb;
     c.W = we - wb;
     c.ncol = (int64_t)c.W * c.m;
-    if (world > 1) {
+    if (world > 1 || (dist && dist->transport != WF4DVAR_TRANSPORT_NONE)) {
       c.comm = wf::make_comm(*dist);
       const size_t sm = (size_t)c.s * c.m;
       c.halo_lo = c.alloc<double>(sm);

@@ -275,7 +275,9 @@ LocalGroup *local_group_create(int world) {
 void local_group_destroy(LocalGroup *g) { delete g; }
 
 Comm *make_comm(const wf4dvar_dist &d) {
-  if (d.world <= 1) return nullptr;
+  // world == 1 with an explicit transport still builds it (single-device check of the
+  // transport's calls: a 1-rank communicator, allreduce = copy, no neighbours)
+  if (d.world <= 1 && d.transport == WF4DVAR_TRANSPORT_NONE) return nullptr;
   if (d.transport == WF4DVAR_TRANSPORT_NCCL) {
     WF_REQUIRE(d.nccl_id != nullptr, WF4DVAR_EINVAL, "NCCL transport needs nccl_id");
     return new NcclComm(d.rank, d.world, d.nccl_id);

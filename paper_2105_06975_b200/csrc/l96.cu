@@ -34,6 +34,55 @@ struct L96Args {
   int w0, WG;   // global index of local window 0; global window count
 };
 
+// ---- contiguous ownership (s == 8 IPT): lane ty of a problem's 8-lane group owns
+// indices [ty IPT, ty IPT + IPT); the periodic neighbours it lacks (two on each side)
+// come from the ring neighbours by register shuffles -- no shared memory, no barrier
+template <int IPT>
+struct Halo2 { double l2, l1, r1, r2; };   // x_{i0-2}, x_{i0-1}, x_{i0+IPT}, x_{i0+IPT+1}
+
+template <int IPT>
+__device__ __forceinline__ Halo2<IPT> halo2(const double (&x)[IPT], int ty) {
+  const int lft = (ty + 7) & 7, rgt = (ty + 1) & 7;
+  Halo2<IPT> h;
+  h.l2 = __shfl_sync(0xffffffffu, x[IPT - 2], lft, 8);
+  h.l1 = __shfl_sync(0xffffffffu, x[IPT - 1], lft, 8);
+  h.r1 = __shfl_sync(0xffffffffu, x[0], rgt, 8);
+  h.r2 = __shfl_sync(0xffffffffu, x[1], rgt, 8);
+  return h;
+}
+
+template <int IPT>
+__device__ __forceinline__ double at(const double (&x)[IPT], const Halo2<IPT> &h, int j) {
+  // j in [-2, IPT + 1], compile-time after unrolling
+  return j == -2 ? h.l2 : j == -1 ? h.l1 : j == IPT ? h.r1 : j == IPT + 1 ? h.r2 : x[j];
+}
+
+template <int IPT>
+__device__ __forceinline__ void l96_rhs_sh(const double (&x)[IPT], double (&f)[IPT], int ty,
+                                           double F) {
+  const Halo2<IPT> h = halo2<IPT>(x, ty);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k)
+    f[k] = (at<IPT>(x, h, k + 1) - at<IPT>(x, h, k - 2)) * at<IPT>(x, h, k - 1) - x[k] + F;
+}
+
+template <int IPT>
+__device__ __forceinline__ void l96_jac_sh(const double (&x)[IPT], const double (&u)[IPT],
+                                           double (&Ju)[IPT], int ty, bool transpose) {
+  const Halo2<IPT> hx = halo2<IPT>(x, ty), hu = halo2<IPT>(u, ty);
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    if (!transpose) {
+      Ju[k] = (at<IPT>(u, hu, k + 1) - at<IPT>(u, hu, k - 2)) * at<IPT>(x, hx, k - 1) +
+              (at<IPT>(x, hx, k + 1) - at<IPT>(x, hx, k - 2)) * at<IPT>(u, hu, k - 1) - u[k];
+    } else {
+      Ju[k] = at<IPT>(x, hx, k - 2) * at<IPT>(u, hu, k - 1) -
+              at<IPT>(x, hx, k + 1) * at<IPT>(u, hu, k + 2) +
+              (at<IPT>(x, hx, k + 2) - at<IPT>(x, hx, k - 1)) * at<IPT>(u, hu, k + 1) - u[k];
+    }
+  }
+}
+
 template <int IPT>
 __device__ __forceinline__ void l96_rhs(const double (&x)[IPT], double (&f)[IPT], double *bx,
                                         int s, int ty, int lane, double F) {
@@ -86,27 +135,42 @@ __device__ __forceinline__ void l96_jac(const double (&x)[IPT], const double (&u
 }
 
 // nonlinear stage states of one RK4 step from x (x1 = x)
-template <int IPT>
+template <int IPT, bool SH>
+__device__ __forceinline__ void rhs_any(const double (&x)[IPT], double (&f)[IPT], double *bx,
+                                        int s, int ty, int lane, double F) {
+  if constexpr (SH) l96_rhs_sh<IPT>(x, f, ty, F);
+  else l96_rhs<IPT>(x, f, bx, s, ty, lane, F);
+}
+
+template <int IPT, bool SH>
+__device__ __forceinline__ void jac_any(const double (&x)[IPT], const double (&u)[IPT],
+                                        double (&Ju)[IPT], double *bx, double *bu, int s, int ty,
+                                        int lane, bool transpose) {
+  if constexpr (SH) l96_jac_sh<IPT>(x, u, Ju, ty, transpose);
+  else l96_jac<IPT>(x, u, Ju, bx, bu, s, ty, lane, transpose);
+}
+
+template <int IPT, bool SH>
 __device__ __forceinline__ void rk4_stages(const double (&x)[IPT], double (&x2)[IPT],
                                            double (&x3)[IPT], double (&x4)[IPT],
                                            double (&xn)[IPT], double *bx, int s, int ty, int lane,
                                            double F, double h) {
   double k1[IPT], k2[IPT], k3[IPT], k4[IPT];
-  l96_rhs<IPT>(x, k1, bx, s, ty, lane, F);
+  rhs_any<IPT, SH>(x, k1, bx, s, ty, lane, F);
 #pragma unroll
   for (int k = 0; k < IPT; ++k) x2[k] = x[k] + 0.5 * h * k1[k];
-  l96_rhs<IPT>(x2, k2, bx, s, ty, lane, F);
+  rhs_any<IPT, SH>(x2, k2, bx, s, ty, lane, F);
 #pragma unroll
   for (int k = 0; k < IPT; ++k) x3[k] = x[k] + 0.5 * h * k2[k];
-  l96_rhs<IPT>(x3, k3, bx, s, ty, lane, F);
+  rhs_any<IPT, SH>(x3, k3, bx, s, ty, lane, F);
 #pragma unroll
   for (int k = 0; k < IPT; ++k) x4[k] = x[k] + h * k3[k];
-  l96_rhs<IPT>(x4, k4, bx, s, ty, lane, F);
+  rhs_any<IPT, SH>(x4, k4, bx, s, ty, lane, F);
 #pragma unroll
   for (int k = 0; k < IPT; ++k) xn[k] = x[k] + (h / 6.0) * (k1[k] + 2.0 * k2[k] + 2.0 * k3[k] + k4[k]);
 }
 
-template <int IPT, int NSUB_MAX>
+template <int IPT, int NSUB_MAX, bool SH>
 __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
   __shared__ double bx[L96Thread<IPT>::S_MAX * 32];
   __shared__ double bu[L96Thread<IPT>::S_MAX * 32];
@@ -135,7 +199,7 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
     double x[IPT];
 #pragma unroll
     for (int k = 0; k < IPT; ++k) {
-      int i = ty + 8 * k;
+      int i = SH ? ty * IPT + k : ty + 8 * k;
       x[k] = (live && i < s) ? a.traj[((int64_t)tw * s + i) * a.m + r] : 0.0;
       v[k] = (live && i < s) ? (from_halo ? a.halo[(int64_t)i * a.m + r]
                                           : a.in[i * ld + (int64_t)ws * a.m + r])
@@ -145,17 +209,17 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
       // forward tangent: nsub RK4 steps
       for (int st = 0; st < a.nsub; ++st) {
         double x2[IPT], x3[IPT], x4[IPT], xn[IPT], d1[IPT], d2[IPT], d3[IPT], d4[IPT], u[IPT];
-        rk4_stages<IPT>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
-        l96_jac<IPT>(x, v, d1, bxw, buw, s, ty, lane, false);
+        rk4_stages<IPT, SH>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
+        jac_any<IPT, SH>(x, v, d1, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) u[k] = v[k] + 0.5 * h * d1[k];
-        l96_jac<IPT>(x2, u, d2, bxw, buw, s, ty, lane, false);
+        jac_any<IPT, SH>(x2, u, d2, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) u[k] = v[k] + 0.5 * h * d2[k];
-        l96_jac<IPT>(x3, u, d3, bxw, buw, s, ty, lane, false);
+        jac_any<IPT, SH>(x3, u, d3, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) u[k] = v[k] + h * d3[k];
-        l96_jac<IPT>(x4, u, d4, bxw, buw, s, ty, lane, false);
+        jac_any<IPT, SH>(x4, u, d4, bxw, buw, s, ty, lane, false);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
           v[k] = v[k] + (h / 6.0) * (d1[k] + 2.0 * d2[k] + 2.0 * d3[k] + d4[k]);
@@ -172,7 +236,7 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
 #pragma unroll
           for (int k = 0; k < IPT; ++k) xs[st][k] = x[k];
           if (st + 1 < a.nsub) {
-            rk4_stages<IPT>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
+            rk4_stages<IPT, SH>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
 #pragma unroll
             for (int k = 0; k < IPT; ++k) x[k] = xn[k];
           }
@@ -184,21 +248,21 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
           double x1[IPT], x2[IPT], x3[IPT], x4[IPT], xn[IPT], lu[IPT], ld1[IPT], ld2[IPT], ld3[IPT];
 #pragma unroll
           for (int k = 0; k < IPT; ++k) x1[k] = xs[st][k];
-          rk4_stages<IPT>(x1, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
+          rk4_stages<IPT, SH>(x1, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
           // lambda_d4 = h/6 l ; lambda_u4 = J4^T lambda_d4
           double lv[IPT], tmp[IPT];
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] = v[k]; tmp[k] = (h / 6.0) * v[k]; }
-          l96_jac<IPT>(x4, tmp, lu, bxw, buw, s, ty, lane, true);
+          jac_any<IPT, SH>(x4, tmp, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld3[k] = (h / 3.0) * v[k] + h * lu[k]; }
-          l96_jac<IPT>(x3, ld3, lu, bxw, buw, s, ty, lane, true);
+          jac_any<IPT, SH>(x3, ld3, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld2[k] = (h / 3.0) * v[k] + 0.5 * h * lu[k]; }
-          l96_jac<IPT>(x2, ld2, lu, bxw, buw, s, ty, lane, true);
+          jac_any<IPT, SH>(x2, ld2, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld1[k] = (h / 6.0) * v[k] + 0.5 * h * lu[k]; }
-          l96_jac<IPT>(x1, ld1, lu, bxw, buw, s, ty, lane, true);
+          jac_any<IPT, SH>(x1, ld1, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
           for (int k = 0; k < IPT; ++k) v[k] = lv[k] + lu[k];
         }
@@ -208,7 +272,7 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
   if (!live) return;
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    int i = ty + 8 * k;
+    int i = SH ? ty * IPT + k : ty + 8 * k;
     if (i < s) {
       int64_t o = i * ld + (int64_t)w * a.m + r;
       double val = a.base[o];
@@ -240,8 +304,11 @@ void l96_step(Ctx &c, bool transpose, double sign, const double *in, const doubl
   const double per = transpose ? (nl * (2.0 * ns - 1.0) + ad * ns) : (nl + tl) * ns;
   double flops = (double)nw * c.m * c.s * per;
   LaunchScope ls(c, K_MODEL, flops, (double)nw * c.m * c.s * 8 * 4);
-  if (c.s <= 40) k_l96_step<5, 8><<<grid, block, 0, c.st>>>(a);
-  else k_l96_step<8, 8><<<grid, block, 0, c.st>>>(a);
+  // contiguous ownership with shuffled neighbours when s == 8 IPT (c2: s = 40)
+  if (c.s == 40) k_l96_step<5, 8, true><<<grid, block, 0, c.st>>>(a);
+  else if (c.s == 64) k_l96_step<8, 8, true><<<grid, block, 0, c.st>>>(a);
+  else if (c.s <= 40) k_l96_step<5, 8, false><<<grid, block, 0, c.st>>>(a);
+  else k_l96_step<8, 8, false><<<grid, block, 0, c.st>>>(a);
   WF_CUDA(cudaGetLastError());
   c.launches++;
 }
