@@ -219,6 +219,21 @@ wf4dvar_status wf4dvar_solve(wf4dvar_ctx ctx, const double *rhs, double *x,
 wf4dvar_status wf4dvar_solve_host(wf4dvar_ctx ctx, const double *rhs_host, double *x_host,
                                   const wf4dvar_solve_opts *opts, wf4dvar_report *rep);
 
+/* Spectral suite: extreme eigenvalues by batched Lanczos, one
+   independent run per RHS column, `steps` steps from the start vector v0 (device,
+   full vector layout of n_local doubles; OP_LHAT uses only its delta_x segment).
+     OP_PA    eigenvalues of P_D^{-1} A (Theorem 3.1): preconditioned
+              Lanczos in the P_D inner product (the recurrence of MINRES);
+              the context's preconditioner must be P_D.
+     OP_LHAT  eigenvalues of L_hat^{-T} L^T L L_hat^{-1} (Section 4, Prop. 4.4/4.5,
+              Supp. Tables S2/S3) on the state segment.
+   ritz_min / ritz_max: [m] host (extreme Ritz values: converge to the extreme
+   eigenvalues as steps grows); alpha / beta: optional [steps*m] host (row = step)
+   tridiagonal entries.  Synchronous.  No reorthogonalisation. */
+typedef enum { WF4DVAR_OP_PA = 0, WF4DVAR_OP_LHAT = 1 } wf4dvar_spectral_op;
+wf4dvar_status wf4dvar_lanczos(wf4dvar_ctx ctx, int32_t op, const double *v0, int32_t steps,
+                               double *ritz_min, double *ritz_max, double *alpha, double *beta);
+
 /* Instrumentation.  When enabled, the library brackets every launch of each
    kernel class with CUDA events on the launching stream; read() returns per
    class: launches, total milliseconds, algorithmic flops and bytes. */

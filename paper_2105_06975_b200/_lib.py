@@ -92,6 +92,7 @@ _sig = {
     "wf4dvar_apply_AP_host": (C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
     "wf4dvar_solve": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts), C.POINTER(Report)]),
     "wf4dvar_solve_host": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts), C.POINTER(Report)]),
+    "wf4dvar_lanczos": (C.c_int, [_ctx, C.c_int32, C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp]),
     "wf4dvar_profile_enable": (C.c_int, [_ctx, C.c_int32]),
     "wf4dvar_profile_read": (C.c_int, [_ctx, C.POINTER(KStat), C.c_int32, _ip]),
     "wf4dvar_launch_count": (C.c_int64, [_ctx]),
@@ -393,6 +394,21 @@ class Context:
                    mark_tol=1e-8, check_every=1, history=False):
         return self._solve(_lib.wf4dvar_solve_host, rhs, x, solver, tol, maxit, restart,
                            mark_tol, check_every, history)
+
+    def lanczos(self, op, v0, steps, tridiag=False):
+        """Extreme Ritz values per RHS of P_D^{-1} A (op="PA") or L_hat^{-T} L^T L L_hat^{-1}
+        (op="LHAT") after `steps` batched Lanczos steps from the device vector v0."""
+        lo = np.zeros(self.m)
+        hi = np.zeros(self.m)
+        a = np.zeros(steps * self.m) if tridiag else None
+        b = np.zeros(steps * self.m) if tridiag else None
+        self._check(_lib.wf4dvar_lanczos(self._h, {"PA": 0, "LHAT": 1}[op], _ptr(v0), int(steps),
+                                         _np_ptr(lo, C.c_double), _np_ptr(hi, C.c_double),
+                                         _np_ptr(a, C.c_double) if tridiag else None,
+                                         _np_ptr(b, C.c_double) if tridiag else None))
+        if tridiag:
+            return lo, hi, a.reshape(steps, self.m), b.reshape(steps, self.m)
+        return lo, hi
 
     def profile_enable(self, on=True):
         self._check(_lib.wf4dvar_profile_enable(self._h, 1 if on else 0))

@@ -193,7 +193,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     if (const char *e = getenv("WF4DVAR_GRAPHS")) c.use_graphs = atoi(e) != 0;
     c.ws_seg = c.alloc<double>((size_t)c.s * c.ncol);
     // dot partials: gy <= 2*148 blocks x up to 4 dots x m
-    c.dot_part_cap = 4 * 148 * 4 * std::max(c.m, 256) + 4096;
+    c.dot_part_cap = 8 * 148 * 4 * std::max(c.m, 256) + 4096;
     c.dot_part = c.alloc<double>(c.dot_part_cap);
     WF_CUDA(cudaMallocHost((void **)&c.hpin, 16 * sizeof(int)));
     set_pc(c, *pc);
@@ -330,6 +330,14 @@ wf4dvar_status wf4dvar_solve_host(wf4dvar_ctx ctx, const double *rhs_host, doubl
     WF_CUDA(cudaMemcpyAsync(x_host, c.dev_io_y, c.n * 8, cudaMemcpyDeviceToHost, c.st));
     WF_CUDA(cudaStreamSynchronize(c.st));
     if (st != WF4DVAR_OK) throw Error{st, c.last_error};
+  });
+}
+
+wf4dvar_status wf4dvar_lanczos(wf4dvar_ctx ctx, int32_t op, const double *v0, int32_t steps,
+                               double *ritz_min, double *ritz_max, double *alpha, double *beta) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(v0, WF4DVAR_EINVAL, "lanczos: v0 is NULL");
+    wf::lanczos(c, op, v0, steps, ritz_min, ritz_max, alpha, beta);
   });
 }
 

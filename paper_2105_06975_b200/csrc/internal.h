@@ -330,6 +330,10 @@ void csr_apply(Ctx &c, double *y, const double *x, const int *rowptr, const int 
 void apply_A(Ctx &c, const double *x, double *y);
 void apply_P(Ctx &c, const double *x, double *y);
 
+// spectral suite (spectral.cu)
+void lanczos(Ctx &c, int op, const double *v0, int steps, double *ritz_min, double *ritz_max,
+             double *alpha_out, double *beta_out);
+
 // Krylov
 void solve(Ctx &c, const double *rhs, double *x, const wf4dvar_solve_opts &o, wf4dvar_report *rep);
 

@@ -557,7 +557,9 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
   const int64_t rows = n / m;
   const int RB = m < 256 ? m : 256;
   const int gx = (m + RB - 1) / RB;
-  int gy = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + gx - 1) / gx, (rows + 255) / 256));
+  // enough blocks to keep ~6 x 256 threads per SM streaming (ncu r01k: 296 blocks left
+  // k_multiaxpy at 25% of DRAM bandwidth, stalled on memory latency)
+  int gy = (int)std::max<int64_t>(1, std::min<int64_t>((6 * 148 + gx - 1) / gx, (rows + 31) / 32));
   const int64_t rpb = (rows + gy - 1) / gy;
   gy = (int)((rows + rpb - 1) / rpb);
   const int jmax = mr + 1;

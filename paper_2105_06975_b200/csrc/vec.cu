@@ -154,7 +154,9 @@ RedGrid red_grid(const Ctx &c, int64_t n) {
   g.rows = n / m;
   g.RB = m < 256 ? m : 256;
   g.gx = (m + g.RB - 1) / g.RB;
-  g.gy = (int)std::max<int64_t>(1, std::min<int64_t>((4 * 148 + g.gx - 1) / g.gx, (g.rows + 255) / 256));
+  // >= ~6 blocks of 256 threads per SM even when rows = n/m is small (configs[2]:
+  // m = 1024, rows = 5100: the old rows/256 cap gave 80 blocks, 1.2 TB/s)
+  g.gy = (int)std::max<int64_t>(1, std::min<int64_t>((6 * 148 + g.gx - 1) / g.gx, (g.rows + 31) / 32));
   g.rpb = (g.rows + g.gy - 1) / g.gy;
   g.gy = (int)((g.rows + g.rpb - 1) / g.rpb);
   return g;

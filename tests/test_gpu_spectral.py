@@ -1,0 +1,77 @@
+"""GPU spectral suite through wf4dvar_lanczos.
+
+* OP_LHAT: extreme eigenvalues of L_M^{-T} L^T L L_M^{-1} with the paper's Dirichlet
+  heat model at s = 500 (M = M_dt, r = 0.4) against the numbers PRINTED in Supp.
+  Tables S2/S3 (tests/golden/lm_spectra_tables_S2_S3.json; minima to the printed 4
+  digits, maxima within 5e-4 -- the printed closed-form rows carry eigs errors of that
+  size) and against the oracle's dense eigensolve.
+* OP_PA: extreme eigenvalues of P_D^{-1} A on BASELINE.json configs[0] against the
+  oracle's dense generalised eigenproblem, and inside Theorem 3.1's intervals."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lhat as LH
+from oracle import models as OM
+from oracle.saddle import Precond, Saddle
+from synth import configs as SC
+
+from .helpers import seeded_vec
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def WF():
+    import paper_2105_06975_b200 as W
+    return W
+
+
+def lhat_ritz(k, Np1, steps=300, m=2):
+    prob = SC.paper_heat_problem(s=500, N=Np1 - 1, m=m, nsteps=1, with_rhs=False)
+    ctx = WF().Context.from_problem(prob, dict(shape="PD", lhat="LM", k=k, rhat="diag"))
+    v0 = torch.from_numpy(seeded_vec(prob.n, 17)).cuda()
+    return ctx.lanczos("LHAT", v0, steps)
+
+
+ROWS = json.load(open(os.path.join(GOLD, "lm_spectra_tables_S2_S3.json")))
+
+
+@pytest.mark.parametrize("row", [r for r in ROWS["rows"] if "min" in r] + ROWS["rows_dirichlet"],
+                         ids=lambda r: f"k{r['k']}-N+1={r['Np1']}")
+def test_lhat_extremes_match_printed_tables(row):
+    lo, hi = lhat_ritz(row["k"], row["Np1"])
+    for c in range(len(lo)):
+        assert abs(lo[c] - row["min"]) <= 6e-5, (lo, row)
+        assert abs(hi[c] - row["max"]) <= 5e-4, (hi, row)
+
+
+def test_lhat_extremes_match_dense_oracle():
+    k, Np1, s = 3, 8, 500
+    lo, hi = lhat_ritz(k, Np1, steps=400)
+    M = OM.heat_dirichlet_step(s, 0.4)
+    L = LH.assemble("L", [M] * (Np1 - 1), s)
+    LM = LH.assemble("LM", [M] * (Np1 - 1), s, k)
+    X = np.linalg.solve(LM.T, L.T)
+    ev = np.linalg.eigvalsh(X @ X.T)
+    np.testing.assert_allclose(lo, ev[0], rtol=1e-7)
+    np.testing.assert_allclose(hi, ev[-1], rtol=1e-9)
+
+
+@pytest.mark.parametrize("pc", [dict(shape="PD", lhat="LM", k=3, rhat="exact"),
+                                dict(shape="PD", lhat="L0", k=1, rhat="me"),
+                                dict(shape="PD", lhat="LM", k=2, rhat="rr")])
+def test_pa_extremes_c0_match_dense_generalised_eigenproblem(pc):
+    import scipy.linalg as sla
+    prob = SC.make_problem(0)
+    ctx = WF().Context.from_problem(prob, pc)
+    v0 = torch.from_numpy(seeded_vec(prob.n, 3)).cuda()
+    lo, hi = ctx.lanczos("PA", v0, 500)
+    sad = Saddle(prob)
+    opc = Precond(pc["shape"], pc["lhat"], pc["k"], pc["rhat"])
+    ev = np.sort(np.real(sla.eigvals(sad.assemble_A(), sad.assemble_P(opc))))
+    np.testing.assert_allclose(lo[0], ev[0], rtol=1e-7)
+    np.testing.assert_allclose(hi[0], ev[-1], rtol=1e-7)

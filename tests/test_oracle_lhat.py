@@ -142,3 +142,20 @@ def test_prop45_and_remark_bounds_heat():
                 assert ev[-1] <= SP.remark_upper(k) + 1e-10
             if k == 4:
                 assert ev[-1] <= SP.s6_upper() + 1e-10
+
+
+@pytest.mark.parametrize("k,Np1", [(3, 8), (4, 9), (4, 13)])
+def test_tables_S2_S3_rows_without_closed_form_dirichlet_heat(k, Np1):
+    """Supp. Tables S2/S3 rows beyond the closed forms, reproduced by the dense oracle
+    with the paper's Dirichlet heat model M = M_dt at s = 500, r = 0.4."""
+    rows = json.load(open(os.path.join(GOLD, "lm_spectra_tables_S2_S3.json")))["rows_dirichlet"]
+    row = next(r for r in rows if r["k"] == k and r["Np1"] == Np1)
+    s = 500
+    M = OM.heat_dirichlet_step(s, 0.4)
+    Ms = [M] * (Np1 - 1)
+    L = LH.assemble("L", Ms, s)
+    LM = LH.assemble("LM", Ms, s, k)
+    X = np.linalg.solve(LM.T, L.T)
+    ev = np.linalg.eigvalsh(X @ X.T)
+    assert round(ev[0], 4) == pytest.approx(row["min"], abs=1e-12)
+    assert abs(ev[-1] - row["max"]) <= 5e-4
