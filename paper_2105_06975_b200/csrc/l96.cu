@@ -313,4 +313,55 @@ void l96_step(Ctx &c, bool transpose, double sign, const double *in, const doubl
   c.launches++;
 }
 
+// Nonlinear forecast for the Gauss-Newton outer loop: for every local
+// window w with a global predecessor, out_w = M_w(x_{w-1}) = nsub nonlinear RK4 steps
+// of Lorenz-96 from the state of window w-1 (local, or the low halo on a rank
+// boundary).  Same thread mapping as k_l96_step.
+template <int IPT, bool SH>
+__global__ void __launch_bounds__(256) k_l96_forecast(double *out, const double *x,
+                                                      const double *halo, double F, double h,
+                                                      int s, int W, int m, int nsub, int w0) {
+  __shared__ double bx[L96Thread<IPT>::S_MAX * 32];
+  const int tid = threadIdx.y * 32 + threadIdx.x;
+  const int wp = tid >> 5, lw = tid & 31;
+  const int lane = lw >> 3, ty = lw & 7;
+  const int r = blockIdx.x * 32 + wp * 4 + lane;
+  double *const bxw = bx + wp * (L96Thread<IPT>::S_MAX * 4);
+  const int w = blockIdx.y;                    // local window
+  if (w0 + w < 1) return;                      // global window 0 has no forecast
+  const bool live = r < m;
+  const int64_t ld = (int64_t)W * m;
+  double xs[IPT];
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = SH ? ty * IPT + k : ty + 8 * k;
+    xs[k] = (live && i < s) ? (w == 0 ? halo[(int64_t)i * m + r] : x[i * ld + (int64_t)(w - 1) * m + r])
+                            : 0.0;
+  }
+  for (int st = 0; st < nsub; ++st) {
+    double x2[IPT], x3[IPT], x4[IPT], xn[IPT];
+    rk4_stages<IPT, SH>(xs, x2, x3, x4, xn, bxw, s, ty, lane, F, h);
+#pragma unroll
+    for (int k = 0; k < IPT; ++k) xs[k] = xn[k];
+  }
+  if (!live) return;
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = SH ? ty * IPT + k : ty + 8 * k;
+    if (i < s) out[i * ld + (int64_t)w * m + r] = xs[k];
+  }
+}
+
+void l96_forecast(Ctx &c, const double *x, double *out) {
+  dim3 grid((c.m + 31) / 32, c.W), block(32, 8);
+  LaunchScope ls(c, K_MODEL, (double)c.W * c.m * c.s * 29.0 * c.l96_nsub,
+                 (double)c.W * c.m * c.s * 16);
+  if (c.s == 40) k_l96_forecast<5, true><<<grid, block, 0, c.st>>>(out, x, c.halo_lo, c.l96_F, c.l96_dt, c.s, c.W, c.m, c.l96_nsub, c.w0);
+  else if (c.s == 64) k_l96_forecast<8, true><<<grid, block, 0, c.st>>>(out, x, c.halo_lo, c.l96_F, c.l96_dt, c.s, c.W, c.m, c.l96_nsub, c.w0);
+  else if (c.s <= 40) k_l96_forecast<5, false><<<grid, block, 0, c.st>>>(out, x, c.halo_lo, c.l96_F, c.l96_dt, c.s, c.W, c.m, c.l96_nsub, c.w0);
+  else k_l96_forecast<8, false><<<grid, block, 0, c.st>>>(out, x, c.halo_lo, c.l96_F, c.l96_dt, c.s, c.W, c.m, c.l96_nsub, c.w0);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
+}
+
 }  // namespace wf
