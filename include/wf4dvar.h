@@ -219,6 +219,20 @@ wf4dvar_status wf4dvar_solve(wf4dvar_ctx ctx, const double *rhs, double *x,
 wf4dvar_status wf4dvar_solve_host(wf4dvar_ctx ctx, const double *rhs_host, double *x_host,
                                   const wf4dvar_solve_opts *opts, wf4dvar_report *rep);
 
+/* Gauss-Newton outer loops of incremental 4D-Var.
+   Each of n_outer iterations, from the iterate x = (x_0..x_N): re-linearise (for L96
+   the tangent-linear trajectory becomes x itself: M_w about x_{w-1}), form the
+   right-hand side b_0 = x_b - x_0, b_w = M_w(x_{w-1}) - x_w (nonlinear forecast),
+   d_w = y_w - H x_w, third block 0 (reading A3), solve the saddle system with
+   `inner`, and update x += delta x.  Device buffers: xb [s][m] (used by the rank
+   owning window 0), y [p][W_local][m], x [s][W_local][m] (in: first guess, out:
+   final iterate).  Optional host outputs [n_outer*m] (row = outer iteration):
+   inner iteration counts, ||delta x||^2 and ||(b, d)||^2 per RHS.  An unconverged
+   inner loop still updates x.  Synchronous. */
+wf4dvar_status wf4dvar_outer_loop(wf4dvar_ctx ctx, const double *xb, const double *y, double *x,
+                                  int32_t n_outer, const wf4dvar_solve_opts *inner,
+                                  int32_t *inner_iters, double *dx_norm2, double *res_norm2);
+
 /* Spectral suite: extreme eigenvalues by batched Lanczos, one
    independent run per RHS column, `steps` steps from the start vector v0 (device,
    full vector layout of n_local doubles; OP_LHAT uses only its delta_x segment).

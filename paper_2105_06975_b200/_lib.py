@@ -92,6 +92,8 @@ _sig = {
     "wf4dvar_apply_AP_host": (C.c_int, [_ctx, C.c_void_p, C.c_void_p]),
     "wf4dvar_solve": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts), C.POINTER(Report)]),
     "wf4dvar_solve_host": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.POINTER(SolveOpts), C.POINTER(Report)]),
+    "wf4dvar_outer_loop": (C.c_int, [_ctx, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                     C.POINTER(SolveOpts), _ip, _dp, _dp]),
     "wf4dvar_lanczos": (C.c_int, [_ctx, C.c_int32, C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp]),
     "wf4dvar_profile_enable": (C.c_int, [_ctx, C.c_int32]),
     "wf4dvar_profile_read": (C.c_int, [_ctx, C.POINTER(KStat), C.c_int32, _ip]),
@@ -394,6 +396,22 @@ class Context:
                    mark_tol=1e-8, check_every=1, history=False):
         return self._solve(_lib.wf4dvar_solve_host, rhs, x, solver, tol, maxit, restart,
                            mark_tol, check_every, history)
+
+    def outer_loop(self, xb, y, x, n_outer, solver="gmres", tol=1e-10, maxit=1000, restart=50,
+                   check_every=1):
+        """Gauss-Newton outer loops (device xb [s][m], y [p][W][m], x [s][W][m] in/out)."""
+        opts = SolveOpts({"minres": MINRES, "gmres": GMRES}[solver], float(tol), int(maxit),
+                         int(restart), float(tol), int(check_every))
+        its = np.zeros(n_outer * self.m, np.int32)
+        dxn = np.zeros(n_outer * self.m)
+        res = np.zeros(n_outer * self.m)
+        self._check(_lib.wf4dvar_outer_loop(self._h, _ptr(xb) if xb is not None else None,
+                                            _ptr(y), _ptr(x), int(n_outer), C.byref(opts),
+                                            _np_ptr(its, C.c_int32), _np_ptr(dxn, C.c_double),
+                                            _np_ptr(res, C.c_double)))
+        return dict(inner_iters=its.reshape(n_outer, self.m),
+                    dx_norm=np.sqrt(dxn.reshape(n_outer, self.m)),
+                    res_norm=np.sqrt(res.reshape(n_outer, self.m)))
 
     def lanczos(self, op, v0, steps, tridiag=False):
         """Extreme Ritz values per RHS of P_D^{-1} A (op="PA") or L_hat^{-T} L^T L L_hat^{-1}

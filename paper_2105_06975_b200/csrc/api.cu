@@ -333,6 +333,16 @@ wf4dvar_status wf4dvar_solve_host(wf4dvar_ctx ctx, const double *rhs_host, doubl
   });
 }
 
+wf4dvar_status wf4dvar_outer_loop(wf4dvar_ctx ctx, const double *xb, const double *y, double *x,
+                                  int32_t n_outer, const wf4dvar_solve_opts *inner,
+                                  int32_t *inner_iters, double *dx_norm2, double *res_norm2) {
+  return guarded(ctx, [&](Ctx &c) {
+    WF_REQUIRE(y && x && inner, WF4DVAR_EINVAL, "outer_loop: bad pointers");
+    WF_REQUIRE(xb || c.w0 > 0, WF4DVAR_EINVAL, "outer_loop: xb is NULL on the rank owning window 0");
+    wf::outer_loop(c, xb, y, x, n_outer, *inner, inner_iters, dx_norm2, res_norm2);
+  });
+}
+
 wf4dvar_status wf4dvar_lanczos(wf4dvar_ctx ctx, int32_t op, const double *v0, int32_t steps,
                                double *ritz_min, double *ritz_max, double *alpha, double *beta) {
   return guarded(ctx, [&](Ctx &c) {

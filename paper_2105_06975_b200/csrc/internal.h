@@ -172,6 +172,7 @@ struct Ctx {
   double *ws_t = nullptr;         // A+P intermediate / P scratch (segment-sized)
   double *ws_seg = nullptr;       // one s*ncol segment
   double *ws_lr = nullptr;        // low-rank scratch [r][ncol]
+  double *outer_ws = nullptr;     // outer loop: rhs, dx, forecast
   double *dot_part = nullptr;     // partial sums
   int dot_part_cap = 0;
   double *hostbuf = nullptr;      // pinned
@@ -329,6 +330,11 @@ void csr_apply(Ctx &c, double *y, const double *x, const int *rowptr, const int 
 
 void apply_A(Ctx &c, const double *x, double *y);
 void apply_P(Ctx &c, const double *x, double *y);
+
+// Gauss-Newton outer loops (outer.cu)
+void outer_loop(Ctx &c, const double *xb, const double *y, double *x, int n_outer,
+                const wf4dvar_solve_opts &inner, int32_t *inner_iters, double *dx_norm2,
+                double *res_norm2);
 
 // spectral suite (spectral.cu)
 void lanczos(Ctx &c, int op, const double *v0, int steps, double *ritz_min, double *ritz_max,
