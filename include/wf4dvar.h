@@ -138,7 +138,14 @@ typedef struct {
   int32_t npvec;
   double block_tol;
   int32_t maxsize, numproc;
+  /* Factors of D_hat and R_hat: WF4DVAR_FACTOR_CHOL (0, default)
+     dense Cholesky, applied as DMMA TRSM (reading A4); WF4DVAR_FACTOR_ICHOL (1) the
+     paper's incomplete Cholesky with zero fill on the non-zero pattern (Matlab ichol
+     'nofill'): the preconditioner blocks become L L^T, applied as
+     sparse triangular solves.  For compact-support covariances; not with R_ME. */
+  int32_t factor;
 } wf4dvar_precond;
+typedef enum { WF4DVAR_FACTOR_CHOL = 0, WF4DVAR_FACTOR_ICHOL = 1 } wf4dvar_factor;
 
 /* Time-window sharding ("the model propagations M_i can be
  * run in parallel", P:L253 the parallel-in-time L_M(k)).  With world > 1 rank g

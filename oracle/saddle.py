@@ -26,6 +26,7 @@ import numpy as np
 import scipy.linalg as sla
 
 from . import lhat as LH
+from . import ichol as IC
 from . import rhat as RH
 from .models import model_matrices
 
@@ -46,6 +47,9 @@ class Precond:
     block_tol: float = float("inf")
     maxsize: int = 0
     numproc: int = 0
+    # "chol": exact Cholesky factors (reading A4); "ichol": IC(0) factors as the paper
+    # applies them: the preconditioner block becomes L L^T
+    factor: str = "chol"
 
 
 def selection_matrix(H_idx, s):
@@ -104,13 +108,29 @@ class Saddle:
     def rhat_matrix(self, pc):
         key = ("Rhat", pc.rhat, pc.gamma, pc.T, pc.block,
                tuple(pc.pvec) if pc.pvec is not None else None, pc.block_tol, pc.maxsize,
-               pc.numproc)
+               pc.numproc, pc.factor)
         if key not in self._cache:
             if pc.rhat == "block" and pc.pvec is not None:
-                self._cache[key] = RH.r_block(self.R, list(pc.pvec), pc.block_tol,
-                                              pc.maxsize or None, pc.numproc or None)[0]
+                M = RH.r_block(self.R, list(pc.pvec), pc.block_tol,
+                               pc.maxsize or None, pc.numproc or None)[0]
             else:
-                self._cache[key] = RH.rhat(self.R, pc.rhat, pc.gamma, pc.T, pc.block)
+                M = RH.rhat(self.R, pc.rhat, pc.gamma, pc.T, pc.block)
+            if pc.factor == "ichol" and pc.rhat != "diag":
+                assert pc.rhat != "me", "R_ME with IC(0) factors is not supported"
+                Lf = IC.ichol0(M)
+                M = Lf @ Lf.T
+            self._cache[key] = M
+        return self._cache[key]
+
+    def dhat_matrix(self, pc, w):
+        """D_hat block of window w: D (+ ridge), or L L^T of its IC(0) factor."""
+        key = ("Dhat", min(w, 1), pc.ridge, pc.factor)
+        if key not in self._cache:
+            M = RH.dhat(self.Dblk(w), pc.ridge)
+            if pc.factor == "ichol":
+                Lf = IC.ichol0(M)
+                M = Lf @ Lf.T
+            self._cache[key] = M
         return self._cache[key]
 
     def _spd_solve(self, key, mat_fn, rhs):
@@ -142,7 +162,7 @@ class Saddle:
         Lh = LH.assemble(pc.lhat, self.Ms, s, pc.k)
         Z = np.zeros
         if pc.shape == "PD":
-            Dh = sla.block_diag(RH.dhat(self.B, pc.ridge), *([RH.dhat(self.Q, pc.ridge)] * self.N))
+            Dh = sla.block_diag(self.dhat_matrix(pc, 0), *([self.dhat_matrix(pc, 1)] * self.N))
             Sh = Lh.T @ np.linalg.solve(D, Lh)
             return sla.block_diag(Dh, Rh, Sh)
         return np.block([[D, Z((W * s, W * p)), Lh],
@@ -176,7 +196,7 @@ class Saddle:
     def _rhat_inv(self, pc, x2):
         key = ("cho_Rhat", pc.rhat, pc.gamma, pc.T, pc.block,
                tuple(pc.pvec) if pc.pvec is not None else None, pc.block_tol, pc.maxsize,
-               pc.numproc)
+               pc.numproc, pc.factor)
         self.counters["Rhat_inv"] += self.W
         return [self._spd_solve(key, lambda: self.rhat_matrix(pc), x2[w]) for w in range(self.W)]
 
@@ -186,8 +206,8 @@ class Saddle:
         c = self.counters
         c2 = self._rhat_inv(pc, x2)
         if pc.shape == "PD":
-            c1 = [self._spd_solve(("cho_D", min(w, 1), pc.ridge),
-                                  lambda w=w: RH.dhat(self.Dblk(w), pc.ridge), x1[w])
+            c1 = [self._spd_solve(("cho_D", min(w, 1), pc.ridge, pc.factor),
+                                  lambda w=w: self.dhat_matrix(pc, w), x1[w])
                   for w in range(W)]
             t = LH.solve_T(pc.lhat, self.Ms, x3, pc.k)
             t = [self.Dblk(w) @ t[w] for w in range(W)]

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libwf4dvar.so")
-SOURCES = ["api.cu", "saddle.cu", "gemm.cu", "trsm.cu", "model.cu", "l96.cu", "vec.cu", "krylov.cu", "comm.cu", "spectral.cu", "outer.cu"]
+SOURCES = ["api.cu", "saddle.cu", "gemm.cu", "trsm.cu", "model.cu", "l96.cu", "vec.cu", "krylov.cu", "comm.cu", "spectral.cu", "outer.cu", "sparse.cu"]
 ARCH = "-gencode=arch=compute_100a,code=sm_100a"
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 

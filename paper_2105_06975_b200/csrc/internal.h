@@ -84,6 +84,13 @@ void fill_diag_pack(Ctx &c, const double *G, int n, bool upper, double *pack);  
 
 struct Ctx;
 
+// ---------------------------------------------------------------- IC(0) factors (sparse.cu)
+struct SparseFactor {
+  int n = 0, nnz = 0;
+  int *lrp = nullptr, *lci = nullptr, *urp = nullptr, *uci = nullptr;
+  double *lv = nullptr, *uv = nullptr, *dinv = nullptr;
+};
+
 // ---------------------------------------------------------------- transport (comm.cu)
 // Stream-ordered collectives of the time-window-sharded path.
 struct Comm {
@@ -163,6 +170,7 @@ struct Ctx {
   double *GR = nullptr, *GRt = nullptr;                                  // chol(R_hat base)
   double *PB = nullptr, *PBt = nullptr, *PQ = nullptr, *PQt = nullptr;  // diagonal-tile packs
   double *PR = nullptr, *PRt = nullptr;
+  SparseFactor icB, icQ, icR;     // IC(0) factors (pc.factor == WF4DVAR_FACTOR_ICHOL)
   double *Rdiag_inv = nullptr;                                           // [p]
   std::vector<int> rblk_starts;   // R_block (Algorithm 1): block starts + p (empty = uniform)
   std::vector<int> pvec_store;    // copy of the caller's pvec (pc.pvec points here)
@@ -354,6 +362,8 @@ void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_
           double *out);
 
 void setup_precond(Ctx &c);
+void make_ichol(Ctx &c, const std::vector<double> &A, int n, const char *name, SparseFactor &f);
+void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int c0, int ncols);
 std::vector<int> algorithm1_blocks(const std::vector<double> &R, int p, const std::vector<int> &pvec,
                                    double tol, int maxsize, int numproc);
 void free_precond(Ctx &c);

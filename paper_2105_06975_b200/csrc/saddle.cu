@@ -48,6 +48,16 @@ static void d_product(Ctx &c, const double *X, double *Y, const double *Z, doubl
 void dhat_inv(Ctx &c, const double *x1, double *y1) {
   const int s = c.s, m = c.m;
   const int64_t ld = c.ncol;
+  if (c.pc.factor == WF4DVAR_FACTOR_ICHOL) {   // (L L^T)^{-1} with the IC(0) factors
+    if (c.w0 == 0) {
+      ichol_solve(c, c.icB, x1, y1, 0, m);
+      ichol_solve(c, c.icQ, x1, y1, m, (int)ld - m);
+    } else {
+      ichol_solve(c, c.icQ, x1, y1, 0, (int)ld);
+    }
+    c.n_Dhat_inv += c.WG;
+    return;
+  }
   TrsmProb f[2], b[2];
   int np;
   if (c.w0 == 0) {
@@ -74,6 +84,11 @@ void rhat_inv(Ctx &c, const double *x2, double *y2) {
   if (c.pc.rhat == WF4DVAR_RDIAG) {
     scale_rows(c, y2, x2, c.Rdiag_inv, p);
     return;   // R_diag applications are not counted in the paper's tables
+  }
+  if (c.pc.factor == WF4DVAR_FACTOR_ICHOL) {
+    ichol_solve(c, c.icR, x2, y2, 0, (int)ld);
+    c.n_Rhat_inv += c.WG;
+    return;
   }
   int blk = (c.pc.rhat == WF4DVAR_RBLOCK) ? c.pc.block : 0;
   TrsmProb f{c.GR, p, x2, ld, y2, ld, p, (int)ld, blk};
@@ -292,6 +307,12 @@ void free_precond(Ctx &c) {
   dev_free(c, c.GR); dev_free(c, c.GRt); dev_free(c, c.Rdiag_inv);
   dev_free(c, c.PB); dev_free(c, c.PBt); dev_free(c, c.PQ); dev_free(c, c.PQt);
   dev_free(c, c.PR); dev_free(c, c.PRt);
+  for (SparseFactor *f : {&c.icB, &c.icQ, &c.icR}) {
+    int *ip[4] = {f->lrp, f->lci, f->urp, f->uci};
+    for (int *q : ip) if (q) { auto it = std::find(c.allocs.begin(), c.allocs.end(), (void *)q); if (it != c.allocs.end()) c.allocs.erase(it); cudaFree(q); }
+    dev_free(c, f->lv); dev_free(c, f->uv); dev_free(c, f->dinv);
+    *f = SparseFactor{};
+  }
   dev_free(c, c.U_me); dev_free(c, c.Kinv_me); dev_free(c, c.ws_lr);
   c.r_me = 0;
 }
@@ -364,8 +385,19 @@ void setup_precond(Ctx &c) {
   free_precond(c);
   Solver sv(c.st);
   std::vector<double> h;
+  WF_REQUIRE(pc.factor == WF4DVAR_FACTOR_CHOL || pc.factor == WF4DVAR_FACTOR_ICHOL, WF4DVAR_EINVAL,
+             "bad factor");
+  WF_REQUIRE(!(pc.factor == WF4DVAR_FACTOR_ICHOL && pc.rhat == WF4DVAR_RME), WF4DVAR_EINVAL,
+             "R_ME with IC(0) factors is not supported");
   // ---- D_hat factors (P_D only)
-  if (pc.shape == WF4DVAR_PD) {
+  if (pc.shape == WF4DVAR_PD && pc.factor == WF4DVAR_FACTOR_ICHOL) {
+    for (int which = 0; which < 2; ++which) {
+      h.resize((size_t)s * s);
+      WF_CUDA(memcpy_sync(c, h.data(), which == 0 ? c.B : c.Q, h.size() * 8, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < s; ++i) h[(size_t)i * s + i] += pc.dhat_ridge;
+      make_ichol(c, h, s, which == 0 ? "B_hat" : "Q_hat", which == 0 ? c.icB : c.icQ);
+    }
+  } else if (pc.shape == WF4DVAR_PD) {
     c.GB = c.alloc<double>((size_t)s * s); c.GBt = c.alloc<double>((size_t)s * s);
     c.GQ = c.alloc<double>((size_t)s * s); c.GQt = c.alloc<double>((size_t)s * s);
     for (int which = 0; which < 2; ++which) {
@@ -492,6 +524,13 @@ void setup_precond(Ctx &c) {
           WF_CUDA(memcpy_sync(c, c.Kinv_me, Kinv.data(), Kinv.size() * 8, cudaMemcpyHostToDevice));
         }
       }
+    }
+    if (pc.factor == WF4DVAR_FACTOR_ICHOL) {
+      std::vector<double> Rf((size_t)p * p);
+      WF_CUDA(memcpy_sync(c, Rf.data(), Rdev, Rf.size() * 8, cudaMemcpyDeviceToHost));
+      make_ichol(c, Rf, p, name, c.icR);
+      cudaFree(Rdev);
+      return;
     }
     c.GR = c.alloc<double>((size_t)p * p);
     c.GRt = c.alloc<double>((size_t)p * p);

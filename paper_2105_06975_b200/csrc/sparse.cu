@@ -1,0 +1,145 @@
+// Sparse incomplete-Cholesky factors: the paper applies
+// D_hat^{-1} and R_hat^{-1} "using the incomplete Cholesky factors computed with the
+// Matlab function ichol with zero-fill, i.e. using the same sparsity structure as B
+// and Q" (R_i: P:L600).
+//
+// Setup (host, untimed): IC(0) of the n x n matrix on the pattern of its non-zero
+// lower triangle, row by row:  for k in pattern(i), k < i:
+//     L_ik = (A_ik - sum_{j in pattern(i) & pattern(k), j < k} L_ij L_kj) / L_kk
+//     L_ii = sqrt(A_ii - sum_{j in pattern(i), j < i} L_ij^2)
+// stored as CSR of the strictly lower part, its transpose (the upper factor L^T) and
+// the reciprocal diagonal.
+// Apply (device): y = L^{-T} L^{-1} x as two sparse triangular solves, one thread per
+// (window, RHS) column walking the rows in order -- the rows of one column are a true
+// recurrence; the W m columns are independent and the reads of the factor row are
+// warp-broadcast, the reads/writes of the solution coalesced across the columns.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "internal.h"
+
+namespace wf {
+
+// forward (upper = 0): y_i = (x_i - sum_{k<i} L_ik y_k) / L_ii, rows ascending
+// backward (upper = 1): y_i = (x_i - sum_{k>i} U_ik y_k) / U_ii, rows descending
+// Columns [c0, c0 + ncols) of [n][ld] arrays; x may alias y.
+__global__ void k_sptrsv(double *y, const double *x, const int *rowptr, const int *col,
+                         const double *val, const double *dinv, int n, int64_t ld, int c0,
+                         int ncols, int upper) {
+  const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (cc >= ncols) return;
+  const int64_t c = c0 + cc;
+  for (int t = 0; t < n; ++t) {
+    const int i = upper ? n - 1 - t : t;
+    double acc = x[(int64_t)i * ld + c];
+    const int k0 = rowptr[i], k1 = rowptr[i + 1];
+    int k = k0;
+    // 4 independent partial sums: the loads of one row are not serialised
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (; k + 4 <= k1; k += 4) {
+      a0 = fma(__ldg(val + k), y[(int64_t)__ldg(col + k) * ld + c], a0);
+      a1 = fma(__ldg(val + k + 1), y[(int64_t)__ldg(col + k + 1) * ld + c], a1);
+      a2 = fma(__ldg(val + k + 2), y[(int64_t)__ldg(col + k + 2) * ld + c], a2);
+      a3 = fma(__ldg(val + k + 3), y[(int64_t)__ldg(col + k + 3) * ld + c], a3);
+    }
+    for (; k < k1; ++k) a0 = fma(__ldg(val + k), y[(int64_t)__ldg(col + k) * ld + c], a0);
+    acc -= (a0 + a1) + (a2 + a3);
+    y[(int64_t)i * ld + c] = acc * __ldg(dinv + i);
+  }
+}
+
+// IC(0) of the row-major n x n host matrix A (exact zeros outside the pattern).
+static void ichol0_host(const std::vector<double> &A, int n, const char *name,
+                        std::vector<int> &lrp, std::vector<int> &lci, std::vector<double> &lv,
+                        std::vector<double> &diag) {
+  // pattern of the strictly lower triangle, row by row (column indices ascending)
+  std::vector<std::vector<int>> pat(n);
+  std::vector<std::vector<double>> Lrow(n);
+  diag.assign(n, 0.0);
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j)
+      if (A[(size_t)i * n + j] != 0.0) pat[i].push_back(j);
+  for (int i = 0; i < n; ++i) {
+    Lrow[i].assign(pat[i].size(), 0.0);
+    for (size_t a = 0; a < pat[i].size(); ++a) {
+      const int k = pat[i][a];
+      // sum over j < k in pattern(i) and pattern(k): merge of two sorted lists
+      double sum = 0.0;
+      size_t p = 0, q = 0;
+      while (p < a && q < pat[k].size()) {
+        const int jp = pat[i][p], jq = pat[k][q];
+        if (jp == jq) { sum += Lrow[i][p] * Lrow[k][q]; ++p; ++q; }
+        else if (jp < jq) ++p;
+        else ++q;
+      }
+      Lrow[i][a] = (A[(size_t)i * n + k] - sum) / diag[k];
+    }
+    double d = A[(size_t)i * n + i];
+    for (double v : Lrow[i]) d -= v * v;
+    WF_REQUIRE(d > 0.0, WF4DVAR_ENOTSPD,
+               std::string("IC(0) breakdown (non-positive pivot) of ") + name + " at row " +
+                   std::to_string(i));
+    diag[i] = std::sqrt(d);
+  }
+  lrp.assign(n + 1, 0);
+  lci.clear();
+  lv.clear();
+  for (int i = 0; i < n; ++i) {
+    for (size_t a = 0; a < pat[i].size(); ++a) {
+      lci.push_back(pat[i][a]);
+      lv.push_back(Lrow[i][a]);
+    }
+    lrp[i + 1] = (int)lci.size();
+  }
+}
+
+void make_ichol(Ctx &c, const std::vector<double> &A, int n, const char *name, SparseFactor &f) {
+  std::vector<int> lrp, lci;
+  std::vector<double> lv, diag;
+  ichol0_host(A, n, name, lrp, lci, lv, diag);
+  const int nnz = (int)lci.size();
+  // upper factor L^T as CSR: row k of L^T holds column k of L
+  std::vector<int> urp(n + 1, 0), uci(nnz);
+  std::vector<double> uv(nnz), dinv(n);
+  for (int k = 0; k < nnz; ++k) urp[lci[k] + 1]++;
+  for (int i = 0; i < n; ++i) urp[i + 1] += urp[i];
+  std::vector<int> fill(urp.begin(), urp.end() - 1);
+  for (int i = 0; i < n; ++i)
+    for (int k = lrp[i]; k < lrp[i + 1]; ++k) {
+      const int dst = fill[lci[k]]++;
+      uci[dst] = i;
+      uv[dst] = lv[k];
+    }
+  for (int i = 0; i < n; ++i) dinv[i] = 1.0 / diag[i];
+  f.n = n;
+  f.nnz = nnz;
+  f.lrp = c.alloc<int>(n + 1); f.urp = c.alloc<int>(n + 1);
+  f.lci = c.alloc<int>(std::max(nnz, 1)); f.uci = c.alloc<int>(std::max(nnz, 1));
+  f.lv = c.alloc<double>(std::max(nnz, 1)); f.uv = c.alloc<double>(std::max(nnz, 1));
+  f.dinv = c.alloc<double>(n);
+  WF_CUDA(memcpy_sync(c, f.lrp, lrp.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+  WF_CUDA(memcpy_sync(c, f.urp, urp.data(), (n + 1) * 4, cudaMemcpyHostToDevice));
+  if (nnz) {
+    WF_CUDA(memcpy_sync(c, f.lci, lci.data(), nnz * 4, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, f.uci, uci.data(), nnz * 4, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, f.lv, lv.data(), (size_t)nnz * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, f.uv, uv.data(), (size_t)nnz * 8, cudaMemcpyHostToDevice));
+  }
+  WF_CUDA(memcpy_sync(c, f.dinv, dinv.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+}
+
+// y[:, c0:c0+ncols] = (L L^T)^{-1} x[:, c0:c0+ncols] over an [n][ncol] segment
+void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int c0, int ncols) {
+  if (ncols <= 0) return;
+  const double cols = ncols;
+  LaunchScope ls(c, K_TRSM, 2.0 * 2.0 * f.nnz * cols + 2.0 * f.n * cols,
+                 8.0 * (2.0 * f.nnz + 4.0 * f.n * cols));
+  const unsigned g = (unsigned)((ncols + 127) / 128);
+  k_sptrsv<<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0, ncols, 0);
+  k_sptrsv<<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol, c0, ncols, 1);
+  WF_CUDA(cudaGetLastError());
+  c.launches += 2;
+}
+
+}  // namespace wf

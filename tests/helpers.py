@@ -15,7 +15,7 @@ def oracle_precond(pc):
                    block=d.get("block", 0), ridge=d.get("ridge", 0.0),
                    pvec=tuple(d["pvec"]) if d.get("pvec") is not None else None,
                    block_tol=d.get("block_tol", float("inf")), maxsize=d.get("maxsize", 0),
-                   numproc=d.get("numproc", 0))
+                   numproc=d.get("numproc", 0), factor=d.get("factor", "chol"))
 
 
 class OracleCols:
