@@ -24,7 +24,7 @@ namespace wf {
 
 constexpr int TB = 64;  // rows per triangle tile
 // The in-panel GEMMs are short (K < SB) and latency bound: a 4-deep cp.async ring.
-#define TRSM_STAGES 3
+#define TRSM_STAGES 4
 
 template <int NB>
 using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, TRSM_STAGES>,
@@ -42,18 +42,13 @@ struct TrsmLaunch {
 };
 
 template <int NB, bool UPPER, bool V16>
-__global__ void __launch_bounds__(128, (NB == 64 ? 2 : 6)) k_trsm(const TrsmLaunch L) {
+__global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   using C = TrsmCfg<NB>;
   extern __shared__ __align__(16) double smem[];
-  // The cp.async ring of the tile GEMM and the diagonal tile (sG | sD) share one
-  // region: the tile is copied in after the GEMM has drained the ring.  Keeps the
-  // CTA at ~61 KB so it can co-reside with two GEMM CTAs (81 KB each) of the
-  // concurrently running covariance product (apply_P: S_hat^{-1} || D_hat^{-1}).
-  constexpr int kPipe = C::SMEM_DOUBLES > kDiagPack ? C::SMEM_DOUBLES : kDiagPack;
-  double *sPipe = smem;                        // kPipe
-  double *sG = smem;                           // [64][65] diagonal tile, transposed
+  double *sPipe = smem;                        // C::SMEM_DOUBLES
+  double *sT = smem + C::SMEM_DOUBLES;         // [64][NB+1]
+  double *sG = sT + TB * (NB + 1);             // [64][65] diagonal tile, transposed
   double *sD = sG + TB * (TB + 1);             // [64] reciprocal diagonal
-  double *sT = smem + kPipe;                   // [64][NB+1]
 
   int panel = blockIdx.x, gi = 0;
   if (panel >= L.panels0) { panel -= L.panels0; gi = 1; }
@@ -74,10 +69,15 @@ __global__ void __launch_bounds__(128, (NB == 64 ? 2 : 6)) k_trsm(const TrsmLaun
   for (int it = 0; it < ntile; ++it) {
     const int ti = UPPER ? (ntile - 1 - it) : it;
     const int r0 = slo + ti * TB, r1 = min(shi, r0 + TB), nr = r1 - r0;
-    // setup-time pack of this diagonal tile (ncu r01g: building it in-kernel from
-    // strided global loads + reciprocals was the top stall of k_trsm)
+    // ---- setup-time pack of this diagonal tile (ncu r01g: building it in-kernel from
+    // strided global loads + reciprocals was the top stall of k_trsm): one contiguous
+    // 33 KB cp.async copy straight into sG|sD, overlapped with the tile GEMM below
     const double *dpk = (P.dpack && (r0 % TB) == 0) ? P.dpack + (int64_t)(r0 / TB) * kDiagPack
                                                       : nullptr;
+    if (dpk) {
+      for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(sG + e, dpk + e, 16);
+      cp_async_commit();
+    }
     // ---- in-segment off-diagonal update: acc = G[r0:r1, K] * Y[K, panel]
     const int kbeg = UPPER ? r1 : slo;
     const int kend = UPPER ? shi : r0;
@@ -89,12 +89,6 @@ __global__ void __launch_bounds__(128, (NB == 64 ? 2 : 6)) k_trsm(const TrsmLaun
     if (kend > kbeg)
       tile_mainloop<C, V16>(sPipe, acc, G + (int64_t)r0 * P.ldg, P.ldg, Y + c0, P.ldy, 0, 0, kbeg,
                             kend, nr, ncols - c0);
-    // ---- the ring is drained (tile_mainloop ends with wait<0> + barrier): copy the
-    // 33 KB diagonal pack into it, overlapped with forming T below
-    if (dpk) {
-      for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(sG + e, dpk + e, 16);
-      cp_async_commit();
-    }
     // ---- T = X - acc  -> shared memory
 #pragma unroll
     for (int i = 0; i < C::FM; ++i) {
@@ -213,8 +207,7 @@ double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
 template <int NB, bool UPPER>
 static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   using C = TrsmCfg<NB>;
-  constexpr int kPipe = C::SMEM_DOUBLES > kDiagPack ? C::SMEM_DOUBLES : kDiagPack;
-  size_t smem = (kPipe + TB * (NB + 1)) * sizeof(double);
+  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + TB * (TB + 1) + TB) * sizeof(double);
   auto kern = v16 ? k_trsm<NB, UPPER, true> : k_trsm<NB, UPPER, false>;
   static bool attr[2] = {false, false};
   if (!attr[v16]) {
