@@ -363,6 +363,42 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     return;
   }
   const int nsb = (n + SB - 1) / SB;
+  static int left_env = -1;
+  if (left_env < 0) {
+    const char *e = getenv("WF4DVAR_TRSM_LEFT");   // tuning experiments only
+    left_env = e ? atoi(e) : 0;
+  }
+  if (left_env) {
+    // left-looking: before solving super-block b, ONE GEMM brings in every solved
+    // block (K = all rows solved so far), then the panel kernel solves b in place
+    for (int it = 0; it < nsb; ++it) {
+      const int kb = upper ? nsb - 1 - it : it;
+      const int lo = kb * SB, hi = std::min(n, lo + SB);
+      TrsmProb cur[2];
+      for (int i = 0; i < np; ++i) cur[i] = probs[i];
+      const int klo = upper ? hi : 0, khi = upper ? n : lo;   // already solved rows
+      if (khi > klo) {
+        GemmProb g[2];
+        for (int i = 0; i < np; ++i) {
+          const TrsmProb &P = probs[i];
+          GemmProb &q = g[i];
+          q = GemmProb{};
+          q.A = P.G + (int64_t)lo * P.ldg + klo; q.lda = P.ldg;
+          q.X = P.Y + (int64_t)klo * P.ldy; q.ldx = P.ldy;
+          q.Y = P.Y + (int64_t)lo * P.ldy; q.ldy = P.ldy;
+          q.Z = P.X + (int64_t)lo * P.ldx; q.ldz = P.ldx;
+          q.M = hi - lo; q.N = P.ncols; q.K = khi - klo;
+          q.alpha = -1.0; q.beta = 1.0;
+          cur[i].X = cur[i].Y; cur[i].ldx = cur[i].ldy;   // the block is now in Y
+        }
+        c.gemm_cls = K_TRSM_UPD;
+        launch_gemm(c, g, np, 1);
+        c.gemm_cls = K_GEMM;
+      }
+      trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
+    }
+    return;
+  }
   TrsmProb cur[2];
   for (int i = 0; i < np; ++i) cur[i] = probs[i];
   for (int it = 0; it < nsb; ++it) {
