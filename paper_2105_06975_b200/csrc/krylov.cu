@@ -342,12 +342,30 @@ __global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc[k] = 0.0;
   if (r < m && u < U) {
-    for (int64_t row = row0 + u; row < row1; row += U) {
-      int64_t f = row * m + r;
-      double wv = w[f];
+    // 4 rows per iteration: up to 32 independent basis loads in flight and 4 x 2 KB
+    // contiguous runs per vector per block (ncu r01q: the 1-row loop reached 44% of
+    // DRAM bandwidth, stalled on long-scoreboard)
+    constexpr int RU = 4;
+    for (int64_t row = row0 + u; row < row1; row += (int64_t)U * RU) {
+      double wv[RU];
+      int64_t f[RU];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (i0 + k < nv) acc[k] = fma(V[(int64_t)(i0 + k) * n + f], wv, acc[k]);
+      for (int q = 0; q < RU; ++q) {
+        const int64_t rq = row + (int64_t)q * U;
+        f[q] = rq * m + r;
+        wv[q] = rq < row1 ? w[f[q]] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (i0 + k < nv) {
+          const double *Vk = V + (int64_t)(i0 + k) * n;
+          double vv[RU];
+#pragma unroll
+          for (int q = 0; q < RU; ++q) vv[q] = (row + (int64_t)q * U < row1) ? __ldcs(Vk + f[q]) : 0.0;
+#pragma unroll
+          for (int q = 0; q < RU; ++q) acc[k] = fma(vv[q], wv[q], acc[k]);
+        }
+      }
     }
   }
 #pragma unroll
@@ -388,23 +406,51 @@ __global__ void __launch_bounds__(256) k_multiaxpy(const double *V, int64_t n, i
   const int64_t row0 = (int64_t)blockIdx.y * rpb, row1 = min(rows, row0 + rpb);
   double nn = 0.0;
   if (r < m && u < U) {
-    for (int64_t row = row0 + u; row < row1; row += U) {
-      int64_t f = row * m + r;
-      double v = w[f];
-      // batches of 8 independent basis loads in flight (ncu r01i: the one-at-a-time
-      // dependent load+FMA chain ran this HBM-bound kernel at 28% of bandwidth);
-      // the fixed i order keeps the result deterministic
-      int i = 0;
-      for (; i + 8 <= nv; i += 8) {
-        double vv[8];
+    // 4 rows x 4 basis vectors per step: 16 independent loads in flight, each h
+    // coefficient loaded once per 4 rows, contiguous 2 KB row runs per block (ncu
+    // r01i/r01q: the 1-row dependent chain ran at 28% / 43% of DRAM bandwidth); the
+    // fixed i order keeps the result deterministic
+    constexpr int RU = 4, IB = 4;
+    for (int64_t row = row0 + u; row < row1; row += (int64_t)U * RU) {
+      double v[RU];
+      int64_t f[RU];
+      bool ok[RU];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) vv[k] = __ldcs(V + (int64_t)(i + k) * n + f);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v = fma(-vv[k], __ldg(h + (i + k) * m + r), v);
+      for (int q = 0; q < RU; ++q) {
+        const int64_t rq = row + (int64_t)q * U;
+        ok[q] = rq < row1;
+        f[q] = rq * m + r;
+        v[q] = ok[q] ? w[f[q]] : 0.0;
       }
-      for (; i < nv; ++i) v = fma(-__ldcs(V + (int64_t)i * n + f), __ldg(h + i * m + r), v);
-      w[f] = v;
-      nn = fma(v, v, nn);
+      int i = 0;
+      for (; i + IB <= nv; i += IB) {
+        double vv[IB][RU], hh[IB];
+#pragma unroll
+        for (int k = 0; k < IB; ++k) {
+          hh[k] = __ldg(h + (i + k) * m + r);
+#pragma unroll
+          for (int q = 0; q < RU; ++q)
+            vv[k][q] = ok[q] ? __ldcs(V + (int64_t)(i + k) * n + f[q]) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < IB; ++k)
+#pragma unroll
+          for (int q = 0; q < RU; ++q) v[q] = fma(-vv[k][q], hh[k], v[q]);
+      }
+      for (; i < nv; ++i) {
+        const double hi = __ldg(h + i * m + r);
+        double vv[RU];
+#pragma unroll
+        for (int q = 0; q < RU; ++q) vv[q] = ok[q] ? __ldcs(V + (int64_t)i * n + f[q]) : 0.0;
+#pragma unroll
+        for (int q = 0; q < RU; ++q) v[q] = fma(-vv[q], hi, v[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < RU; ++q)
+        if (ok[q]) {
+          w[f[q]] = v[q];
+          nn = fma(v[q], v[q], nn);
+        }
     }
   }
   if (!norm_part) return;
