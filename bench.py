@@ -3,21 +3,21 @@
 
 Workload (default): BASELINE.json configs[3] -- linear heat s=4096, N=127
 (128 windows), p=1024, 64 RHS, P_D with the parallel-in-time L_M(4) and R_hat = R,
-preconditioned MINRES.  configs[3] is the configuration
-BASELINE.json asks to be reported at 1/2/4/8 GPUs and the one whose covariance
-products are true FP64 contractions; other configs via --config.
+preconditioned MINRES; other configs via --config.
 
-One STEP = one batched MINRES iteration over all m RHS = one A apply + one P_D
-apply + the Krylov vector work.  value = steps/s
-summed over ranks = A+P applies/s of the whole job.  Each rank solves its own
-independent batch (distinct seeds): no data-path collective, scaling "weak".
+One STEP = one batched MINRES (GMRES for configs[4]) iteration over all m RHS = one
+A apply + one P apply + the Krylov vector work.
+value = A+P applies/s of the whole job: with N > 1 ranks (torchrun) the time
+windows of ONE batch are sharded over the ranks (NCCL halos + Krylov allreduce,
+scaling "strong", default --shard time) or every rank solves its own batch
+(--shard batch, scaling "weak").
 
-Timing: W warm-up steps, then exactly K steps inside ONE wf4dvar_solve call
-(tol below reach, so exactly K iterations; the solve's initialisation -- one
-extra P apply and two reductions -- is inside the timed region, which only
-makes the number pessimistic), bracketed by barrier + cuda synchronize, CUDA
-events on the library's stream, max over ranks.  Inputs are larger than L2
-(each Krylov vector is 604 MB at configs[3]).
+Timing: W warm-up steps, then exactly K steps inside ONE wf4dvar_solve call (tol
+below reach; the solve's initialisation -- one extra P apply -- is inside the timed
+region, which only makes the number pessimistic), bracketed by barrier + cuda
+synchronize, CUDA events on the library's stream, max over ranks.  Inputs are larger
+than L2 at configs[1..4] (each configs[3] vector is 604 MB).  The per-kernel-class
+roofline comes from a second, instrumented pass of the same K steps.
 """
 import argparse
 import json

@@ -176,12 +176,9 @@ struct LocalComm : Comm {
     if (ops.empty()) return;
     std::unique_lock<std::mutex> lk(g->mu);
     // 1. post every send (data ready once the stream reaches this point)
-    int nsend = 0;
     for (const P2P &o : ops)
-      if (o.send) {
+      if (o.send)
         g->mail[{rank, o.peer}].push_back({(const double *)o.buf, o.count, record_new(st)});
-        ++nsend;
-      }
     g->cv.notify_all();
     // 2. receive: wait for the matching post, copy after its ready event
     for (const P2P &o : ops) {
@@ -207,7 +204,6 @@ struct LocalComm : Comm {
       WF_CUDA(cudaStreamWaitEvent(st, e, 0));
       cudaEventDestroy(e);
     }
-    (void)nsend;
   }
 
   // post (ptr, ready) for generation gen and wait until all ranks posted

@@ -127,7 +127,7 @@ void lanczos(Ctx &c, int op, const double *v0, int steps, double *ritz_min, doub
          *z = c.kws_take<double>(n), *t1 = c.kws_take<double>(n), *t2 = c.kws_take<double>(n);
   double *S = c.kws_take<double>(16 * (size_t)m);
   double *dots_d = S, *inv = S + m, *gam = S + 2 * m, *alpha = S + 3 * m, *bprev = S + 4 * m,
-         *c1 = S + 5 * m, *c2 = S + 6 * m, *c3 = S + 7 * m, *zero = S + 8 * m;
+         *c1 = S + 5 * m, *c2 = S + 6 * m, *c3 = S + 7 * m;
   double *rec_a = c.kws_take<double>((size_t)steps * m);
   double *rec_b = c.kws_take<double>((size_t)steps * m);
   WF_CUDA(cudaMemsetAsync(S, 0, 16 * (size_t)m * 8, c.st));
@@ -193,7 +193,6 @@ void lanczos(Ctx &c, int op, const double *v0, int steps, double *ritz_min, doub
     WF_CUDA(cudaGetLastError());
     ++k_done;
   }
-  (void)zero;
   std::vector<double> ha((size_t)steps * m), hb((size_t)steps * m);
   WF_CUDA(memcpy_sync(c, ha.data(), rec_a, ha.size() * 8, cudaMemcpyDeviceToHost));
   WF_CUDA(memcpy_sync(c, hb.data(), rec_b, hb.size() * 8, cudaMemcpyDeviceToHost));
