@@ -37,7 +37,12 @@ CELLS = {
     2: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
     3: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
     4: dict(shape="PI", lhat="LM", k=4, rhat="exact", solver="gmres"),
+    # NEXT-1 workload with the paper's preconditioner choices: R_block by Algorithm 1,
+    # IC(0) factors of B_RR / Q_RR (ridge 0.01)
+    5: dict(shape="PD", lhat="LM", k=4, rhat="block", solver="minres", factor="ichol",
+            ridge=0.01, block_tol=0.05),
 }
+PC_KEYS = ("shape", "lhat", "k", "rhat", "factor", "ridge", "block_tol", "pvec")
 
 
 FP64_ALU_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12   # TFLOP/s, FP64 DFMA pipe at max SM clock
@@ -150,6 +155,11 @@ def cell_of(args):
     return cell
 
 
+def workload_name(config):
+    return (f"BASELINE.json configs[{config}]" if config <= 4 else
+            "NEXT-1 paper heat workload (SURVEY 8(f); not a BASELINE.json config)")
+
+
 def sample_problem(SC, config):
     """The oracle's bounded sample of a config: ONE RHS column and at most 16 of its
     windows (every window costs the same in the blockwise oracle, so per-apply time
@@ -164,7 +174,10 @@ def oracle_sample(prob, cell, reps=1):
     from oracle.saddle import Precond, Saddle
     from synth.layout import to_paper_order
     sad = Saddle(prob, col=0)
-    opc = Precond(shape=cell["shape"], lhat=cell["lhat"], k=cell["k"], rhat=cell["rhat"])
+    opc = Precond(shape=cell["shape"], lhat=cell["lhat"], k=cell["k"], rhat=cell["rhat"],
+                  ridge=cell.get("ridge", 0.0), factor=cell.get("factor", "chol"),
+                  block_tol=cell.get("block_tol", float("inf")),
+                  pvec=tuple(cell["pvec"]) if cell.get("pvec") else None)
     v = np.random.Generator(np.random.PCG64(7)).standard_normal((2 * prob.s + prob.p) * prob.W)
     sad.apply_Pinv(opc, v)          # factorisations (setup) outside the timed sample
     t0 = time.perf_counter()
@@ -189,6 +202,8 @@ def run_reference(args):
     from synth import configs as SC
     cell = cell_of(args)
     prob, wscale = sample_problem(SC, args.config)
+    if cell["rhat"] == "block" and "pvec" not in cell and "pvec" in prob.extra:
+        cell["pvec"] = prob.extra["pvec"]
     m_full = args.m or SC.CONFIGS[args.config]["m"]
     # bounded sample: one untimed warm-up apply (the oracle's factorisations), then as
     # many of the K steps as fit a ~150 s budget
@@ -205,7 +220,7 @@ def run_reference(args):
                 unit="A+P applies/s", n_gpus=args.gpus, steps=args.steps, warmup=args.warmup,
                 ms_per_step=t * m_full * 1e3, higher_is_better=True, scaling="weak",
                 vs_baseline=None, dtype="f64", data="synthetic",
-                config=dict(workload=f"BASELINE.json configs[{args.config}]", cell=cell,
+                config=dict(workload=workload_name(args.config), cell=cell,
                             s=prob.s, p=prob.p, N=SC.CONFIGS[args.config]["N"], m=m_full),
                 cpu_baseline=dict(value=val, unit="A+P applies/s", cores=cores, kind="oracle",
                                   sample=sample),
@@ -234,7 +249,9 @@ def main():
     time_shard = ws > 1 and args.shard == "time"
     prob = SC.make_problem(args.config, seed0=0 if time_shard else rank * m, m=m)
     stream = torch.cuda.Stream(device=dev)
-    pc = {k: cell[k] for k in ("shape", "lhat", "k", "rhat")}
+    if cell["rhat"] == "block" and "pvec" not in cell and "pvec" in prob.extra:
+        cell["pvec"] = prob.extra["pvec"]     # Algorithm 1 on the workload's block structure
+    pc = {k: cell[k] for k in PC_KEYS if k in cell}
     dkw = {}
     if time_shard:
         ids = [W.nccl_unique_id() if rank == 0 else None]
@@ -376,7 +393,7 @@ def main():
                 n_gpus=ws, steps=steps, warmup=args.warmup, ms_per_step=secs / steps * 1e3,
                 higher_is_better=True, scaling="strong" if time_shard else "weak", vs_baseline=None, dtype="f64",
                 data="synthetic",
-                config=dict(workload=f"BASELINE.json configs[{args.config}]",
+                config=dict(workload=workload_name(args.config),
                             desc=SC.CONFIGS[args.config]["desc"], cell=cell, s=prob.s, p=prob.p,
                             N=prob.N, m=m, step="one batched Krylov iteration (1 A + 1 P apply)",
                             l2="inputs larger than L2 (no flush needed)",

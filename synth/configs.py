@@ -39,6 +39,12 @@ CONFIGS = {
     4: dict(model="heat", s=2048, N=31, q=1, m=256, B=(0.02, 1.0), Q=(0.02, 0.1),
             R=(0.1, 0.01), heat_r=0.25,
             desc="BJ.c4 heat s=2048 N=31 p=2048, 256 RHS"),
+    # not a BASELINE.json config: the widened row NEXT-1 -- the paper's own
+    # heat workload (explicit Dirichlet model, 5-point smoothed H, compact-support
+    # modified SOAR, block-structured R_i) at a size that makes the GPU work visible
+    5: dict(model="heat_explicit", s=2048, N=31, m=32, nsteps=2,
+            desc="NEXT-1 paper heat s=2048 N=31 p=1024 (explicit Dirichlet, smoothed H, "
+                 "compact SOAR, block R), 32 RHS"),
 }
 
 
@@ -178,6 +184,9 @@ def make_problem(cfg, seed0=0, m=None, N=None, with_rhs=True):
     c = dict(CONFIGS[cfg])
     mm = c["m"] if m is None else m
     NN = c["N"] if N is None else N
+    if c["model"] == "heat_explicit":
+        return paper_heat_problem(s=c["s"], N=NN, m=mm, nsteps=c["nsteps"], seed0=seed0,
+                                  with_rhs=with_rhs)
     kw = {}
     if c["model"] == "l96":
         kw = dict(F=c["F"], dt=c["dt"], nsub=c["nsub"], spinup=c["spinup"])
