@@ -212,6 +212,76 @@ static void heat_explicit_launch(Ctx &c, bool transpose, double sign, const doub
   WF_CUDA(cudaGetLastError());
 }
 
+// Same recursions, the forward one streamed over register batches of 16 independent
+// loads (coalesced across the CTA's 128 columns) and its results kept in shared
+// memory only for the rows the backward pass reads (each thread owns one column:
+// no barriers) -- the register version exposed one global-load latency per step.
+template <int H, int TI>
+__global__ void __launch_bounds__(128) k_heat_iir_smem(double *out, const double *base,
+                                                       const double *in, const double *add2,
+                                                       const int *row_map, double rho,
+                                                       double gain, int s, int W, int m,
+                                                       int w_first, int w_step, int nw, int dir,
+                                                       const double *halo, int w0, int WG) {
+  constexpr int R = TI + 2 * H + 1;      // rows i0 - H .. i0 + TI + H
+  constexpr int RU = TI + H + 1;         // rows kept for the backward pass (i0 ..)
+  extern __shared__ double tile[];       // [RU][128]; thread t owns column t (no barrier)
+  const int64_t ld = (int64_t)W * m;
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.y * TI;
+  const int cc = blockIdx.x * 128 + tid;
+  if (cc >= nw * m) return;
+  const int tt = cc / m, r = cc - tt * m;
+  const int w = w_first + tt * w_step, ws = w + dir;
+  const bool has = (w0 + ws >= 0 && w0 + ws < WG);
+  const int64_t col = (int64_t)w * m + r;
+  double *tc = tile + tid;
+  double v = 0.0;
+  if (has) {
+    // forward recursion streamed over the input rows, 16 loads in flight per thread;
+    // u is kept (in shared memory) only for the rows the backward pass needs
+    const double *src = (ws < 0 || ws >= W) ? halo + r : in + (int64_t)ws * m + r;
+    const int64_t sld = (ws < 0 || ws >= W) ? (int64_t)m : ld;
+    int row0 = (i0 - H) % s;
+    row0 = row0 < 0 ? row0 + s : row0;
+    double u = 0.0;
+    for (int j = 0; j < R; j += 16) {
+      double x[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        int row = row0 + j + q;
+        row = row >= s ? row - s : row;
+        row = row >= s ? row % s : row;
+        x[q] = (j + q < R) ? __ldg(src + (int64_t)row * sld) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (j + q < R) {
+          u = fma(rho, u, x[q]);
+          if (j + q >= H) tc[(j + q - H) * 128] = u;
+        }
+      }
+    }
+    // backward: v_i = u_i + rho v_{i+1} from the last kept row; outputs rows i0..i0+TI-1
+#pragma unroll 8
+    for (int j = RU - 1; j >= TI; --j) v = fma(rho, v, tc[j * 128]);
+  }
+#pragma unroll 4
+  for (int j = TI - 1; j >= 0; --j) {
+    if (has) v = fma(rho, v, tc[j * 128]);
+    const int i = i0 + j;
+    if (i < s) {
+      double val = base[(int64_t)i * ld + col];
+      if (has) val = fma(gain, v, val);
+      if (add2) {
+        int jj = row_map[i];
+        if (jj >= 0) val += add2[(int64_t)jj * ld + col];
+      }
+      out[(int64_t)i * ld + col] = val;
+    }
+  }
+}
+
 // z_w += z_{w-1} (forward, w ascending) or z_w += z_{w+1} (backward): L_I^{-1} / L_I^{-T}
 __global__ void k_window_scan(double *z, int rows, int W, int m, int dir) {
   const int64_t ld = (int64_t)W * m;
@@ -241,13 +311,35 @@ template <int H>
 static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *in,
                             const double *base, double *out, int w_first, int w_step, int nw,
                             const double *add2, const int *row_map) {
-  constexpr int TI = 32;
   int cols = nw * c.m;
-  dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
-  k_heat_iir<H, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_rho,
-                                            sign * c.heat_gain, c.s, c.W, c.m, w_first, w_step,
-                                            nw, transpose ? 1 : -1,
-                                            transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+  static int smem_env = -1;
+  if (smem_env < 0) {
+    const char *e = getenv("WF4DVAR_HEAT_IIR_SMEM");   // tuning experiments only
+    smem_env = e ? atoi(e) : 1;
+  }
+  if (smem_env) {
+    constexpr int TI = 32;
+    constexpr size_t smem = (size_t)(TI + H + 1) * 128 * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      WF_CUDA(cudaFuncSetAttribute(k_heat_iir_smem<H, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr = true;
+    }
+    dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
+    k_heat_iir_smem<H, TI><<<grid, 128, smem, c.st>>>(out, base, in, add2, row_map, c.heat_rho,
+                                                      sign * c.heat_gain, c.s, c.W, c.m, w_first,
+                                                      w_step, nw, transpose ? 1 : -1,
+                                                      transpose ? c.halo_hi : c.halo_lo, c.w0,
+                                                      c.WG);
+  } else {
+    constexpr int TI = 32;
+    dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
+    k_heat_iir<H, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_rho,
+                                              sign * c.heat_gain, c.s, c.W, c.m, w_first, w_step,
+                                              nw, transpose ? 1 : -1,
+                                              transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+  }
   WF_CUDA(cudaGetLastError());
 }
 
