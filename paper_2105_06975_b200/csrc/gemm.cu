@@ -260,11 +260,7 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   // panels and (2*148/gm) X column panels; pick the gm minimising that L2 footprint
   // (~sqrt(2*148*BN/BM)), capped at the M-tiles of the problem
   {
-    static int gm_env = -2;
-    if (gm_env == -2) {
-      const char *e = getenv("WF4DVAR_GEMM_GM");   // tuning experiments only
-      gm_env = e ? atoi(e) : -1;
-    }
+    static const int gm_env = env_int("WF4DVAR_GEMM_GM", -1);   // tuning experiments only
     int best = 1;
     double best_fp = 1e300;
     for (int g = 1; g <= 64; g *= 2) {
@@ -275,13 +271,7 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   }
   size_t smem = C::SMEM_DOUBLES * sizeof(double);
   // stream-K hybrid when one batch of large tiles quantises badly onto the waves
-  static int sk_env = -2;
-  if (sk_env == -2) {
-    const char *e = getenv("WF4DVAR_GEMM_SK");   // 0 disables (tuning experiments)
-    // measured r01f: no gain at configs[3] (38.7 -> 40.8 ms per step; the partial
-    // last wave runs one CTA per SM and finishes early anyway) -> opt-in only
-    sk_env = e ? atoi(e) : 0;
-  }
+  static const int sk_env = env_int("WF4DVAR_GEMM_SK", 0);   // 0 disables (tuning experiments)
   const int G = 2 * 148;   // resident CTAs of the 64x128 / 81 KB configuration
   const int nk = (probs[0].K + C::BK - 1) / C::BK;
   bool same_k = nprob == 1 || probs[0].K == probs[1].K;
@@ -309,11 +299,8 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     S.flags = c.sk_flags;
     S.epoch = ++c.sk_epoch;
     if (S.epoch == 0) S.epoch = ++c.sk_epoch;
-    static bool attr = false;
-    if (!attr) {
-      WF_CUDA(cudaFuncSetAttribute(k_gemm_sk<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(k_gemm_sk<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    WF_CUDA(attr);
     k_gemm_sk<C, true><<<G, C::NT, smem, c.st>>>(L, S);
     WF_CUDA(cudaGetLastError());
     return;
@@ -321,18 +308,12 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   }
   dim3 grid(tiles, 1, batch);
   if (v16) {
-    static bool attr = false;
-    if (!attr) {
-      WF_CUDA(cudaFuncSetAttribute(k_gemm<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(k_gemm<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    WF_CUDA(attr);
     k_gemm<C, true><<<grid, C::NT, smem, c.st>>>(L);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      WF_CUDA(cudaFuncSetAttribute(k_gemm<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr = true;
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(k_gemm<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    WF_CUDA(attr);
     k_gemm<C, false><<<grid, C::NT, smem, c.st>>>(L);
   }
   WF_CUDA(cudaGetLastError());
@@ -357,11 +338,7 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
   }
   if (flops_hint >= 0) flops = flops_hint;
   LaunchScope ls(c, c.gemm_cls, flops, bytes);
-  static int force = -2;
-  if (force == -2) {
-    const char *e = getenv("WF4DVAR_GEMM_CFG");   // tuning experiments only
-    force = e ? atoi(e) : -1;
-  }
+  static const int force = env_int("WF4DVAR_GEMM_CFG", -1);   // tuning experiments only
   if (force >= 0 && huge_tiles * batch >= 2 * 148) {
     if (force == 1) run<CfgWide>(c, ps, valid, batch, v16);
     else if (force == 3) run<TileCfg<64, 128, 16, 32, 64, 3>>(c, ps, valid, batch, v16);

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 #include <vector>
@@ -10,6 +11,12 @@
 #include "../../include/wf4dvar.h"
 
 namespace wf {
+
+// integer tuning knob from the environment (read once by the callers' static locals)
+inline int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 
 // ---------------------------------------------------------------- errors
 struct Error {

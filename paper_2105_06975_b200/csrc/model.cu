@@ -312,20 +312,13 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
                             const double *base, double *out, int w_first, int w_step, int nw,
                             const double *add2, const int *row_map) {
   int cols = nw * c.m;
-  static int smem_env = -1;
-  if (smem_env < 0) {
-    const char *e = getenv("WF4DVAR_HEAT_IIR_SMEM");   // tuning experiments only
-    smem_env = e ? atoi(e) : 1;
-  }
+  static const int smem_env = env_int("WF4DVAR_HEAT_IIR_SMEM", 1);   // tuning experiments only
   if (smem_env) {
     constexpr int TI = 32;
     constexpr size_t smem = (size_t)(TI + H + 1) * 128 * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      WF_CUDA(cudaFuncSetAttribute(k_heat_iir_smem<H, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      attr = true;
-    }
+    static const cudaError_t attr = cudaFuncSetAttribute(k_heat_iir_smem<H, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem);
+    WF_CUDA(attr);
     dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
     k_heat_iir_smem<H, TI><<<grid, 128, smem, c.st>>>(out, base, in, add2, row_map, c.heat_rho,
                                                       sign * c.heat_gain, c.s, c.W, c.m, w_first,

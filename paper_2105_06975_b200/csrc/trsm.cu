@@ -209,11 +209,12 @@ static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   using C = TrsmCfg<NB>;
   size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + TB * (TB + 1) + TB) * sizeof(double);
   auto kern = v16 ? k_trsm<NB, UPPER, true> : k_trsm<NB, UPPER, false>;
-  static bool attr[2] = {false, false};
-  if (!attr[v16]) {
-    WF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr[v16] = true;
-  }
+  // one-time (thread-safe static initialisation) opt-in to the large dynamic smem
+  static const cudaError_t attr_v =
+      cudaFuncSetAttribute(k_trsm<NB, UPPER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static const cudaError_t attr_n =
+      cudaFuncSetAttribute(k_trsm<NB, UPPER, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  WF_CUDA(v16 ? attr_v : attr_n);
   kern<<<dim3(panels, nseg), 128, smem, c.st>>>(L);
   WF_CUDA(cudaGetLastError());
 }
@@ -336,23 +337,15 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     trsm_segments(c, probs, np, upper, 0, blk, n);
     return;
   }
-  static int leaf_env = -1;
-  if (leaf_env < 0) {
-    const char *e = getenv("WF4DVAR_TRSM_LEAF");   // tuning experiments only (0 = blocked)
-    // measured r01c (kbench, bench c3): the recursive split does not beat the
-    // super-block scheme at n = 4096 (small-K couplings run at < 24 TFLOP/s), so
-    // the default stays blocked; WF4DVAR_TRSM_LEAF=512 selects the recursion
-    leaf_env = e ? atoi(e) : 0;
-  }
+  // measured r01c/r01l (kbench, bench c3): the recursive split is within 1% of the
+  // super-block scheme at n = 4096, so the default stays blocked; WF4DVAR_TRSM_LEAF=512
+  // selects the recursion
+  static const int leaf_env = env_int("WF4DVAR_TRSM_LEAF", 0);   // tuning experiments only (0 = blocked)
   if (leaf_env > 0 && n > leaf_env) {
     trsm_rec(c, probs, np, upper, 0, n, leaf_env, true);
     return;
   }
-  static int sb_env = -1;
-  if (sb_env < 0) {
-    const char *e = getenv("WF4DVAR_TRSM_SB");   // tuning experiments only
-    sb_env = e ? atoi(e) : 0;
-  }
+  static const int sb_env = env_int("WF4DVAR_TRSM_SB", 0);   // tuning experiments only
   // measured (tools/kbench.py, r01): at n = 4096 SB = 512 gives 19.1 TFLOP/s vs 16.2
   // (256) and 12.3 (128) -- the coupling GEMMs need K >= 512 to run efficiently
   // (1024 at n = 4096: 20.6 TFLOP/s, above cuBLAS DTRSM's 18.8 on the same shape)
@@ -363,11 +356,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     return;
   }
   const int nsb = (n + SB - 1) / SB;
-  static int left_env = -1;
-  if (left_env < 0) {
-    const char *e = getenv("WF4DVAR_TRSM_LEFT");   // tuning experiments only
-    left_env = e ? atoi(e) : 0;
-  }
+  static const int left_env = env_int("WF4DVAR_TRSM_LEFT", 0);   // tuning experiments only
   if (left_env) {
     // left-looking: before solving super-block b, ONE GEMM brings in every solved
     // block (K = all rows solved so far), then the panel kernel solves b in place
