@@ -260,6 +260,8 @@ static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int
   if ((total_cols + 63) / 64 * ctas_per_col < 148) NB = 32;
   if ((total_cols + 31) / 32 * ctas_per_col < 148) NB = 16;
   if ((total_cols + 15) / 16 * ctas_per_col < 148) NB = 8;
+  static const int nb_env = env_int("WF4DVAR_TRSM_NB", 0);   // tuning experiments only
+  if (nb_env == 8 || nb_env == 16 || nb_env == 32 || nb_env == 64) NB = nb_env;
   int panels = 0;
   for (int i = 0; i < np; ++i) {
     int pi = (L.p[i].ncols + NB - 1) / NB;
