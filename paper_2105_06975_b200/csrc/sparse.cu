@@ -49,6 +49,53 @@ __global__ void k_sptrsv(double *y, const double *x, const int *rowptr, const in
   }
 }
 
+// Same solves with LPC lanes per column: the lanes split the row's non-zeros and
+// reduce by shuffles, and the last RB solution values of the column live in a
+// shared-memory ring (entries farther back -- the wrap-around corners of a periodic
+// band -- are read from global memory).  r01t: the one-thread-per-column version,
+// reading the solution back through L2 one latency per non-zero, ran the configs-5
+// IC(0) solves at ~1 GB/s.
+template <int LPC, int RB>
+__global__ void __launch_bounds__(128) k_sptrsv_ring(double *y, const double *x, const int *rowptr,
+                                                     const int *col, const double *val,
+                                                     const double *dinv, int n, int64_t ld,
+                                                     int c0, int ncols, int upper) {
+  constexpr int CPB = 128 / LPC;                 // columns per block
+  __shared__ double ring[RB][CPB];
+  const int lc = threadIdx.x / LPC, q = threadIdx.x % LPC;
+  const int cc = blockIdx.x * CPB + lc;
+  const bool live = cc < ncols;
+  const int64_t c = c0 + (live ? cc : 0);
+  for (int t = 0; t < n; ++t) {
+    const int i = upper ? n - 1 - t : t;
+    const int k0 = rowptr[i], k1 = rowptr[i + 1];
+    double a0 = 0.0, a1 = 0.0;
+    int k = k0 + q;
+    for (; k + LPC < k1; k += 2 * LPC) {
+      const int j0 = __ldg(col + k), j1 = __ldg(col + k + LPC);
+      const int d0 = upper ? j0 - i : i - j0, d1 = upper ? j1 - i : i - j1;
+      const double y0 = d0 <= RB ? ring[j0 % RB][lc] : y[(int64_t)j0 * ld + c];
+      const double y1 = d1 <= RB ? ring[j1 % RB][lc] : y[(int64_t)j1 * ld + c];
+      a0 = fma(__ldg(val + k), y0, a0);
+      a1 = fma(__ldg(val + k + LPC), y1, a1);
+    }
+    if (k < k1) {
+      const int j0 = __ldg(col + k);
+      const int d0 = upper ? j0 - i : i - j0;
+      a0 = fma(__ldg(val + k), d0 <= RB ? ring[j0 % RB][lc] : y[(int64_t)j0 * ld + c], a0);
+    }
+    double acc = a0 + a1;
+#pragma unroll
+    for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, LPC);
+    const double yi = (live ? x[(int64_t)i * ld + c] - acc : 0.0) * __ldg(dinv + i);
+    if (q == 0) {
+      ring[i % RB][lc] = yi;
+      if (live) y[(int64_t)i * ld + c] = yi;
+    }
+    __syncwarp();
+  }
+}
+
 // IC(0) of the row-major n x n host matrix A (exact zeros outside the pattern).
 static void ichol0_host(const std::vector<double> &A, int n, const char *name,
                         std::vector<int> &lrp, std::vector<int> &lci, std::vector<double> &lv,
@@ -135,9 +182,19 @@ void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int 
   const double cols = ncols;
   LaunchScope ls(c, K_TRSM, 2.0 * 2.0 * f.nnz * cols + 2.0 * f.n * cols,
                  8.0 * (2.0 * f.nnz + 4.0 * f.n * cols));
-  const unsigned g = (unsigned)((ncols + 127) / 128);
-  k_sptrsv<<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0, ncols, 0);
-  k_sptrsv<<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol, c0, ncols, 1);
+  static const int ring_env = env_int("WF4DVAR_SPTRSV_RING", 1);   // tuning experiments only
+  if (ring_env) {
+    constexpr int LPC = 8, RB = 256, CPB = 128 / LPC;
+    const unsigned g = (unsigned)((ncols + CPB - 1) / CPB);
+    k_sptrsv_ring<LPC, RB><<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0,
+                                                ncols, 0);
+    k_sptrsv_ring<LPC, RB><<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol, c0,
+                                                ncols, 1);
+  } else {
+    const unsigned g = (unsigned)((ncols + 127) / 128);
+    k_sptrsv<<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0, ncols, 0);
+    k_sptrsv<<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol, c0, ncols, 1);
+  }
   WF_CUDA(cudaGetLastError());
   c.launches += 2;
 }
