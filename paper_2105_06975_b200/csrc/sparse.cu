@@ -55,7 +55,7 @@ __global__ void k_sptrsv(double *y, const double *x, const int *rowptr, const in
 // band -- are read from global memory).  r01t: the one-thread-per-column version,
 // reading the solution back through L2 one latency per non-zero, ran the configs-5
 // IC(0) solves at ~1 GB/s.
-template <int LPC, int RB>
+template <int LPC, int RB, int E>
 __global__ void __launch_bounds__(128) k_sptrsv_ring(double *y, const double *x, const int *rowptr,
                                                      const int *col, const double *val,
                                                      const double *dinv, int n, int64_t ld,
@@ -66,28 +66,56 @@ __global__ void __launch_bounds__(128) k_sptrsv_ring(double *y, const double *x,
   const int cc = blockIdx.x * CPB + lc;
   const bool live = cc < ncols;
   const int64_t c = c0 + (live ? cc : 0);
+  // software pipeline: the next row's factor entries (up to E per lane, i.e. LPC*E per
+  // row -- longer rows take a slow tail loop) and right-hand side are loaded while the
+  // current row is reduced, so each row costs one shared-memory round instead of a
+  // chain of L2 latencies
+  int jn[E];
+  double vn[E], xn = 0.0, dn = 0.0;
+  int kn0 = 0, kn1 = 0;
+  auto fetch = [&](int i) {
+    kn0 = __ldg(rowptr + i);
+    kn1 = __ldg(rowptr + i + 1);
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int k = kn0 + q + e * LPC;
+      jn[e] = k < kn1 ? __ldg(col + k) : -1;
+      vn[e] = k < kn1 ? __ldg(val + k) : 0.0;
+    }
+    xn = live ? x[(int64_t)i * ld + c] : 0.0;
+    dn = __ldg(dinv + i);
+  };
+  fetch(upper ? n - 1 : 0);
   for (int t = 0; t < n; ++t) {
     const int i = upper ? n - 1 - t : t;
-    const int k0 = rowptr[i], k1 = rowptr[i + 1];
+    int jj[E];
+    double vv[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) { jj[e] = jn[e]; vv[e] = vn[e]; }
+    const double xi = xn, di = dn;
+    const int k0 = kn0, k1 = kn1;
+    if (t + 1 < n) fetch(upper ? i - 1 : i + 1);
     double a0 = 0.0, a1 = 0.0;
-    int k = k0 + q;
-    for (; k + LPC < k1; k += 2 * LPC) {
-      const int j0 = __ldg(col + k), j1 = __ldg(col + k + LPC);
-      const int d0 = upper ? j0 - i : i - j0, d1 = upper ? j1 - i : i - j1;
-      const double y0 = d0 <= RB ? ring[j0 % RB][lc] : y[(int64_t)j0 * ld + c];
-      const double y1 = d1 <= RB ? ring[j1 % RB][lc] : y[(int64_t)j1 * ld + c];
-      a0 = fma(__ldg(val + k), y0, a0);
-      a1 = fma(__ldg(val + k + LPC), y1, a1);
+#pragma unroll
+    for (int e = 0; e < E; e += 2) {
+      if (jj[e] >= 0) {
+        const int d = upper ? jj[e] - i : i - jj[e];
+        a0 = fma(vv[e], d <= RB ? ring[jj[e] % RB][lc] : y[(int64_t)jj[e] * ld + c], a0);
+      }
+      if (e + 1 < E && jj[e + 1] >= 0) {
+        const int d = upper ? jj[e + 1] - i : i - jj[e + 1];
+        a1 = fma(vv[e + 1], d <= RB ? ring[jj[e + 1] % RB][lc] : y[(int64_t)jj[e + 1] * ld + c], a1);
+      }
     }
-    if (k < k1) {
-      const int j0 = __ldg(col + k);
-      const int d0 = upper ? j0 - i : i - j0;
-      a0 = fma(__ldg(val + k), d0 <= RB ? ring[j0 % RB][lc] : y[(int64_t)j0 * ld + c], a0);
+    for (int k = k0 + q + E * LPC; k < k1; k += LPC) {   // rows longer than LPC * E
+      const int j = __ldg(col + k);
+      const int d = upper ? j - i : i - j;
+      a0 = fma(__ldg(val + k), d <= RB ? ring[j % RB][lc] : y[(int64_t)j * ld + c], a0);
     }
     double acc = a0 + a1;
 #pragma unroll
     for (int o = LPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, LPC);
-    const double yi = (live ? x[(int64_t)i * ld + c] - acc : 0.0) * __ldg(dinv + i);
+    const double yi = (xi - acc) * di;
     if (q == 0) {
       ring[i % RB][lc] = yi;
       if (live) y[(int64_t)i * ld + c] = yi;
@@ -184,12 +212,12 @@ void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int 
                  8.0 * (2.0 * f.nnz + 4.0 * f.n * cols));
   static const int ring_env = env_int("WF4DVAR_SPTRSV_RING", 1);   // tuning experiments only
   if (ring_env) {
-    constexpr int LPC = 8, RB = 256, CPB = 128 / LPC;
+    constexpr int LPC = 8, RB = 256, E = 16, CPB = 128 / LPC;
     const unsigned g = (unsigned)((ncols + CPB - 1) / CPB);
-    k_sptrsv_ring<LPC, RB><<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0,
-                                                ncols, 0);
-    k_sptrsv_ring<LPC, RB><<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol, c0,
-                                                ncols, 1);
+    k_sptrsv_ring<LPC, RB, E><<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol,
+                                                   c0, ncols, 0);
+    k_sptrsv_ring<LPC, RB, E><<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol,
+                                                   c0, ncols, 1);
   } else {
     const unsigned g = (unsigned)((ncols + 127) / 128);
     k_sptrsv<<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0, ncols, 0);
