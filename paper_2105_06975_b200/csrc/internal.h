@@ -370,7 +370,8 @@ void dots(Ctx &c, int nd, const double *const *a, const double *const *b, int64_
 
 void setup_precond(Ctx &c);
 void make_ichol(Ctx &c, const std::vector<double> &A, int n, const char *name, SparseFactor &f);
-void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int c0, int ncols);
+void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int c0, int ncols,
+                 const SparseFactor *g = nullptr, int nsplit = 0);
 std::vector<int> algorithm1_blocks(const std::vector<double> &R, int p, const std::vector<int> &pvec,
                                    double tol, int maxsize, int numproc);
 void free_precond(Ctx &c);

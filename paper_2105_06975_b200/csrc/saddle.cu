@@ -50,8 +50,7 @@ void dhat_inv(Ctx &c, const double *x1, double *y1) {
   const int64_t ld = c.ncol;
   if (c.pc.factor == WF4DVAR_FACTOR_ICHOL) {   // (L L^T)^{-1} with the IC(0) factors
     if (c.w0 == 0) {
-      ichol_solve(c, c.icB, x1, y1, 0, m);
-      ichol_solve(c, c.icQ, x1, y1, m, (int)ld - m);
+      ichol_solve(c, c.icB, x1, y1, 0, (int)ld, &c.icQ, m);   // B on window 0, Q after
     } else {
       ichol_solve(c, c.icQ, x1, y1, 0, (int)ld);
     }

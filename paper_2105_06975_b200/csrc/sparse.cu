@@ -55,10 +55,14 @@ __global__ void k_sptrsv(double *y, const double *x, const int *rowptr, const in
 // band -- are read from global memory).  r01t: the one-thread-per-column version,
 // reading the solution back through L2 one latency per non-zero, ran the configs-5
 // IC(0) solves at ~1 GB/s.
+struct SpTri { const int *rowptr, *col; const double *val, *dinv; };
+
+// columns [c0, c0 + nsplit) use factor f0, [c0 + nsplit, c0 + ncols) factor f1 (B on
+// window 0 and Q on the other windows in ONE launch: the serial row recurrence is the
+// cost, so two launches would double it)
 template <int LPC, int RB, int E>
-__global__ void __launch_bounds__(128) k_sptrsv_ring(double *y, const double *x, const int *rowptr,
-                                                     const int *col, const double *val,
-                                                     const double *dinv, int n, int64_t ld,
+__global__ void __launch_bounds__(128) k_sptrsv_ring(double *y, const double *x, SpTri f0,
+                                                     SpTri f1, int nsplit, int n, int64_t ld,
                                                      int c0, int ncols, int upper) {
   constexpr int CPB = 128 / LPC;                 // columns per block
   __shared__ double ring[RB][CPB];
@@ -66,6 +70,9 @@ __global__ void __launch_bounds__(128) k_sptrsv_ring(double *y, const double *x,
   const int cc = blockIdx.x * CPB + lc;
   const bool live = cc < ncols;
   const int64_t c = c0 + (live ? cc : 0);
+  const SpTri &F = cc < nsplit ? f0 : f1;
+  const int *rowptr = F.rowptr, *col = F.col;
+  const double *val = F.val, *dinv = F.dinv;
   // software pipeline: the next row's factor entries (up to E per lane, i.e. LPC*E per
   // row -- longer rows take a slow tail loop) and right-hand side are loaded while the
   // current row is reduced, so each row costs one shared-memory round instead of a
@@ -204,24 +211,34 @@ void make_ichol(Ctx &c, const std::vector<double> &A, int n, const char *name, S
   WF_CUDA(memcpy_sync(c, f.dinv, dinv.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
 }
 
-// y[:, c0:c0+ncols] = (L L^T)^{-1} x[:, c0:c0+ncols] over an [n][ncol] segment
-void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int c0, int ncols) {
+// y[:, c0:c0+ncols] = (L L^T)^{-1} x[:, c0:c0+ncols] over an [n][ncol] segment; with g
+// given, columns from c0 + nsplit on use the factor g (same n) in the same launches
+void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int c0, int ncols,
+                 const SparseFactor *g, int nsplit) {
   if (ncols <= 0) return;
+  if (!g) { g = &f; nsplit = ncols; }
   const double cols = ncols;
   LaunchScope ls(c, K_TRSM, 2.0 * 2.0 * f.nnz * cols + 2.0 * f.n * cols,
                  8.0 * (2.0 * f.nnz + 4.0 * f.n * cols));
   static const int ring_env = env_int("WF4DVAR_SPTRSV_RING", 1);   // tuning experiments only
   if (ring_env) {
     constexpr int LPC = 8, RB = 256, E = 16, CPB = 128 / LPC;
-    const unsigned g = (unsigned)((ncols + CPB - 1) / CPB);
-    k_sptrsv_ring<LPC, RB, E><<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol,
-                                                   c0, ncols, 0);
-    k_sptrsv_ring<LPC, RB, E><<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol,
-                                                   c0, ncols, 1);
+    const unsigned gb = (unsigned)((ncols + CPB - 1) / CPB);
+    const SpTri fl{f.lrp, f.lci, f.lv, f.dinv}, fu{f.urp, f.uci, f.uv, f.dinv};
+    const SpTri gl{g->lrp, g->lci, g->lv, g->dinv}, gu{g->urp, g->uci, g->uv, g->dinv};
+    k_sptrsv_ring<LPC, RB, E><<<gb, 128, 0, c.st>>>(y, x, fl, gl, nsplit, f.n, c.ncol, c0, ncols,
+                                                    0);
+    k_sptrsv_ring<LPC, RB, E><<<gb, 128, 0, c.st>>>(y, y, fu, gu, nsplit, f.n, c.ncol, c0, ncols,
+                                                    1);
   } else {
-    const unsigned g = (unsigned)((ncols + 127) / 128);
-    k_sptrsv<<<g, 128, 0, c.st>>>(y, x, f.lrp, f.lci, f.lv, f.dinv, f.n, c.ncol, c0, ncols, 0);
-    k_sptrsv<<<g, 128, 0, c.st>>>(y, y, f.urp, f.uci, f.uv, f.dinv, f.n, c.ncol, c0, ncols, 1);
+    for (int part = 0; part < 2; ++part) {
+      const SparseFactor &h = part ? *g : f;
+      const int a = part ? c0 + nsplit : c0, nc = part ? ncols - nsplit : nsplit;
+      if (nc <= 0) continue;
+      const unsigned gb = (unsigned)((nc + 127) / 128);
+      k_sptrsv<<<gb, 128, 0, c.st>>>(y, x, h.lrp, h.lci, h.lv, h.dinv, h.n, c.ncol, a, nc, 0);
+      k_sptrsv<<<gb, 128, 0, c.st>>>(y, y, h.urp, h.uci, h.uv, h.dinv, h.n, c.ncol, a, nc, 1);
+    }
   }
   WF_CUDA(cudaGetLastError());
   c.launches += 2;
