@@ -198,6 +198,8 @@ typedef struct {
   int64_t n_apply_A, n_apply_P;
   int64_t n_R, n_Rhat_inv, n_D, n_Dhat_inv, n_M; /* per-window constituent products,
                           counted as in Tables 7.2-7.3, S5-S7 (R_diag not counted)  */
+  double seconds_init;   /* part of `seconds` spent before the first iteration (MINRES:
+                            x = 0, r = b, z_1 = P^{-1} b and the first inner products) */
 } wf4dvar_report;
 
 wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond *pc,

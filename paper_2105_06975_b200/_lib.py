@@ -72,7 +72,7 @@ class Report(C.Structure):
                 ("history", _dp), ("seconds", C.c_double), ("seconds_to_mark", C.c_double),
                 ("iters_to_mark", C.c_int32), ("n_apply_A", C.c_int64), ("n_apply_P", C.c_int64),
                 ("n_R", C.c_int64), ("n_Rhat_inv", C.c_int64), ("n_D", C.c_int64),
-                ("n_Dhat_inv", C.c_int64), ("n_M", C.c_int64)]
+                ("n_Dhat_inv", C.c_int64), ("n_M", C.c_int64), ("seconds_init", C.c_double)]
 
 
 class KStat(C.Structure):
@@ -385,7 +385,7 @@ class Context:
                    seconds=rep.seconds, seconds_to_mark=rep.seconds_to_mark,
                    iters_to_mark=rep.iters_to_mark, n_apply_A=rep.n_apply_A,
                    n_apply_P=rep.n_apply_P, n_R=rep.n_R, n_Rhat_inv=rep.n_Rhat_inv, n_D=rep.n_D,
-                   n_Dhat_inv=rep.n_Dhat_inv, n_M=rep.n_M)
+                   n_Dhat_inv=rep.n_Dhat_inv, n_M=rep.n_M, seconds_init=rep.seconds_init)
         if hist is not None:
             out["history"] = hist.reshape(maxit + 1, self.m)
         return out

@@ -244,6 +244,7 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   if (c.hpin) cudaFreeHost(c.hpin);
   if (c.kws) cudaFree(c.kws);
   for (auto e : c.iter_events) cudaEventDestroy(e);
+  if (c.ev_init) cudaEventDestroy(c.ev_init);
   delete ctx;
   return WF4DVAR_OK;
 }

@@ -248,6 +248,7 @@ struct Ctx {
   }
   int *hpin = nullptr;   // pinned host flags
   std::vector<cudaEvent_t> iter_events;
+  cudaEvent_t ev_init = nullptr;  // end of the solver initialisation (report.seconds_init)
   cudaEvent_t iter_event(size_t i) {
     while (iter_events.size() <= i) {
       cudaEvent_t e;

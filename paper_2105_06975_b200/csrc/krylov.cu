@@ -213,6 +213,8 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   }
   k_minres_init<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
   c.launches++;
+  if (!c.ev_init) WF_CUDA(cudaEventCreate(&c.ev_init));
+  WF_CUDA(cudaEventRecord(c.ev_init, c.st));
   int h[4];
   int j = 0;
   bool indef = false;
@@ -302,6 +304,8 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
     rep->seconds = ms * 1e-3;
     rep->iters_to_mark = h[2];
     rep->seconds_to_mark = -1;
+    cudaEventElapsedTime(&ms, e0, c.ev_init);
+    rep->seconds_init = ms * 1e-3;
     if (h[2] >= 0) {
       cudaEventElapsedTime(&ms, e0, c.iter_event(h[2]));
       rep->seconds_to_mark = ms * 1e-3;
