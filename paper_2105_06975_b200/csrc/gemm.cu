@@ -219,6 +219,98 @@ __global__ void __launch_bounds__(C::NT) k_gemm_sk(const GemmLaunch L, const SkA
   }
 }
 
+// ------------------------------------------------------------------ TMA-engine staging
+// The same 64x128 / 4-warp DMMA tile, with the operand tiles staged by the TMA copy
+// engine (cp.async.bulk, 1-D row copies into the padded, conflict-free shared layout)
+// and an mbarrier ring instead of per-thread cp.async + __syncthreads: warp 0's lanes
+// arm a stage's "full" barrier with its byte count and issue the row copies; every
+// warp waits on "full", runs its DMMAs and arrives on the stage's "empty" barrier;
+// warp 0 refills a stage once all four warps have released it.  No thread computes
+// per-element addresses or bounds in the main loop.
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred P;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+      "@!P bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+               "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT) k_gemm_bulk(const GemmLaunch L) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
+  int tile = blockIdx.x, gi, m0, n0;
+  tile_coords<C>(L, tile, gi, m0, n0);
+  const GemmProb &P = L.p[gi];
+  const int b = blockIdx.z;
+  const double *A = P.A + (int64_t)b * P.sA;
+  const double *X = P.X + (int64_t)b * P.sX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int nk = P.K / C::BK;                       // K % BK == 0 (host checks)
+  const int rowsA = min(C::BM, P.M - m0);
+  const int colsB = min(C::BN, P.N - n0);           // even (host checks)
+  const unsigned bytes = (unsigned)(rowsA * C::BK * 8 + C::BK * colsB * 8);
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int kt) {   // warp 0: arm + copy the rows of k-tile kt into stage kt % S
+    const int s = kt % C::STAGES;
+    double *sA = smem + s * C::STAGE, *sB = sA + C::A_STAGE;
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], bytes);
+    __syncwarp();
+    const int k0 = kt * C::BK;
+    for (int r = lane; r < rowsA; r += 32)
+      bulk_g2s(sA + r * C::LDA, A + (int64_t)(m0 + r) * P.lda + k0, C::BK * 8, &full[s]);
+    for (int r = lane; r < C::BK; r += 32)
+      bulk_g2s(sB + r * C::LDB, X + (int64_t)(k0 + r) * P.ldx + n0, (unsigned)colsB * 8, &full[s]);
+  };
+  if (warp == 0)
+    for (int kt = 0; kt < C::STAGES - 1 && kt < nk; ++kt) issue(kt);
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    // refill: k-tile kt + S - 1 goes into the stage every warp released at kt - 1
+    if (warp == 0 && kt + C::STAGES - 1 < nk) {
+      const int kn = kt + C::STAGES - 1;
+      if (kn >= C::STAGES) mbar_wait(&empty[kn % C::STAGES], ((kn / C::STAGES) - 1) & 1);
+      issue(kn);
+    }
+    const int s = kt % C::STAGES;
+    mbar_wait(&full[s], (kt / C::STAGES) & 1);
+    const double *st = smem + s * C::STAGE;
+    mma_stage<C>(st, st + C::A_STAGE, acc, wm, wn, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  GemmProb Pb = P;
+  Pb.Y = P.Y + (int64_t)b * P.sY;
+  Pb.Z = P.Z ? P.Z + (int64_t)b * P.sZ : nullptr;
+  tile_epilogue<C>(Pb, m0, n0, acc);
+}
+
 // Large problems: 64x128 CTA tile, 4 warps of 32x64 (32 independent DMMA
 // accumulator tiles per warp per k-step), BK = 16, 3-stage cp.async ring,
 // 81 KB smem -> 2 CTAs (8 warps) per SM.  Chosen by measurement (tools/kbench.py,
@@ -305,6 +397,21 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     WF_CUDA(cudaGetLastError());
     return;
   }
+  }
+  if constexpr (C::BM == 64 && C::BN == 128 && C::BK == 16 && C::STAGES == 3) {
+    static const int bulk_env = env_int("WF4DVAR_GEMM_BULK", 1);   // tuning experiments only
+    bool ok = bulk_env && v16;
+    for (int i = 0; i < nprob; ++i)
+      ok = ok && probs[i].K % C::BK == 0 && probs[i].N % 2 == 0 && probs[i].K > 0 &&
+           ((uintptr_t)probs[i].A % 16 == 0) && ((uintptr_t)probs[i].X % 16 == 0);
+    if (ok) {
+      static const cudaError_t attr =
+          cudaFuncSetAttribute(k_gemm_bulk<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      WF_CUDA(attr);
+      k_gemm_bulk<C><<<dim3(tiles, 1, batch), C::NT, smem, c.st>>>(L);
+      WF_CUDA(cudaGetLastError());
+      return;
+    }
   }
   dim3 grid(tiles, 1, batch);
   if (v16) {
