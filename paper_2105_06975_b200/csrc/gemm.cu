@@ -399,7 +399,10 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   }
   }
   if constexpr (C::BM == 64 && C::BN == 128 && C::BK == 16 && C::STAGES == 3) {
-    static const int bulk_env = env_int("WF4DVAR_GEMM_BULK", 1);   // tuning experiments only
+    // measured r01x: 20.0 vs 32.5 TFLOP/s at 4096x8128x4096 -- 80 small (128 B / 1 KB)
+    // bulk copies per stage through the copy engine cost more than the per-thread
+    // cp.async issue they replace -> opt-in only (WF4DVAR_GEMM_BULK=1)
+    static const int bulk_env = env_int("WF4DVAR_GEMM_BULK", 0);   // tuning experiments only
     bool ok = bulk_env && v16;
     for (int i = 0; i < nprob; ++i)
       ok = ok && probs[i].K % C::BK == 0 && probs[i].N % 2 == 0 && probs[i].K > 0 &&
