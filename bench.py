@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--m", type=int, default=None, help="override the RHS batch width")
+    ap.add_argument("--N", type=int, default=None,
+                    help="override N (experiments: a G-way time shard of configs[3] is N+1 = 128/G)")
     ap.add_argument("--shape", default=None)
     ap.add_argument("--lhat", default=None)
     ap.add_argument("--k", type=int, default=None)
@@ -247,7 +249,7 @@ def main():
     cfgm = SC.CONFIGS[args.config]["m"]
     m = args.m or cfgm
     time_shard = ws > 1 and args.shard == "time"
-    prob = SC.make_problem(args.config, seed0=0 if time_shard else rank * m, m=m)
+    prob = SC.make_problem(args.config, seed0=0 if time_shard else rank * m, m=m, N=args.N)
     stream = torch.cuda.Stream(device=dev)
     if cell["rhat"] == "block" and "pvec" not in cell and "pvec" in prob.extra:
         cell["pvec"] = prob.extra["pvec"]     # Algorithm 1 on the workload's block structure
