@@ -351,8 +351,13 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   // measured (tools/kbench.py, r01): at n = 4096 SB = 512 gives 19.1 TFLOP/s vs 16.2
   // (256) and 12.3 (128) -- the coupling GEMMs need K >= 512 to run efficiently
   // (1024 at n = 4096: 20.6 TFLOP/s, above cuBLAS DTRSM's 18.8 on the same shape)
+  // narrow right-hand sides (a time shard of configs[3] on 8 ranks: 1024 columns) gain
+  // from shorter panel chains: r01z measured SB = 512 4.5% faster per step there
+  int total_cols = 0;
+  for (int i = 0; i < np; ++i) total_cols += probs[i].ncols;
   const int SB = sb_env > 0 ? sb_env
-                            : (n >= 4096 ? 1024 : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
+                            : (n >= 4096 ? (total_cols <= 1536 ? 512 : 1024)
+                                         : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
   if (n <= SB) {
     trsm_segments(c, probs, np, upper, 0, n, n);
     return;
