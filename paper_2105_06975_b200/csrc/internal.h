@@ -96,6 +96,9 @@ struct SparseFactor {
   int n = 0, nnz = 0;
   int *lrp = nullptr, *lci = nullptr, *urp = nullptr, *uci = nullptr;
   double *lv = nullptr, *uv = nullptr, *dinv = nullptr;
+  // the same factor densified (row-major lower / upper, diagonal-tile packs) for the
+  // DMMA TRSM: at n <= 4096 a dense solve of the banded factor beats the sparse one
+  double *Gd = nullptr, *Gdt = nullptr, *Pd = nullptr, *Pdt = nullptr;
 };
 
 // ---------------------------------------------------------------- transport (comm.cu)

@@ -310,6 +310,7 @@ void free_precond(Ctx &c) {
     int *ip[4] = {f->lrp, f->lci, f->urp, f->uci};
     for (int *q : ip) if (q) { auto it = std::find(c.allocs.begin(), c.allocs.end(), (void *)q); if (it != c.allocs.end()) c.allocs.erase(it); cudaFree(q); }
     dev_free(c, f->lv); dev_free(c, f->uv); dev_free(c, f->dinv);
+    dev_free(c, f->Gd); dev_free(c, f->Gdt); dev_free(c, f->Pd); dev_free(c, f->Pdt);
     *f = SparseFactor{};
   }
   dev_free(c, c.U_me); dev_free(c, c.Kinv_me); dev_free(c, c.ws_lr);

@@ -209,6 +209,24 @@ void make_ichol(Ctx &c, const std::vector<double> &A, int n, const char *name, S
     WF_CUDA(memcpy_sync(c, f.uv, uv.data(), (size_t)nnz * 8, cudaMemcpyHostToDevice));
   }
   WF_CUDA(memcpy_sync(c, f.dinv, dinv.data(), (size_t)n * 8, cudaMemcpyHostToDevice));
+  static const int dense_env = env_int("WF4DVAR_ICHOL_DENSE_MAX", 4096);   // tuning knob
+  if (n <= dense_env) {
+    // densified L and L^T for the DMMA TRSM path (the values are the IC(0) factor's)
+    std::vector<double> Ld((size_t)n * n, 0.0), Ud((size_t)n * n, 0.0);
+    for (int i = 0; i < n; ++i) {
+      Ld[(size_t)i * n + i] = Ud[(size_t)i * n + i] = diag[i];
+      for (int k = lrp[i]; k < lrp[i + 1]; ++k) {
+        Ld[(size_t)i * n + lci[k]] = lv[k];
+        Ud[(size_t)lci[k] * n + i] = lv[k];
+      }
+    }
+    f.Gd = c.alloc<double>((size_t)n * n);
+    f.Gdt = c.alloc<double>((size_t)n * n);
+    WF_CUDA(memcpy_sync(c, f.Gd, Ld.data(), Ld.size() * 8, cudaMemcpyHostToDevice));
+    WF_CUDA(memcpy_sync(c, f.Gdt, Ud.data(), Ud.size() * 8, cudaMemcpyHostToDevice));
+    f.Pd = make_diag_pack(c, f.Gd, n, false);
+    f.Pdt = make_diag_pack(c, f.Gdt, n, true);
+  }
 }
 
 // y[:, c0:c0+ncols] = (L L^T)^{-1} x[:, c0:c0+ncols] over an [n][ncol] segment; with g
@@ -217,6 +235,25 @@ void ichol_solve(Ctx &c, const SparseFactor &f, const double *x, double *y, int 
                  const SparseFactor *g, int nsplit) {
   if (ncols <= 0) return;
   if (!g) { g = &f; nsplit = ncols; }
+  if (f.Gd && g->Gd) {
+    // dense DMMA TRSM pair on the densified factors (B / Q groups in one launch each)
+    const int64_t ld = c.ncol;
+    TrsmProb fw[2], bw[2];
+    int np = 0;
+    const SparseFactor *fs[2] = {&f, g};
+    const int cs[2] = {c0, c0 + nsplit}, nc[2] = {nsplit, ncols - nsplit};
+    for (int p = 0; p < 2; ++p) {
+      if (nc[p] <= 0) continue;
+      fw[np] = TrsmProb{fs[p]->Gd, fs[p]->n, x + cs[p], ld, y + cs[p], ld, fs[p]->n, nc[p], 0};
+      bw[np] = TrsmProb{fs[p]->Gdt, fs[p]->n, y + cs[p], ld, y + cs[p], ld, fs[p]->n, nc[p], 0};
+      fw[np].dpack = fs[p]->Pd;
+      bw[np].dpack = fs[p]->Pdt;
+      ++np;
+    }
+    launch_trsm(c, fw, np, false);
+    launch_trsm(c, bw, np, true);
+    return;
+  }
   const double cols = ncols;
   LaunchScope ls(c, K_TRSM, 2.0 * 2.0 * f.nnz * cols + 2.0 * f.n * cols,
                  8.0 * (2.0 * f.nnz + 4.0 * f.n * cols));

@@ -75,3 +75,31 @@ def test_solve_ichol(solver, pc):
         xo, info = fn(sad.apply_A, lambda v: sad.apply_Pinv(opc, v), B[c], **kw)
         assert rep["converged"][c] and info["converged"]
         assert np.linalg.norm(X[c] - xo) / np.linalg.norm(xo) <= 1e-9
+
+
+def test_sparse_triangular_solve_path():
+    """The factors are densified for the DMMA TRSM at n <= 4096 (default); the sparse
+    triangular-solve kernels serve larger n.  Run the parity check of CELLS[0]/[2] with
+    the sparse path forced (separate process: the knob is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "import paper_2105_06975_b200 as W\n"
+        "from tests.test_gpu_ichol import problem, CELLS\n"
+        "from tests.helpers import OracleCols, rel_err_cols, seeded_vec\n"
+        "prob = problem(); ora = OracleCols(prob); x = seeded_vec(prob.n, 8)\n"
+        "worst = 0.0\n"
+        "for pc in (CELLS[0], CELLS[2]):\n"
+        "    ctx = W.Context.from_problem(prob, pc)\n"
+        "    y = torch.empty(prob.n, dtype=torch.float64, device='cuda')\n"
+        "    ctx.apply_P(torch.from_numpy(x).cuda(), y); torch.cuda.synchronize()\n"
+        "    worst = max(worst, max(rel_err_cols(y.cpu().numpy(), ora.apply_P(pc, x), prob).values()))\n"
+        "print('WORST', worst)\n"
+        "assert worst <= 1e-10, worst\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WF4DVAR_ICHOL_DENSE_MAX="0")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
