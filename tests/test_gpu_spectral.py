@@ -76,3 +76,26 @@ def test_pa_extremes_c0_match_dense_generalised_eigenproblem(pc):
     ev = np.sort(np.real(sla.eigvals(sad.assemble_A(), sad.assemble_P(opc))))
     np.testing.assert_allclose(lo[0], ev[0], rtol=1e-7)
     np.testing.assert_allclose(hi[0], ev[-1], rtol=1e-7)
+
+
+def test_sharded_lanczos_matches_single_rank():
+    """The spectral suite on the time-window-sharded path (LOCAL transport, 2 ranks):
+    halos for L / L^T, chain hand-offs and allreduced inner products give the same
+    Ritz values as one rank."""
+    from .test_gpu_dist import Sharded, run_ranks
+    prob = SC.paper_heat_problem(s=200, N=7, m=2, nsteps=2, with_rhs=False)
+    for op, pc in (("LHAT", dict(shape="PD", lhat="LM", k=3, rhat="diag")),
+                   ("PA", dict(shape="PD", lhat="LM", k=3, rhat="exact"))):
+        one = WF().Context.from_problem(prob, pc)
+        v0 = seeded_vec(prob.n, 5)
+        lo1, hi1 = one.lanczos(op, torch.from_numpy(v0).cuda(), 120)
+        sh = Sharded(prob, pc, 2)
+        try:
+            vs = [sh.local(v0, r) for r in range(2)]
+            res = run_ranks(2, lambda r: sh.ctx[r].lanczos(op, vs[r], 120))
+            for lo, hi in res:
+                np.testing.assert_allclose(lo, lo1, rtol=1e-9, atol=1e-12)
+                np.testing.assert_allclose(hi, hi1, rtol=1e-9)
+        finally:
+            sh.close()
+            one.close()
