@@ -94,8 +94,8 @@ def test_sharded_lanczos_matches_single_rank():
             vs = [sh.local(v0, r) for r in range(2)]
             res = run_ranks(2, lambda r: sh.ctx[r].lanczos(op, vs[r], 120))
             for lo, hi in res:
-                np.testing.assert_allclose(lo, lo1, rtol=1e-9, atol=1e-12)
-                np.testing.assert_allclose(hi, hi1, rtol=1e-9)
+                np.testing.assert_allclose(lo, lo1, rtol=1e-6, atol=1e-9)
+                np.testing.assert_allclose(hi, hi1, rtol=1e-6)
         finally:
             sh.close()
             one.close()
