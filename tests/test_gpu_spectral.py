@@ -81,21 +81,24 @@ def test_pa_extremes_c0_match_dense_generalised_eigenproblem(pc):
 def test_sharded_lanczos_matches_single_rank():
     """The spectral suite on the time-window-sharded path (LOCAL transport, 2 ranks):
     halos for L / L^T, chain hand-offs and allreduced inner products give the same
-    Ritz values as one rank."""
+    Ritz values as one rank.  30 steps: without reorthogonalisation the unconverged
+    end of the spectrum amplifies the rounding-order difference of the sharded
+    reductions (r01ab: 5e-5 relative at the bottom after 120 steps), while the
+    first steps agree to rounding."""
     from .test_gpu_dist import Sharded, run_ranks
     prob = SC.paper_heat_problem(s=200, N=7, m=2, nsteps=2, with_rhs=False)
     for op, pc in (("LHAT", dict(shape="PD", lhat="LM", k=3, rhat="diag")),
                    ("PA", dict(shape="PD", lhat="LM", k=3, rhat="exact"))):
         one = WF().Context.from_problem(prob, pc)
         v0 = seeded_vec(prob.n, 5)
-        lo1, hi1 = one.lanczos(op, torch.from_numpy(v0).cuda(), 120)
+        lo1, hi1 = one.lanczos(op, torch.from_numpy(v0).cuda(), 30)
         sh = Sharded(prob, pc, 2)
         try:
             vs = [sh.local(v0, r) for r in range(2)]
-            res = run_ranks(2, lambda r: sh.ctx[r].lanczos(op, vs[r], 120))
+            res = run_ranks(2, lambda r: sh.ctx[r].lanczos(op, vs[r], 30))
             for lo, hi in res:
-                np.testing.assert_allclose(lo, lo1, rtol=1e-6, atol=1e-9)
-                np.testing.assert_allclose(hi, hi1, rtol=1e-6)
+                np.testing.assert_allclose(lo, lo1, rtol=1e-9)
+                np.testing.assert_allclose(hi, hi1, rtol=1e-9)
         finally:
             sh.close()
             one.close()
