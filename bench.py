@@ -366,9 +366,12 @@ def main():
                     peak_source="MEASURED_PEAKS.json hbm_gbs")
     roof.update(kernel=dom, launches=d["launches"],
                 flops_per_launch=d["flops"] / max(d["launches"], 1),
+                bytes_per_launch=d["bytes"] / max(d["launches"], 1),
                 share_of_step=d["ms"] / tot_ms if tot_ms else None, traffic=None,
-                how="algorithmic flops (2MNK per GEMM) / CUDA-event time of the class's "
-                    "launches in a profiled pass of the same K steps")
+                how=("algorithmic bytes" if roof["bound"] == "hbm" else
+                     "algorithmic flops (2MNK per GEMM, 2 per FMA otherwise)") +
+                    " / CUDA-event time of the class's launches in a profiled pass of the "
+                    "same K steps")
     traffic_file = os.path.join(ROOT, "profiles", f"ncu_traffic_c{args.config}.json")
     if os.path.exists(traffic_file):
         tr = json.load(open(traffic_file)).get(dom)

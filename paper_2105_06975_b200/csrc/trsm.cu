@@ -219,6 +219,85 @@ static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   WF_CUDA(cudaGetLastError());
 }
 
+// Small triangles: every segment (diagonal block) has <= 64 rows -- R_hat / D_hat of the
+// L96 configs (s = 40, 50; p = 20, 25) and the R_block blocks.  The 64-row panel kernel
+// above spends such a solve in the shuffle chain of a mostly empty tile; here one
+// thread owns one right-hand-side column in registers (coalesced row loads across the
+// warp) and runs the right-looking substitution
+//     y_i = t_i / G_ii,   t_k -= G_ki y_i   (k after i),
+// whose updates are independent FMAs, against the segment's factor held TRANSPOSED in
+// shared memory (sGt[i][k] = G[k][i], broadcast 16-byte pair loads; masked to the
+// strict triangle, identity padding past the segment so padded rows stay 0).
+template <int NMAX, bool UPPER>
+__global__ void __launch_bounds__(128) k_trsm_small(const TrsmLaunch L) {
+  constexpr int LD = NMAX + 2;
+  __shared__ __align__(16) double sGt[NMAX * LD];
+  __shared__ double sD[NMAX];
+  int chunk = blockIdx.x, gi = 0;
+  if (chunk >= L.panels0) { chunk -= L.panels0; gi = 1; }
+  const TrsmProb &P = L.p[gi];
+  const int slo = L.ntab ? L.tab[blockIdx.y] : L.seg_lo + blockIdx.y * L.seg_len;
+  const int shi = L.ntab ? L.tab[blockIdx.y + 1] : min(L.seg_hi, slo + L.seg_len);
+  const int len = shi - slo;
+  if (len <= 0) return;
+  for (int e = threadIdx.x; e < NMAX * NMAX; e += 128) {
+    const int i = e / NMAX, k = e % NMAX;
+    const bool keep = (UPPER ? (k < i) : (k > i)) && i < len && k < len;
+    sGt[i * LD + k] = keep ? P.G[(int64_t)(slo + k) * P.ldg + slo + i] : 0.0;
+  }
+  for (int e = threadIdx.x; e < NMAX; e += 128)
+    sD[e] = e < len ? 1.0 / P.G[(int64_t)(slo + e) * P.ldg + slo + e] : 1.0;
+  __syncthreads();
+  const int col = chunk * 128 + threadIdx.x;
+  if (col >= P.ncols) return;
+  double y[NMAX];
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) y[i] = i < len ? P.X[(int64_t)(slo + i) * P.ldx + col] : 0.0;
+  if (!UPPER) {
+#pragma unroll
+    for (int i = 0; i < NMAX; ++i) {
+      y[i] *= sD[i];
+      // pairs from the even index at or below i + 1 (sGt[i][i] = 0 keeps y_i unchanged)
+#pragma unroll
+      for (int k = (i + 1) & ~1; k < NMAX; k += 2) {
+        const double2 gg = *reinterpret_cast<const double2 *>(&sGt[i * LD + k]);
+        y[k] = fma(-gg.x, y[i], y[k]);
+        y[k + 1] = fma(-gg.y, y[i], y[k + 1]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = NMAX - 1; i >= 0; --i) {
+      y[i] *= sD[i];
+#pragma unroll
+      for (int k = 0; k < i; k += 2) {
+        const double2 gg = *reinterpret_cast<const double2 *>(&sGt[i * LD + k]);
+        y[k] = fma(-gg.x, y[i], y[k]);
+        y[k + 1] = fma(-gg.y, y[i], y[k + 1]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i)
+    if (i < len) P.Y[(int64_t)(slo + i) * P.ldy + col] = y[i];
+}
+
+template <bool UPPER>
+static void run_small(Ctx &c, const TrsmLaunch &L, int chunks, int nseg, int maxlen) {
+  const dim3 grid(chunks, nseg);
+  switch ((maxlen + 7) / 8) {
+    case 1: k_trsm_small<8, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    case 2: k_trsm_small<16, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    case 3: k_trsm_small<24, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    case 4: k_trsm_small<32, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    case 5: k_trsm_small<40, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    case 6: k_trsm_small<48, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    case 7: k_trsm_small<56, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+    default: k_trsm_small<64, UPPER><<<grid, 128, 0, c.st>>>(L); break;
+  }
+  WF_CUDA(cudaGetLastError());
+}
+
 // one k_trsm launch over segments [seg_lo + j*seg_len ...) of every problem
 static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int seg_lo,
                           int seg_len, int seg_hi, const std::vector<int> *tab = nullptr) {
@@ -254,6 +333,25 @@ static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int
   }
   L.seg_lo = seg_lo; L.seg_len = seg_len; L.seg_hi = seg_hi;
   if (tab) { L.seg_lo = 0; L.seg_len = 1; }
+  // every segment <= 64 rows: the thread-per-column kernel
+  static const int small_env = env_int("WF4DVAR_TRSM_SMALL", 1);   // 0: panel kernel always
+  int maxlen = tab ? 0 : std::min(seg_len, seg_hi - seg_lo);
+  if (tab)
+    for (int j = 0; j < nseg; ++j) maxlen = std::max(maxlen, (*tab)[j + 1] - (*tab)[j]);
+  if (small_env && maxlen <= 64) {
+    int chunks = 0;
+    for (int i = 0; i < np; ++i) {
+      const int ci = (L.p[i].ncols + 127) / 128;
+      if (i == 0) L.panels0 = ci;
+      chunks += ci;
+    }
+    if (np == 1) L.panels0 = chunks;
+    LaunchScope ls(c, K_TRSM, flops, bytes);
+    upper ? run_small<true>(c, L, chunks, nseg, maxlen)
+          : run_small<false>(c, L, chunks, nseg, maxlen);
+    c.launches++;
+    return;
+  }
   // panel width: as wide as possible while still filling the SMs
   const int ctas_per_col = nseg;
   int NB = 64;

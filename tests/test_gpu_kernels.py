@@ -14,7 +14,9 @@ def L():
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (37, 19, 5), (128, 128, 32), (300, 517, 129),
-                                   (1000, 336, 1000), (64, 8128, 512)])
+                                   (1000, 336, 1000), (64, 8128, 512),
+                                   # streaming kernel (M, K <= 64)
+                                   (40, 5000, 40), (64, 1000, 64), (63, 333, 17)])
 @pytest.mark.parametrize("with_z", [False, True])
 def test_gemm_vs_float64_reference(M, N, K, with_z):
     g = torch.Generator().manual_seed(M * 7 + N + K)
@@ -61,7 +63,10 @@ def test_gemm_strided_views_and_odd_ld():
 
 @pytest.mark.parametrize("n,ncols,blk", [(5, 3, 0), (64, 64, 0), (130, 17, 0), (600, 40, 0),
                                          (1000, 336, 0), (2048, 96, 0), (500, 21, 50),
-                                         (256, 64, 64)])
+                                         (256, 64, 64),
+                                         # thread-per-column kernel (segments <= 64 rows)
+                                         (40, 5000, 0), (50, 333, 0), (200, 700, 7),
+                                         (17, 129, 0), (300, 260, 64)])
 @pytest.mark.parametrize("upper", [False, True])
 def test_trsm_vs_float64_reference(n, ncols, blk, upper):
     g = torch.Generator().manual_seed(n + ncols + blk)
