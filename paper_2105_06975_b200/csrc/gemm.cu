@@ -432,55 +432,59 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
 // Small operators (M, K <= 64: the s x s and p x p covariances of the L96 configs,
 // s = 40, 50).  A 64x128 DMMA tile with K <= 64 never fills its cp.async ring and
 // wastes most of its M rows; the product is HBM bound, so this kernel is the
-// streaming form: one thread per column keeps x[0:K] in registers and writes the M
-// outputs, A resident in shared memory (broadcast 16-byte pairs, two rows and two
-// partial sums per row in flight).
+// streaming form: one thread per (column, group of GR rows) streams x[0:K] of its
+// column and accumulates its GR outputs (two partial sums each), the GR x K block of
+// A resident in shared memory (broadcast 16-byte pairs).  The row groups of one
+// column read x from L2 after the first; they exist for memory-level parallelism
+// (ncu r01ad: one thread per column = 11 warps per SM, 0.5 TB/s).
+constexpr int kSmallGR = 8;
 template <int KMAX>
 __global__ void __launch_bounds__(128) k_gemm_small(const GemmLaunch L) {
   constexpr int LD = KMAX + 2;
-  __shared__ __align__(16) double sA[64 * LD];
+  __shared__ __align__(16) double sA[kSmallGR * LD];
   int chunk = blockIdx.x, gi = 0;
   if (chunk >= L.tiles0) { chunk -= L.tiles0; gi = 1; }
   const GemmProb &P = L.p[gi];
+  const int r0 = blockIdx.y * kSmallGR;
+  if (r0 >= P.M) return;
   const int b = blockIdx.z;
   const double *A = P.A + (int64_t)b * P.sA;
   const double *X = P.X + (int64_t)b * P.sX;
   double *Y = P.Y + (int64_t)b * P.sY;
   const double *Z = P.Z ? P.Z + (int64_t)b * P.sZ : nullptr;
-  for (int e = threadIdx.x; e < 64 * KMAX; e += 128) {
+  for (int e = threadIdx.x; e < kSmallGR * KMAX; e += 128) {
     const int r = e / KMAX, k = e % KMAX;
-    sA[r * LD + k] = (r < P.M && k < P.K) ? A[(int64_t)r * P.lda + k] : 0.0;
+    sA[r * LD + k] = (r0 + r < P.M && k < P.K) ? A[(int64_t)(r0 + r) * P.lda + k] : 0.0;
   }
   __syncthreads();
   const int col = chunk * 128 + threadIdx.x;
   if (col >= P.N) return;
-  double x[KMAX];
+  double acc0[kSmallGR], acc1[kSmallGR];
 #pragma unroll
-  for (int k = 0; k < KMAX; ++k) x[k] = k < P.K ? X[(int64_t)k * P.ldx + col] : 0.0;
-#pragma unroll 1
-  for (int r = 0; r < P.M; r += 2) {
-    double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+  for (int r = 0; r < kSmallGR; ++r) acc0[r] = acc1[r] = 0.0;
 #pragma unroll
-    for (int k = 0; k < KMAX; k += 2) {
-      const double2 g0 = *reinterpret_cast<const double2 *>(&sA[r * LD + k]);
-      const double2 g1 = *reinterpret_cast<const double2 *>(&sA[(r + 1) * LD + k]);
-      a0 = fma(g0.x, x[k], a0);
-      a1 = fma(g0.y, x[k + 1], a1);
-      b0 = fma(g1.x, x[k], b0);
-      b1 = fma(g1.y, x[k + 1], b1);
+  for (int k = 0; k < KMAX; k += 2) {
+    const double x0 = k < P.K ? X[(int64_t)k * P.ldx + col] : 0.0;
+    const double x1 = k + 1 < P.K ? X[(int64_t)(k + 1) * P.ldx + col] : 0.0;
+#pragma unroll
+    for (int r = 0; r < kSmallGR; ++r) {
+      const double2 g = *reinterpret_cast<const double2 *>(&sA[r * LD + k]);
+      acc0[r] = fma(g.x, x0, acc0[r]);
+      acc1[r] = fma(g.y, x1, acc1[r]);
     }
+  }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = r + h;
-      if (row >= P.M) break;
-      double v = P.alpha * (h ? b0 + b1 : a0 + a1);
+  for (int r = 0; r < kSmallGR; ++r) {
+    const int row = r0 + r;
+    if (row < P.M) {
+      double v = P.alpha * (acc0[r] + acc1[r]);
       if (Z) v += P.beta * Z[(int64_t)(P.zrow ? P.zrow[row] : row) * P.ldz + col];
       Y[(int64_t)row * P.ldy + col] = v;
     }
   }
 }
 
-static void run_small(Ctx &c, const GemmProb *probs, int nprob, int batch, int kmax) {
+static void run_small(Ctx &c, const GemmProb *probs, int nprob, int batch, int mmax, int kmax) {
   GemmLaunch L{};
   int chunks = 0;
   for (int i = 0; i < nprob; ++i) {
@@ -490,7 +494,7 @@ static void run_small(Ctx &c, const GemmProb *probs, int nprob, int batch, int k
     chunks += ci;
   }
   if (nprob == 1) L.tiles0 = chunks;
-  const dim3 grid(chunks, 1, batch);
+  const dim3 grid(chunks, (mmax + kSmallGR - 1) / kSmallGR, batch);
   switch ((kmax + 7) / 8) {
     case 1: k_gemm_small<8><<<grid, 128, 0, c.st>>>(L); break;
     case 2: k_gemm_small<16><<<grid, 128, 0, c.st>>>(L); break;
@@ -530,7 +534,7 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
     kmax = std::max(kmax, ps[i].K);
   }
   if (small_env && mmax <= 64 && kmax <= 64 && kmax > 0) {
-    run_small(c, ps, valid, batch, kmax);
+    run_small(c, ps, valid, batch, mmax, kmax);
     c.launches++;
     return;
   }

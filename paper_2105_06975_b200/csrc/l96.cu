@@ -170,10 +170,16 @@ __device__ __forceinline__ void rk4_stages(const double (&x)[IPT], double (&x2)[
   for (int k = 0; k < IPT; ++k) xn[k] = x[k] + (h / 6.0) * (k1[k] + 2.0 * k2[k] + 2.0 * k3[k] + k4[k]);
 }
 
-template <int IPT, int NSUB_MAX, bool SH>
-__global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
-  __shared__ double bx[L96Thread<IPT>::S_MAX * 32];
-  __shared__ double bu[L96Thread<IPT>::S_MAX * 32];
+// ADJ: the adjoint keeps the substep start states in (dynamic) shared memory,
+// [NSUB_MAX * IPT][256] -- in registers they pushed the kernel to 184 registers, one
+// 256-thread CTA per SM (ncu r01ad: 12% warps active, FP64 pipe 28-35%); forward and
+// adjoint are separate instantiations so each gets its own register allocation, and
+// the IPT = 5 (s <= 40) variants are held to 2 CTAs per SM (IPT = 8 would spill).
+template <int IPT, int NSUB_MAX, bool SH, bool ADJ>
+__global__ void __launch_bounds__(256, IPT <= 5 ? 2 : 1) k_l96_step(const L96Args a) {
+  extern __shared__ double xs_sm[];
+  __shared__ double bx[SH ? 1 : L96Thread<IPT>::S_MAX * 32];
+  __shared__ double bu[SH ? 1 : L96Thread<IPT>::S_MAX * 32];
   // 4 problems per warp, 8 lanes per problem (lane = 8 p + ty): the periodic
   // neighbour exchange stays inside the warp (warp-private shared memory, __syncwarp
   // instead of __syncthreads; layout [i][4] -> every access is 32 consecutive doubles)
@@ -205,7 +211,7 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
                                           : a.in[i * ld + (int64_t)ws * a.m + r])
                              : 0.0;
     }
-    if (a.dir < 0) {
+    if constexpr (!ADJ) {
       // forward tangent: nsub RK4 steps
       for (int st = 0; st < a.nsub; ++st) {
         double x2[IPT], x3[IPT], x4[IPT], xn[IPT], d1[IPT], d2[IPT], d3[IPT], d4[IPT], u[IPT];
@@ -228,13 +234,13 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
       }
     } else {
       // adjoint: store the substep start states, then sweep the substeps backwards
-      double xs[NSUB_MAX][IPT];
+      // xs(st, k) = xs_sm[(st IPT + k) 256 + tid]: consecutive threads, consecutive words
 #pragma unroll
       for (int st = 0; st < NSUB_MAX; ++st) {
         if (st < a.nsub) {
           double x2[IPT], x3[IPT], x4[IPT], xn[IPT];
 #pragma unroll
-          for (int k = 0; k < IPT; ++k) xs[st][k] = x[k];
+          for (int k = 0; k < IPT; ++k) xs_sm[(st * IPT + k) * 256 + tid] = x[k];
           if (st + 1 < a.nsub) {
             rk4_stages<IPT, SH>(x, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
 #pragma unroll
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
         if (st < a.nsub) {
           double x1[IPT], x2[IPT], x3[IPT], x4[IPT], xn[IPT], lu[IPT], ld1[IPT], ld2[IPT], ld3[IPT];
 #pragma unroll
-          for (int k = 0; k < IPT; ++k) x1[k] = xs[st][k];
+          for (int k = 0; k < IPT; ++k) x1[k] = xs_sm[(st * IPT + k) * 256 + tid];
           rk4_stages<IPT, SH>(x1, x2, x3, x4, xn, bxw, s, ty, lane, a.F, h);
           // lambda_d4 = h/6 l ; lambda_u4 = J4^T lambda_d4
           double lv[IPT], tmp[IPT];
@@ -286,6 +292,26 @@ __global__ void __launch_bounds__(256) k_l96_step(const L96Args a) {
   }
 }
 
+template <int IPT, int NSUB_MAX, bool SH>
+static void launch_step_n(Ctx &c, const L96Args &a, dim3 grid, bool transpose) {
+  const dim3 block(32, 8);
+  if (!transpose) {
+    k_l96_step<IPT, NSUB_MAX, SH, false><<<grid, block, 0, c.st>>>(a);
+    return;
+  }
+  const int smem = NSUB_MAX * IPT * 256 * (int)sizeof(double);
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      k_l96_step<IPT, NSUB_MAX, SH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  WF_CUDA(attr);
+  k_l96_step<IPT, NSUB_MAX, SH, true><<<grid, block, smem, c.st>>>(a);
+}
+
+template <int IPT, bool SH>
+static void launch_step(Ctx &c, const L96Args &a, dim3 grid, bool transpose, bool small_sub) {
+  if (small_sub) launch_step_n<IPT, 5, SH>(c, a, grid, transpose);
+  else launch_step_n<IPT, 8, SH>(c, a, grid, transpose);
+}
+
 void l96_step(Ctx &c, bool transpose, double sign, const double *in, const double *base, double *out,
               int w_first, int w_step, int nw, const double *add2, const int *row_map) {
   L96Args a{};
@@ -294,7 +320,7 @@ void l96_step(Ctx &c, bool transpose, double sign, const double *in, const doubl
   a.w0 = c.w0; a.WG = c.WG; a.halo = transpose ? c.halo_hi : c.halo_lo;
   a.nsub = c.l96_nsub; a.w_first = w_first; a.w_step = w_step; a.nw = nw;
   a.dir = transpose ? 1 : -1;
-  dim3 grid((c.m + 31) / 32, nw), block(32, 8);
+  dim3 grid((c.m + 31) / 32, nw);
   // flops per state element and RK4 substep, counted from the kernel's arithmetic:
   //   nonlinear stages: 4 tendencies x 4 + stage states 3 x 2 + update 7      = 29
   //   tangent:  4 Jacobian products x 6 + stage tangents 3 x 2 + update 7      = 37
@@ -305,10 +331,11 @@ void l96_step(Ctx &c, bool transpose, double sign, const double *in, const doubl
   double flops = (double)nw * c.m * c.s * per;
   LaunchScope ls(c, K_MODEL, flops, (double)nw * c.m * c.s * 8 * 4);
   // contiguous ownership with shuffled neighbours when s == 8 IPT (c2: s = 40)
-  if (c.s == 40) k_l96_step<5, 8, true><<<grid, block, 0, c.st>>>(a);
-  else if (c.s == 64) k_l96_step<8, 8, true><<<grid, block, 0, c.st>>>(a);
-  else if (c.s <= 40) k_l96_step<5, 8, false><<<grid, block, 0, c.st>>>(a);
-  else k_l96_step<8, 8, false><<<grid, block, 0, c.st>>>(a);
+  const bool small_sub = c.l96_nsub <= 5;
+  if (c.s == 40) launch_step<5, true>(c, a, grid, transpose, small_sub);
+  else if (c.s == 64) launch_step<8, true>(c, a, grid, transpose, small_sub);
+  else if (c.s <= 40) launch_step<5, false>(c, a, grid, transpose, small_sub);
+  else launch_step<8, false>(c, a, grid, transpose, small_sub);
   WF_CUDA(cudaGetLastError());
   c.launches++;
 }
