@@ -153,6 +153,10 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     WF_CUDA(memcpy_sync(c, c.B, p.B, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
     WF_CUDA(memcpy_sync(c, c.Q, p.Q, (size_t)c.s * c.s * 8, cudaMemcpyHostToDevice));
     WF_CUDA(memcpy_sync(c, c.R, p.R, (size_t)c.p * c.p * 8, cudaMemcpyHostToDevice));
+    // compact-support covariances: column ranges of their non-zero tiles
+    register_tile_ranges(c, c.B, c.s, c.s, c.s);
+    register_tile_ranges(c, c.Q, c.s, c.s, c.s);
+    register_tile_ranges(c, c.R, c.p, c.p, c.p);
     if (p.H_rowptr) {
       // general H_i: CSR and its transpose (built here, host side)
       c.H_general = true;

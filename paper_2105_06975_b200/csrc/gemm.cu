@@ -49,7 +49,14 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  tile_mainloop<C, V16>(smem, acc, A, P.lda, X, P.ldx, m0, n0, 0, P.K, P.M, P.N);
+  if (P.kr) {   // banded A: only the K tiles its rows meet (zeros skipped exactly)
+    int lo[2], hi[2];
+    const int nint = kr_intervals(P.kr, m0, min(C::BM, P.M - m0), P.kr_c0, 0, P.K, lo, hi);
+    for (int q = 0; q < nint; ++q)
+      tile_mainloop<C, V16>(smem, acc, A, P.lda, X, P.ldx, m0, n0, lo[q], hi[q], P.M, P.N);
+  } else {
+    tile_mainloop<C, V16>(smem, acc, A, P.lda, X, P.ldx, m0, n0, 0, P.K, P.M, P.N);
+  }
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
@@ -367,8 +374,10 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   const int G = 2 * 148;   // resident CTAs of the 64x128 / 81 KB configuration
   const int nk = (probs[0].K + C::BK - 1) / C::BK;
   bool same_k = nprob == 1 || probs[0].K == probs[1].K;
+  bool banded = false;
+  for (int i = 0; i < nprob; ++i) banded = banded || probs[i].kr;
   if constexpr (C::BM == 64 && C::BN == 128 && C::STAGES == 3 && C::BK == 16) {
-  if (sk_env && v16 && batch == 1 && same_k && tiles > G &&
+  if (sk_env && !banded && v16 && batch == 1 && same_k && tiles > G &&
       (tiles % G) != 0 && (double)(tiles % G) / G < 0.75 && nk >= 8) {
     const int r = tiles % G;
     SkArgs S{};
@@ -403,7 +412,7 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     // bulk copies per stage through the copy engine cost more than the per-thread
     // cp.async issue they replace -> opt-in only (WF4DVAR_GEMM_BULK=1)
     static const int bulk_env = env_int("WF4DVAR_GEMM_BULK", 0);   // tuning experiments only
-    bool ok = bulk_env && v16;
+    bool ok = bulk_env && v16 && !banded;
     for (int i = 0; i < nprob; ++i)
       ok = ok && probs[i].K % C::BK == 0 && probs[i].N % 2 == 0 && probs[i].K > 0 &&
            ((uintptr_t)probs[i].A % 16 == 0) && ((uintptr_t)probs[i].X % 16 == 0);
@@ -508,6 +517,101 @@ static void run_small(Ctx &c, const GemmProb *probs, int nprob, int batch, int m
   WF_CUDA(cudaGetLastError());
 }
 
+// ---- tile column ranges (banded covariances and factors)
+// flag[t][j] = 1 iff G[64 t : 64 t + 64, 16 j : 16 j + 16] has a non-zero
+__global__ void k_tile_mask(const double *G, int64_t ld, int rows, int cols, unsigned char *flag) {
+  const int t = blockIdx.x, nj = (cols + 15) / 16;
+  for (int j = threadIdx.x; j < nj; j += blockDim.x) {
+    unsigned char f = 0;
+    for (int r = t * 64; r < min(rows, t * 64 + 64) && !f; ++r)
+      for (int k = j * 16; k < min(cols, j * 16 + 16); ++k)
+        if (G[(int64_t)r * ld + k] != 0.0) { f = 1; break; }
+    flag[(int64_t)t * nj + j] = f;
+  }
+}
+
+void register_tile_ranges(Ctx &c, const double *G, int rows, int cols, int64_t ld) {
+  static const int env = env_int("WF4DVAR_BANDED", 1);   // 0: dense K loops always
+  if (!env || !G || rows <= 0 || cols <= 0) return;
+  unregister_tile_ranges(c, G);
+  const int nt = (rows + 63) / 64, nj = (cols + 15) / 16;
+  unsigned char *dflag = nullptr;
+  WF_CUDA(cudaMalloc(&dflag, (size_t)nt * nj));
+  k_tile_mask<<<nt, 128, 0, c.st>>>(G, ld, rows, cols, dflag);
+  std::vector<unsigned char> f((size_t)nt * nj);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = memcpy_sync(c, f.data(), dflag, f.size(), cudaMemcpyDeviceToHost);
+  cudaFree(dflag);
+  WF_CUDA(e);
+  // per tile: the non-zero chunks as two intervals split at the largest internal gap
+  TileRanges tr;
+  tr.base = G; tr.ld = ld; tr.rows = rows; tr.cols = cols;
+  tr.h.resize(nt);
+  double covered = 0;
+  for (int t = 0; t < nt; ++t) {
+    const unsigned char *ft = &f[(size_t)t * nj];
+    int first = -1, last = -1, gap = 0, gs = -1, ge = -1, prev = -1;
+    for (int j = 0; j < nj; ++j) {
+      if (!ft[j]) continue;
+      if (first < 0) first = j;
+      if (prev >= 0 && j - prev - 1 > gap) { gap = j - prev - 1; gs = prev + 1; ge = j; }
+      prev = last = j;
+    }
+    KRange k{0, 0, 0, 0};
+    if (first >= 0) {
+      if (gap >= 2) k = KRange{first * 16, gs * 16, ge * 16, std::min(cols, (last + 1) * 16)};
+      else k = KRange{first * 16, std::min(cols, (last + 1) * 16), 0, 0};
+    }
+    tr.h[t] = k;
+    covered += (double)std::min(64, rows - t * 64) * ((k.a1 - k.a0) + (k.b1 - k.b0));
+  }
+  if (covered > 0.75 * (double)rows * cols) return;   // not worth the bookkeeping
+  tr.d = c.alloc<KRange>(nt);
+  WF_CUDA(memcpy_sync(c, tr.d, tr.h.data(), nt * sizeof(KRange), cudaMemcpyHostToDevice));
+  c.tranges.push_back(std::move(tr));
+}
+
+void unregister_tile_ranges(Ctx &c, const void *G) {
+  for (size_t i = 0; i < c.tranges.size();) {
+    if (c.tranges[i].base == G) {
+      auto it = std::find(c.allocs.begin(), c.allocs.end(), (void *)c.tranges[i].d);
+      if (it != c.allocs.end()) c.allocs.erase(it);
+      cudaFree(c.tranges[i].d);
+      c.tranges.erase(c.tranges.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+}
+
+const TileRanges *find_tile_ranges(const Ctx &c, const double *A, int *row0, int *col0) {
+  for (const TileRanges &t : c.tranges) {
+    if (A < t.base || A >= t.base + (int64_t)t.rows * t.ld) continue;
+    const int64_t off = A - t.base;
+    const int r = (int)(off / t.ld), q = (int)(off % t.ld);
+    if (r % 64 != 0 || q >= t.cols) return nullptr;
+    *row0 = r;
+    *col0 = q;
+    return &t;
+  }
+  return nullptr;
+}
+
+// sum over the 64-row tiles of rows [r0, r0 + nrows) of rows x covered columns in
+// [k0, k1): the algorithmic (non-zero tile) work of a banded product
+double kr_work(const TileRanges &t, int r0, int nrows, int k0, int k1) {
+  double w = 0;
+  for (int r = r0; r < r0 + nrows;) {
+    const int tt = r / 64, re = std::min(r0 + nrows, tt * 64 + 64);
+    const KRange &k = t.h[tt];
+    const int ca = std::max(0, std::min(k.a1, k1) - std::max(k.a0, k0));
+    const int cb = std::max(0, std::min(k.b1, k1) - std::max(k.b0, k0));
+    w += (double)(re - r) * (ca + cb);
+    r = re;
+  }
+  return w;
+}
+
 void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flops_hint) {
   int valid = 0;
   GemmProb ps[2];
@@ -518,8 +622,17 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
   bool v16 = true;
   int tm, tn, huge_tiles = 0, big_tiles = 0;
   for (int i = 0; i < valid; ++i) {
-    const GemmProb &p = ps[i];
-    flops += 2.0 * p.M * (double)p.N * p.K * batch;
+    GemmProb &p = ps[i];
+    int r0 = 0, c0 = 0;
+    const TileRanges *t = (!p.kr && batch == 1 && !c.tranges.empty() && p.M > 64)
+                              ? find_tile_ranges(c, p.A, &r0, &c0) : nullptr;
+    if (t && c0 % 16 == 0 && p.lda == t->ld && r0 + p.M <= t->rows && c0 + p.K <= t->cols) {
+      p.kr = t->d + r0 / 64;
+      p.kr_c0 = c0;
+      flops += 2.0 * p.N * kr_work(*t, r0, p.M, c0, c0 + p.K);
+    } else {
+      flops += 2.0 * p.M * (double)p.N * p.K * batch;
+    }
     bytes += 8.0 * batch * ((double)p.M * p.K + (double)p.K * p.N + (double)p.M * p.N * (p.Z ? 2 : 1));
     v16 = v16 && aligned16(p);
     huge_tiles += tiles_of<CfgHuge>(p, tm, tn);

@@ -56,6 +56,61 @@ struct Prof {
   std::vector<cudaEvent_t> pool;
 };
 
+// ---------------------------------------------------------------- tile column ranges
+// Non-zero columns of a dense-stored matrix per 64-row tile, as at most two disjoint
+// intervals [a0, a1) u [b0, b1) (multiples of 16, b0 == b1 when there is one): the
+// compact-support (modified-SOAR) covariances of the paper's workload and
+// their Cholesky / IC(0) factors are periodic bands, so a 64-row tile meets the
+// diagonal band plus at most one wrap-around block.  The DMMA GEMM and TRSM kernels
+// skip the K tiles outside them (the dense storage stays; the zeros are not read).
+struct KRange { int a0, a1, b0, b1; };
+struct TileRanges {
+  const double *base = nullptr;
+  int64_t ld = 0;
+  int rows = 0, cols = 0;
+  KRange *d = nullptr;          // device, one per 64-row tile
+  std::vector<KRange> h;        // host copy (flop accounting)
+};
+struct Ctx;
+// scan G on the device and register its ranges if they skip >= 25% of the tiles
+void register_tile_ranges(Ctx &c, const double *G, int rows, int cols, int64_t ld);
+void unregister_tile_ranges(Ctx &c, const void *G);
+// the registered matrix containing A (row offset a multiple of 64), else nullptr
+const TileRanges *find_tile_ranges(const Ctx &c, const double *A, int *row0, int *col0);
+// sum over the 64-row tiles of rows [r0, r0 + nrows) of rows x covered columns in [k0, k1)
+double kr_work(const TileRanges &t, int r0, int nrows, int k0, int k1);
+
+// Column intervals met by rows [r0, r0 + nrows) (kr indexed by 64-row tile from row 0),
+// shifted by -c0 and clipped to [kbeg, kend): disjoint, ascending; returns 0..2.
+// Cover of several tiles: the union of their first and of their second intervals.
+__device__ __forceinline__ int kr_intervals(const KRange *kr, int r0, int nrows, int c0,
+                                            int kbeg, int kend, int (&lo)[2], int (&hi)[2]) {
+  const int t0 = r0 >> 6, t1 = (r0 + nrows - 1) >> 6;
+  int a0 = 1 << 30, a1 = -(1 << 30), b0 = 1 << 30, b1 = -(1 << 30);
+  for (int t = t0; t <= t1; ++t) {
+    const KRange k = kr[t];
+    if (k.a1 > k.a0) { a0 = min(a0, k.a0); a1 = max(a1, k.a1); }
+    if (k.b1 > k.b0) { b0 = min(b0, k.b0); b1 = max(b1, k.b1); }
+  }
+  int n = 0;
+  auto add = [&](int x0, int x1) {
+    x0 = max(x0 - c0, kbeg);
+    x1 = min(x1 - c0, kend);
+    if (x1 > x0) { lo[n] = x0; hi[n] = x1; ++n; }
+  };
+  const bool ha = a1 > a0, hb = b1 > b0;
+  if (ha && hb && b0 < a1 && b1 > a0) {
+    add(min(a0, b0), max(a1, b1));
+  } else if (ha && hb && b0 < a0) {
+    add(b0, b1);
+    add(a0, a1);
+  } else {
+    if (ha) add(a0, a1);
+    if (hb) add(b0, b1);
+  }
+  return n;
+}
+
 // ---------------------------------------------------------------- GEMM
 // Y[b] = alpha * A[b] (M x K, row-major, lda) * X[b] (K x N, row-major, ldx)
 //        + beta * Z[b] (rows optionally re-indexed by zrow: Z row zrow[i] feeds Y row i)
@@ -68,6 +123,10 @@ struct GemmProb {
   const int *zrow;
   int M, N, K;
   double alpha, beta;
+  // optional column ranges of A: kr[t] covers GEMM rows [64 t, 64 t + 64); columns are
+  // A's own minus kr_c0 (filled by launch_gemm from the registry)
+  const KRange *kr = nullptr;
+  int kr_c0 = 0;
 };
 
 // Triangular solve with a CTA per column panel:
@@ -83,6 +142,7 @@ struct TrsmProb {
   int blk;        // 0 = dense triangle, else block-diagonal block size
   const std::vector<int> *segs = nullptr;   // else: block-diagonal with these block starts
   const double *dpack = nullptr;            // optional setup pack of the diagonal tiles
+  const KRange *kr = nullptr;               // optional column ranges of G (64-row tiles)
 };
 struct Ctx;
 // pack of the 64x64 diagonal tiles of an n x n triangular factor (ld = n), setup time
@@ -182,6 +242,7 @@ struct Ctx {
   double *PR = nullptr, *PRt = nullptr;
   SparseFactor icB, icQ, icR;     // IC(0) factors (pc.factor == WF4DVAR_FACTOR_ICHOL)
   double *Rdiag_inv = nullptr;                                           // [p]
+  std::vector<TileRanges> tranges; // registered column ranges (banded covariances / factors)
   std::vector<int> rblk_starts;   // R_block (Algorithm 1): block starts + p (empty = uniform)
   std::vector<int> pvec_store;    // copy of the caller's pvec (pc.pvec points here)
   double *U_me = nullptr, *Kinv_me = nullptr; int r_me = 0;              // Woodbury

@@ -294,6 +294,7 @@ static void eigh(Ctx &c, Solver &sv, const double *Adev, int n, std::vector<doub
 
 static void dev_free(Ctx &c, double *&ptr) {
   if (!ptr) return;
+  unregister_tile_ranges(c, ptr);
   auto it = std::find(c.allocs.begin(), c.allocs.end(), (void *)ptr);
   if (it != c.allocs.end()) c.allocs.erase(it);
   cudaFree(ptr);

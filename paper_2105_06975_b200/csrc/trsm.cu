@@ -86,9 +86,18 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
     for (int i = 0; i < C::FM; ++i)
 #pragma unroll
       for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    if (kend > kbeg)
-      tile_mainloop<C, V16>(sPipe, acc, G + (int64_t)r0 * P.ldg, P.ldg, Y + c0, P.ldy, 0, 0, kbeg,
-                            kend, nr, ncols - c0);
+    if (kend > kbeg) {
+      if (P.kr && (r0 & 63) == 0) {   // banded factor: only the K tiles these rows meet
+        int lo[2], hi[2];
+        const int nint = kr_intervals(P.kr, r0, nr, 0, kbeg, kend, lo, hi);
+        for (int q = 0; q < nint; ++q)
+          tile_mainloop<C, V16>(sPipe, acc, G + (int64_t)r0 * P.ldg, P.ldg, Y + c0, P.ldy, 0, 0,
+                                lo[q], hi[q], nr, ncols - c0);
+      } else {
+        tile_mainloop<C, V16>(sPipe, acc, G + (int64_t)r0 * P.ldg, P.ldg, Y + c0, P.ldy, 0, 0,
+                              kbeg, kend, nr, ncols - c0);
+      }
+    }
     // ---- T = X - acc  -> shared memory
 #pragma unroll
     for (int i = 0; i < C::FM; ++i) {
@@ -200,6 +209,7 @@ double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
   const int nt = (n + TB - 1) / TB;
   double *pk = c.alloc<double>((size_t)nt * kDiagPack);
   fill_diag_pack(c, G, n, upper, pk);
+  register_tile_ranges(c, G, n, n, n);   // banded factors: skip their zero tiles
   WF_CUDA(cudaStreamSynchronize(c.st));
   return pk;
 }
@@ -326,7 +336,19 @@ static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int
     L.p[i] = probs[i];
     total_cols += probs[i].ncols;
     double rows = seg_hi - seg_lo;
-    flops += tri * probs[i].ncols;
+    int r0 = 0, c0 = 0;
+    const TileRanges *tr = probs[i].kr ? find_tile_ranges(c, probs[i].G, &r0, &c0) : nullptr;
+    if (tr && r0 == 0 && c0 == 0) {   // banded: the non-zero tiles of each segment's triangle
+      double w = 0;
+      for (int j = 0; j < nseg; ++j) {
+        const int a = tab ? (*tab)[j] : seg_lo + j * seg_len;
+        const int b = tab ? (*tab)[j + 1] : std::min(seg_hi, a + seg_len);
+        w += kr_work(*tr, a, b - a, a, b);
+      }
+      flops += 2.0 * w * probs[i].ncols;
+    } else {
+      flops += tri * probs[i].ncols;
+    }
     bytes += 8.0 * (tri / 2 + 2.0 * rows * probs[i].ncols);
     v16 = v16 && ((uintptr_t)probs[i].G % 16 == 0) && ((uintptr_t)probs[i].Y % 16 == 0) &&
           (probs[i].ldg % 2 == 0) && (probs[i].ldy % 2 == 0);
@@ -427,6 +449,13 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   for (int i = 0; i < nprob; ++i)
     if (probs_in[i].ncols > 0 && probs_in[i].n > 0) probs[np++] = probs_in[i];
   if (!np) return;
+  for (int i = 0; i < np; ++i) {   // banded factor: its registered column ranges
+    int r0 = 0, c0 = 0;
+    const TileRanges *tr = (!probs[i].kr && !c.tranges.empty())
+                               ? find_tile_ranges(c, probs[i].G, &r0, &c0) : nullptr;
+    if (tr && r0 == 0 && c0 == 0 && tr->ld == probs[i].ldg && tr->rows >= probs[i].n)
+      probs[i].kr = tr->d;
+  }
   const int n = probs[0].n;
   const int blk = probs[0].blk;
   if (probs[0].segs) {   // variable block-diagonal factor (Algorithm 1): independent segments
