@@ -88,6 +88,11 @@ typedef enum {
                           r = heat_r; applied as n fused 3-point sweeps          */
 } wf4dvar_model;
 
+/* B, Q, R (and the triangular factors built from them) are stored densely on the
+ * device.  Compact-support matrices (e.g. the modified SOAR of P:L566-570, zero for
+ * circular lag >= maxval) are detected at create / set_precond time: the exact-zero
+ * 64 x 16 tiles are never read by the covariance products and triangular solves
+ * (results bit-identical to the dense loops; env WF4DVAR_BANDED=0 disables it). */
 typedef struct {
   int32_t s, p, N, m;      /* state size, obs per window, N (W = N+1 windows), RHS   */
   const double *B;         /* [s*s] host, SPD, row-major                            */
