@@ -502,7 +502,7 @@ extern "C" int wf4dvar_test_trsm(int n, int ncols, int upper, int blk, const dou
     // reuses memory), into a per-thread buffer grown on demand
     static thread_local double *pk = nullptr;
     static thread_local size_t pk_cap = 0;
-    const size_t need = (size_t)((n + 63) / 64) * (64 * 65 + 64);
+    const size_t need = wf::diag_pack_doubles(n);
     if (need > pk_cap) {
       if (pk) cudaFree(pk);
       WF_CUDA(cudaMalloc(&pk, need * 8));

@@ -148,6 +148,7 @@ struct Ctx;
 // pack of the 64x64 diagonal tiles of an n x n triangular factor (ld = n), setup time
 double *make_diag_pack(Ctx &c, const double *G, int n, bool upper);
 void fill_diag_pack(Ctx &c, const double *G, int n, bool upper, double *pack);   // async
+size_t diag_pack_doubles(int n);   // size of that pack
 
 struct Ctx;
 

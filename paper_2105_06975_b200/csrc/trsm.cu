@@ -31,7 +31,18 @@ using TrsmCfg = typename std::conditional<NB == 8, TileCfg<64, 8, 16, 16, 8, TRS
                                           TileCfg<64, NB, 16, 32, NB / 2, TRSM_STAGES>>::type;
 
 constexpr int kMaxSegTab = 512;
-constexpr int kDiagPack = TB * (TB + 1) + TB;   // doubles per packed diagonal tile   // variable block-diagonal factors (Algorithm 1 R_block)
+// doubles per packed diagonal tile: substitution form (transposed masked tile, stride
+// 65, + 64 reciprocals = 4160) or inverse form (G_ii^{-1} row-major, stride kInvLd)
+constexpr int kInvLd = TB + 4;
+constexpr int kDiagPack = TB * kInvLd;
+static_assert(kDiagPack >= TB * (TB + 1) + TB, "pack holds either form");
+
+// WF4DVAR_TRSM_INV=1: diagonal tiles applied as setup-time inverses (one DMMA product
+// per tile instead of the 64-step substitution chain)
+static int trsm_inv_mode() {
+  static const int v = env_int("WF4DVAR_TRSM_INV", 0);
+  return v;
+}
 
 struct TrsmLaunch {
   TrsmProb p[2];
@@ -41,7 +52,7 @@ struct TrsmLaunch {
   int tab[kMaxSegTab + 1];
 };
 
-template <int NB, bool UPPER, bool V16>
+template <int NB, bool UPPER, bool V16, bool INV>
 __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   using C = TrsmCfg<NB>;
   extern __shared__ __align__(16) double smem[];
@@ -111,6 +122,44 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
           if (rr < nr && c0 + cc < ncols) xv = X[(int64_t)(r0 + rr) * P.ldx + c0 + cc];
           sT[rr * (NB + 1) + cc] = xv - acc[i][j][h];
         }
+    }
+    if (INV && dpk) {
+      // ---- Y_i = G_ii^{-1} T_i on the tensor pipe (the setup-time inverse in sG,
+      // row-major stride kInvLd; identity padding past a ragged tile).  Warp w owns
+      // the 8-row blocks w and w + 4 across all NB columns.
+      cp_async_wait<0>();
+      __syncthreads();
+      constexpr int NJ = NB / 8;
+      double ya[2][NJ][2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) ya[q][j][0] = ya[q][j][1] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < TB; kk += 4) {
+        const double a0 = sG[(warp * 8 + g) * kInvLd + kk + t];
+        const double a1 = sG[((warp + 4) * 8 + g) * kInvLd + kk + t];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+          const double b = sT[(kk + t) * (NB + 1) + j * 8 + g];
+          dmma884(ya[0][j][0], ya[0][j][1], a0, b);
+          dmma884(ya[1][j][0], ya[1][j][1], a1, b);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int rr = (warp + 4 * q) * 8 + g;
+        if (rr >= nr) continue;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int cc = j * 8 + 2 * t + h;
+            if (c0 + cc < ncols) Y[(int64_t)(r0 + rr) * P.ldy + c0 + cc] = ya[q][j][h];
+          }
+      }
+      __syncthreads();   // Y rows visible to the CTA; sG / sT free for the next tile
+      continue;
     }
     // ---- diagonal tile, transposed and masked:
     //   sG[c][r] = G[r0 + r][r0 + c] for r strictly below (lower) / above (upper) c, else 0;
@@ -199,11 +248,58 @@ __global__ void k_pack_diag(const double *G, int n, int upper, double *pack) {
   for (int e = threadIdx.x; e < TB; e += blockDim.x) pk[e * (TB + 1) + TB] = 0.0;   // pad col
 }
 
+// Inverse form: pack[t] = G_tt^{-1} (row-major, stride kInvLd), computed column by
+// column (thread j: substitution of G_tt x = e_j), identity padding past n.
+__global__ void k_pack_diag_inv(const double *G, int n, int upper, double *pack) {
+  __shared__ double sg[TB][TB + 1];
+  const int t = blockIdx.x;
+  const int r0 = t * TB, nr = min(TB, n - r0);
+  double *pk = pack + (int64_t)t * kDiagPack;
+  for (int e = threadIdx.x; e < TB * TB; e += blockDim.x) {
+    const int r = e / TB, cc = e % TB;
+    sg[r][cc] = (r < nr && cc < nr) ? G[(int64_t)(r0 + r) * n + r0 + cc] : (r == cc ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j >= TB) return;
+  double x[TB];
+#pragma unroll
+  for (int i = 0; i < TB; ++i) x[i] = 0.0;
+  if (!upper) {
+#pragma unroll
+    for (int i = 0; i < TB; ++i) {
+      if (i < j) continue;
+      double v = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < TB; ++k)
+        if (k >= j && k < i) v = fma(-sg[i][k], x[k], v);
+      x[i] = v / sg[i][i];
+    }
+  } else {
+#pragma unroll
+    for (int i = TB - 1; i >= 0; --i) {
+      if (i > j) continue;
+      double v = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < TB; ++k)
+        if (k > i && k <= j) v = fma(-sg[i][k], x[k], v);
+      x[i] = v / sg[i][i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TB; ++i) pk[i * kInvLd + j] = x[i];
+  for (int e = j; e < TB * (kInvLd - TB); e += TB)   // padding columns
+    pk[(e / (kInvLd - TB)) * kInvLd + TB + e % (kInvLd - TB)] = 0.0;
+}
+
 void fill_diag_pack(Ctx &c, const double *G, int n, bool upper, double *pk) {
   const int nt = (n + TB - 1) / TB;
-  k_pack_diag<<<nt, 256, 0, c.st>>>(G, n, upper ? 1 : 0, pk);
+  if (trsm_inv_mode()) k_pack_diag_inv<<<nt, TB, 0, c.st>>>(G, n, upper ? 1 : 0, pk);
+  else k_pack_diag<<<nt, 256, 0, c.st>>>(G, n, upper ? 1 : 0, pk);
   WF_CUDA(cudaGetLastError());
 }
+
+size_t diag_pack_doubles(int n) { return (size_t)((n + TB - 1) / TB) * kDiagPack; }
 
 double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
   const int nt = (n + TB - 1) / TB;
@@ -214,19 +310,25 @@ double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
   return pk;
 }
 
-template <int NB, bool UPPER>
-static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
+template <int NB, bool UPPER, bool INV>
+static void run_inv(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   using C = TrsmCfg<NB>;
-  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + TB * (TB + 1) + TB) * sizeof(double);
-  auto kern = v16 ? k_trsm<NB, UPPER, true> : k_trsm<NB, UPPER, false>;
+  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + kDiagPack) * sizeof(double);
+  auto kern = v16 ? k_trsm<NB, UPPER, true, INV> : k_trsm<NB, UPPER, false, INV>;
   // one-time (thread-safe static initialisation) opt-in to the large dynamic smem
   static const cudaError_t attr_v =
-      cudaFuncSetAttribute(k_trsm<NB, UPPER, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_trsm<NB, UPPER, true, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   static const cudaError_t attr_n =
-      cudaFuncSetAttribute(k_trsm<NB, UPPER, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_trsm<NB, UPPER, false, INV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   WF_CUDA(v16 ? attr_v : attr_n);
   kern<<<dim3(panels, nseg), 128, smem, c.st>>>(L);
   WF_CUDA(cudaGetLastError());
+}
+
+template <int NB, bool UPPER>
+static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
+  if (trsm_inv_mode()) run_inv<NB, UPPER, true>(c, L, panels, nseg, v16);
+  else run_inv<NB, UPPER, false>(c, L, panels, nseg, v16);
 }
 
 // Small triangles: every segment (diagonal block) has <= 64 rows -- R_hat / D_hat of the
