@@ -105,3 +105,36 @@ def test_trsm_in_place():
     torch.cuda.synchronize()
     torch.testing.assert_close(Yd.cpu(), torch.linalg.solve_triangular(G, X, upper=False),
                                rtol=1e-12, atol=1e-12)
+
+
+SUBST = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2105_06975_b200 import _lib
+g = torch.Generator().manual_seed(4)
+for n, ncols, upper in ((600, 40, False), (600, 40, True), (130, 17, False)):
+    M = torch.randn(n, n, generator=g, dtype=torch.float64)
+    S = M @ M.T / n + torch.eye(n, dtype=torch.float64)
+    F = torch.linalg.cholesky(S)
+    F = (F.T if upper else F).contiguous()
+    X = torch.randn(n, ncols, generator=g, dtype=torch.float64)
+    Y = torch.empty(n, ncols, dtype=torch.float64, device="cuda")
+    _lib.test_trsm(F.cuda(), X.cuda(), Y, upper=upper)
+    torch.cuda.synchronize()
+    Yc = Y.cpu()
+    bwd = ((F @ Yc - X).norm() / (F.norm() * Yc.norm())).item()
+    assert bwd <= 4e-15, (n, upper, bwd)
+print("ok")
+"""
+
+
+def test_trsm_substitution_form():
+    """The diagonal tiles' substitution form (WF4DVAR_TRSM_INV=0, the pre-A31 path)
+    stays available and backward stable."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", SUBST, root], capture_output=True, text=True,
+                       env=dict(os.environ, WF4DVAR_TRSM_INV="0"), timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
