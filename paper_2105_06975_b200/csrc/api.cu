@@ -129,6 +129,8 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       WF_CUDA(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    WF_CUDA(cudaStreamCreateWithFlags(&c.cpy, cudaStreamNonBlocking));
+    for (auto &e : c.ev_in) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.s = p.s; c.p = p.p; c.N = p.N; c.WG = p.N + 1; c.m = p.m; c.model = p.model;
     int wb = 0, we = c.WG;
     wf::partition(c.WG, world, rank, &wb, &we);
@@ -235,6 +237,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
   }
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.cpy) { cudaStreamSynchronize(c.cpy); cudaStreamDestroy(c.cpy); }
+  for (auto &e : c.ev_in) if (e) cudaEventDestroy(e);
   c.drop_graphs();
   if (c.own_st) { cudaStreamSynchronize(c.own_st); cudaStreamDestroy(c.own_st); }
   delete c.comm;
@@ -298,10 +302,11 @@ wf4dvar_status wf4dvar_apply_AP_host(wf4dvar_ctx ctx, const double *x_host, doub
       c.dev_io_t = c.alloc<double>(c.n);
       c.dev_io_y = c.alloc<double>(c.n);
     }
-    WF_CUDA(cudaMemcpyAsync(c.dev_io_x, x_host, c.n * 8, cudaMemcpyHostToDevice, c.st));
-    wf::apply_P(c, c.dev_io_x, c.dev_io_t);
-    wf::apply_A(c, c.dev_io_t, c.dev_io_y);
-    WF_CUDA(cudaMemcpyAsync(y_host, c.dev_io_y, c.n * 8, cudaMemcpyDeviceToHost, c.st));
+    // block-wise copies overlapped with the blocks' solves / products (see apply_P /
+    // apply_A): the input blocks land in the order the streams consume them, each
+    // output block leaves as soon as it is computed
+    wf::apply_P(c, c.dev_io_x, c.dev_io_t, x_host);
+    wf::apply_A(c, c.dev_io_t, c.dev_io_y, y_host);
     WF_CUDA(cudaStreamSynchronize(c.st));
   });
 }

@@ -215,6 +215,8 @@ struct Ctx {
   // fork/join streams: the three independent blocks of A and of P_D run concurrently
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaStream_t cpy = nullptr;          // host path: block-wise H2D of apply_P's input
+  cudaEvent_t ev_in[4] = {nullptr, nullptr, nullptr, nullptr};
   bool aux_priority = true;       // env WF4DVAR_AUX_PRIORITY=0 disables (experiments)
   int device = 0;
   // device data
@@ -409,8 +411,13 @@ void pack_window(Ctx &c, double *dst, const double *seg, int wl);
 void csr_apply(Ctx &c, double *y, const double *x, const int *rowptr, const int *col,
                const double *val, int nrows, bool accumulate);
 
-void apply_A(Ctx &c, const double *x, double *y);
-void apply_P(Ctx &c, const double *x, double *y);
+// host_y != nullptr: every output block is copied to host_y on its own stream as soon
+// as it is computed (the host path, overlapping the D2H with the remaining blocks)
+void apply_A(Ctx &c, const double *x, double *y, double *host_y = nullptr);
+// host_x != nullptr: x is the library's device staging buffer, filled from host_x block
+// by block (D_hat / first block first) on the copy stream; each block's solve starts
+// when its own input has landed
+void apply_P(Ctx &c, const double *x, double *y, const double *host_x = nullptr);
 
 // Gauss-Newton outer loops (outer.cu)
 void outer_loop(Ctx &c, const double *xb, const double *y, double *x, int n_outer,

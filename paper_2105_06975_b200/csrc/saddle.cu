@@ -126,7 +126,7 @@ void join(Ctx &c) {
   }
 }
 
-void apply_A(Ctx &c, const double *x, double *y) {
+void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
   const int s = c.s, p = c.p;
   const int64_t ld = c.ncol;
   const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
@@ -162,6 +162,9 @@ void apply_A(Ctx &c, const double *x, double *y) {
       GemmProb g = gp(c.R, p, x2, ld, y2, ld, x3, ld, p, (int)ld, p, 1.0, 1.0, c.H_idx);
       launch_gemm(c, &g, 1, 1);
     }
+    if (host_y)
+      WF_CUDA(cudaMemcpyAsync(host_y + (int64_t)s * ld, y2, (size_t)p * ld * 8,
+                              cudaMemcpyDeviceToHost, c.st));
   }
   {
     // c3 = L^T x1 + H^T x2 (selection H: scatter fused into the model pass)
@@ -172,33 +175,57 @@ void apply_A(Ctx &c, const double *x, double *y) {
     } else {
       model_step(c, true, -1.0, x1, x1, y3, 0, 1, c.W, x2, c.H_inv);
     }
+    if (host_y)
+      WF_CUDA(cudaMemcpyAsync(host_y + (int64_t)(s + p) * ld, y3, (size_t)s * ld * 8,
+                              cudaMemcpyDeviceToHost, c.st));
   }
   // c1 = L x3 + D x1
   model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
   d_product(c, x1, y1, y1, 1.0, 1.0);
+  if (host_y)
+    WF_CUDA(cudaMemcpyAsync(host_y, y1, (size_t)s * ld * 8, cudaMemcpyDeviceToHost, c.st));
   join(c);
   c.n_R += c.WG;
   c.n_M += 2 * c.N;
   c.n_A++;
 }
 
-void apply_P(Ctx &c, const double *x, double *y) {
+void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
   const int s = c.s, p = c.p;
   const int64_t ld = c.ncol;
   const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
   double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  // host path: the three input blocks in the order their consumers need them
+  // (x1: the D_hat^{-1} / D products, x3: the L_hat chain, x2: the small R_hat^{-1})
+  auto wait_in = [&](int b) {
+    if (host_x) WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_in[b], 0));
+  };
+  if (host_x) {
+    WF_CUDA(cudaEventRecord(c.ev_in[3], c.st));
+    WF_CUDA(cudaStreamWaitEvent(c.cpy, c.ev_in[3], 0));
+    const int64_t off[3] = {0, (int64_t)(s + p) * ld, (int64_t)s * ld};
+    const int64_t len[3] = {(int64_t)s * ld, (int64_t)s * ld, (int64_t)p * ld};
+    for (int b = 0; b < 3; ++b) {
+      WF_CUDA(cudaMemcpyAsync(const_cast<double *>(x) + off[b], host_x + off[b], len[b] * 8,
+                              cudaMemcpyHostToDevice, c.cpy));
+      WF_CUDA(cudaEventRecord(c.ev_in[b], c.cpy));
+    }
+  }
   fork(c);
   if (c.pc.shape == WF4DVAR_PD) {
     // three independent blocks: D_hat^{-1} | R_hat^{-1} | S_hat^{-1}
     {
       OnStream os(c, c.aux[0]);
+      wait_in(2);
       rhat_inv(c, x2, y2);
     }
     {
       OnStream os(c, c.aux[1]);
+      wait_in(0);
       dhat_inv(c, x1, y1);                     // latency-bound TRSM chain: priority stream
     }
     double *t = c.ws_seg;
+    wait_in(1);
     copy(c, t, x3, (int64_t)s * ld);
     lhat_solve(c, true, t);                    // L_hat^{-T} x3
     d_product(c, t, y3, nullptr, 1.0, 0.0);    // D (exact D)
@@ -206,8 +233,11 @@ void apply_P(Ctx &c, const double *x, double *y) {
   } else {
     {
       OnStream os(c, c.aux[0]);
+      wait_in(2);
       rhat_inv(c, x2, y2);                     // c2
     }
+    wait_in(0);
+    wait_in(1);
     copy(c, y1, x3, (int64_t)s * ld);
     lhat_solve(c, true, y1);                   // c1 = L_hat^{-T} x3
     d_product(c, y1, y3, x1, -1.0, 1.0);       // x1 - D c1
