@@ -96,6 +96,7 @@ struct SkArgs {
   unsigned *flags;           // [G]
   unsigned epoch;            // value a published flag carries in this launch
   int G, dp_tiles, sk_tiles, nk;
+  int dp_begin;              // first data-parallel tile this launch runs (dp_tiles: none)
 };
 
 template <class C>
@@ -216,7 +217,7 @@ __global__ void __launch_bounds__(C::NT) k_gemm_sk(const GemmLaunch L, const SkA
     piece(lt, 0, S.nk);
   if (first_is_end) piece(lt_first, kb_first, lt_last == lt_first ? ke_last : S.nk);
   // ---- data-parallel part
-  for (int tile = c; tile < S.dp_tiles; tile += S.G) {
+  for (int tile = S.dp_begin + c; tile < S.dp_tiles; tile += S.G) {
     int gi, m0, n0;
     tile_coords<C>(L, tile, gi, m0, n0);
     const GemmProb &P = L.p[gi];
@@ -370,15 +371,23 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   }
   size_t smem = C::SMEM_DOUBLES * sizeof(double);
   // stream-K hybrid when one batch of large tiles quantises badly onto the waves
-  static const int sk_env = env_int("WF4DVAR_GEMM_SK", 0);   // 0 disables (tuning experiments)
+  // Split launch (default): the data-parallel waves run in the plain k_gemm (its main
+  // loop keeps 214 registers and ~95% DMMA-pipe occupancy in steady state, ncu r01ak),
+  // then the stream-K kernel runs only the last G + r tiles split evenly by
+  // k-iterations.  The single persistent kernel (WF4DVAR_GEMM_SK=2) runs its DP tiles
+  // at 254 registers / 81% pipe and lost (r01ak: 29.9 vs 30.8 TFLOP/s at
+  // 4096 x 8256 x 4096).  Only when the tail wave is nearly empty (r < 0.3 G): the
+  // stream-K part costs (G + r) / G tile-times at lower efficiency.
+  static const int sk_env = env_int("WF4DVAR_GEMM_SK", 1);   // 0 disables
   const int G = 2 * 148;   // resident CTAs of the 64x128 / 81 KB configuration
   const int nk = (probs[0].K + C::BK - 1) / C::BK;
   bool same_k = nprob == 1 || probs[0].K == probs[1].K;
   bool banded = false;
   for (int i = 0; i < nprob; ++i) banded = banded || probs[i].kr;
   if constexpr (C::BM == 64 && C::BN == 128 && C::STAGES == 3 && C::BK == 16) {
+  const double sk_max_tail = sk_env == 2 ? 0.75 : 0.3;
   if (sk_env && !banded && v16 && batch == 1 && same_k && tiles > G &&
-      (tiles % G) != 0 && (double)(tiles % G) / G < 0.75 && nk >= 8) {
+      (tiles % G) != 0 && (double)(tiles % G) / G < sk_max_tail && nk >= 8) {
     const int r = tiles % G;
     SkArgs S{};
     S.G = G;
@@ -402,6 +411,15 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     if (S.epoch == 0) S.epoch = ++c.sk_epoch;
     static const cudaError_t attr = cudaFuncSetAttribute(k_gemm_sk<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     WF_CUDA(attr);
+    S.dp_begin = 0;
+    if (sk_env != 2 && S.dp_tiles > 0) {
+      static const cudaError_t attr_dp = cudaFuncSetAttribute(k_gemm<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      WF_CUDA(attr_dp);
+      k_gemm<C, true><<<dim3(S.dp_tiles, 1, 1), C::NT, smem, c.st>>>(L);   // tiles [0, dp_tiles)
+      WF_CUDA(cudaGetLastError());
+      c.launches++;
+      S.dp_begin = S.dp_tiles;
+    }
     k_gemm_sk<C, true><<<G, C::NT, smem, c.st>>>(L, S);
     WF_CUDA(cudaGetLastError());
     return;

@@ -32,12 +32,13 @@ def test_gemm_vs_float64_reference(M, N, K, with_z):
 
 
 @pytest.mark.parametrize("M,N,K", [(1024, 2432, 256), (1000, 2500, 200), (3072, 8192, 1024),
-                                   (4096, 8192, 128)])
+                                   (4096, 8192, 128), (4096, 8256, 512)])
 def test_gemm_stream_k_tail_vs_float64_reference(M, N, K):
-    """Tile counts that leave a partial last wave (304, 320, 3072 tiles of 64x128 on
-    296 resident CTAs) take the stream-K hybrid: split tiles, parked partials,
-    deterministic fix-up.  Same tolerance as the data-parallel kernel, and
-    bitwise-reproducible across launches."""
+    """Tile counts that leave a nearly empty last wave (304, 320, 4160 tiles of 64x128
+    on 296 resident CTAs) take the stream-K hybrid: the data-parallel waves in the
+    plain kernel, the last G + r tiles split by k-iterations with parked partials and
+    a deterministic fix-up (3072 / 4096 tiles: plain kernel).  Same tolerance as the
+    data-parallel kernel, and bitwise-reproducible across launches."""
     g = torch.Generator().manual_seed(M + N + K)
     A = torch.randn(M, K, generator=g, dtype=torch.float64).cuda()
     X = torch.randn(K, N, generator=g, dtype=torch.float64).cuda()

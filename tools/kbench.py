@@ -26,7 +26,8 @@ def timeit(fn, reps=5):
 def main():
     out = {}
     gemm_shapes = [] if "--trsm-only" in sys.argv else [
-        (4096, 8128, 4096), (1024, 8192, 1024), (3584, 8192, 512), (1000, 320, 1000)]
+        (4096, 8128, 4096), (4096, 8256, 4096), (4096, 8192, 4096), (3072, 8256, 1024),
+        (2048, 8256, 1024), (1024, 8192, 1024), (3584, 8192, 512), (1000, 320, 1000)]
     for (M, N, K) in gemm_shapes:
         A = torch.randn(M, K, dtype=torch.float64, device="cuda")
         X = torch.randn(K, N, dtype=torch.float64, device="cuda")
