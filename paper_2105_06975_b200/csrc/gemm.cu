@@ -644,10 +644,15 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
     int r0 = 0, c0 = 0;
     const TileRanges *t = (!p.kr && batch == 1 && !c.tranges.empty() && p.M > 64)
                               ? find_tile_ranges(c, p.A, &r0, &c0) : nullptr;
-    if (t && c0 % 16 == 0 && p.lda == t->ld && r0 + p.M <= t->rows && c0 + p.K <= t->cols) {
+    // attach only where the ranges skip work: the off-diagonal blocks a blocked TRSM
+    // couples with are dense even when the (triangular) factor is registered, and a
+    // dense GEMM keeps the stream-K tail (r01am: the coupling GEMMs had lost it)
+    const double w = (t && c0 % 16 == 0 && p.lda == t->ld && r0 + p.M <= t->rows &&
+                      c0 + p.K <= t->cols) ? kr_work(*t, r0, p.M, c0, c0 + p.K) : -1.0;
+    if (w >= 0 && w < 0.9 * (double)p.M * p.K) {
       p.kr = t->d + r0 / 64;
       p.kr_c0 = c0;
-      flops += 2.0 * p.N * kr_work(*t, r0, p.M, c0, c0 + p.K);
+      flops += 2.0 * p.N * w;
     } else {
       flops += 2.0 * p.M * (double)p.N * p.K * batch;
     }
