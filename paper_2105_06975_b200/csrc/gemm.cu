@@ -385,7 +385,8 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
   bool banded = false;
   for (int i = 0; i < nprob; ++i) banded = banded || probs[i].kr;
   if constexpr (C::BM == 64 && C::BN == 128 && C::STAGES == 3 && C::BK == 16) {
-  const double sk_max_tail = sk_env == 2 ? 0.75 : 0.3;
+  static const int sk_tail_env = env_int("WF4DVAR_GEMM_SK_TAIL", 30);   // percent of G
+  const double sk_max_tail = sk_env == 2 ? 0.75 : sk_tail_env / 100.0;
   if (sk_env && !banded && v16 && batch == 1 && same_k && tiles > G &&
       (tiles % G) != 0 && (double)(tiles % G) / G < sk_max_tail && nk >= 8) {
     const int r = tiles % G;
