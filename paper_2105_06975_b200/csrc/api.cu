@@ -243,8 +243,10 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   if (c.own_st) { cudaStreamSynchronize(c.own_st); cudaStreamDestroy(c.own_st); }
   delete c.comm;
   c.comm = nullptr;
-  if (c.sk_ws) cudaFree(c.sk_ws);
-  if (c.sk_flags) cudaFree(c.sk_flags);
+  for (auto &e : c.sk_states) {
+    if (e.ws) cudaFree(e.ws);
+    if (e.flags) cudaFree(e.flags);
+  }
   for (void *p : c.allocs) cudaFree(p);
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : c.prof.pool) cudaEventDestroy(e);

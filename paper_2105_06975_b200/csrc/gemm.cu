@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
 struct SkArgs {
   double *ws;                // [G][C::NT * FM*FN*2] parked partial accumulators
   unsigned *flags;           // [G]
-  unsigned epoch;            // value a published flag carries in this launch
+  unsigned epoch;            // unused (kept for the layout); flags are 0 / 1, reset by
+                             // their consumer, so a captured graph can replay the launch
   int G, dp_tiles, sk_tiles, nk;
   int dp_begin;              // first data-parallel tile this launch runs (dp_tiles: none)
 };
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(C::NT) k_gemm_sk(const GemmLaunch L, const SkA
           for (int h = 0; h < 2; ++h, ++q) slot[(int64_t)q * C::NT + threadIdx.x] = acc[i][j][h];
       __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) atomicExch(S.flags + c, S.epoch);
+      if (threadIdx.x == 0) atomicExch(S.flags + c, 1u);
       return;
     }
     if (kb > 0) {
@@ -189,7 +190,10 @@ __global__ void __launch_bounds__(C::NT) k_gemm_sk(const GemmLaunch L, const SkA
       while (c0 > 0 && range_lo(c0) > tile_lo) --c0;
       for (int cc = c - 1; cc >= c0; --cc) {
         if (threadIdx.x == 0) {
-          while (atomicAdd(S.flags + cc, 0u) != S.epoch) __nanosleep(64);
+          while (atomicAdd(S.flags + cc, 0u) != 1u) __nanosleep(64);
+          // the only consumer of CTA cc's start piece: re-arm its flag for the next
+          // launch on this stream (the slot is not rewritten before then)
+          atomicExch(S.flags + cc, 0u);
         }
         __syncthreads();
         __threadfence();
@@ -397,19 +401,29 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     S.nk = nk;
     constexpr int NACC = C::FM * C::FN * 2;
     const size_t need = (size_t)G * C::NT * NACC;
-    if (c.sk_ws_cap < need) {
-      if (c.sk_ws) cudaFree(c.sk_ws);
-      if (c.sk_flags) cudaFree(c.sk_flags);
-      c.sk_ws = nullptr; c.sk_flags = nullptr; c.sk_ws_cap = 0;
-      WF_CUDA(cudaMalloc(&c.sk_ws, need * 8));
-      WF_CUDA(cudaMalloc(&c.sk_flags, G * sizeof(unsigned)));
-      WF_CUDA(cudaMemsetAsync(c.sk_flags, 0, G * sizeof(unsigned), c.st));
-      c.sk_ws_cap = need;
+    // one workspace per stream: stream-K GEMMs on the fork/join streams may run
+    // concurrently (D product on the main stream, D_hat / R_hat coupling GEMMs on the
+    // aux streams) and must not share parked partials or flags
+    Ctx::SkState *st = nullptr;
+    for (auto &e : c.sk_states)
+      if (e.stream == c.st) st = &e;
+    if (!st) {
+      c.sk_states.push_back(Ctx::SkState{});
+      st = &c.sk_states.back();
+      st->stream = c.st;
     }
-    S.ws = c.sk_ws;
-    S.flags = c.sk_flags;
-    S.epoch = ++c.sk_epoch;
-    if (S.epoch == 0) S.epoch = ++c.sk_epoch;
+    if (st->cap < need) {
+      if (st->ws) cudaFree(st->ws);
+      if (st->flags) cudaFree(st->flags);
+      st->ws = nullptr; st->flags = nullptr; st->cap = 0;
+      WF_CUDA(cudaMalloc(&st->ws, need * 8));
+      WF_CUDA(cudaMalloc(&st->flags, G * sizeof(unsigned)));
+      WF_CUDA(cudaMemsetAsync(st->flags, 0, G * sizeof(unsigned), c.st));
+      st->cap = need;
+    }
+    S.ws = st->ws;
+    S.flags = st->flags;
+    S.epoch = 1;
     static const cudaError_t attr = cudaFuncSetAttribute(k_gemm_sk<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     WF_CUDA(attr);
     S.dp_begin = 0;

@@ -285,10 +285,9 @@ struct Ctx {
     for (auto &k : mg_key) k = nullptr;
   }
   int gemm_cls = K_GEMM;          // profiling class of the next launch_gemm
-  double *sk_ws = nullptr;        // stream-K GEMM: parked partial tiles
-  unsigned *sk_flags = nullptr;   // stream-K GEMM: per-CTA publish flags
-  size_t sk_ws_cap = 0;
-  unsigned sk_epoch = 0;
+  // stream-K GEMM: parked partial tiles and per-CTA publish flags, one set per stream
+  struct SkState { cudaStream_t stream = nullptr; double *ws = nullptr; unsigned *flags = nullptr; size_t cap = 0; };
+  std::vector<SkState> sk_states;
   Prof prof;
   std::string last_error;
   std::vector<void *> allocs;

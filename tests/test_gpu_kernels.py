@@ -139,3 +139,30 @@ def test_trsm_substitution_form():
     r = subprocess.run([sys.executable, "-c", SUBST, root], capture_output=True, text=True,
                        env=dict(os.environ, WF4DVAR_TRSM_INV="0"), timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_gemm_stream_k_concurrent_streams_and_repeats():
+    """Stream-K GEMMs on two streams at once (as the fork/join blocks of A and P run
+    them) keep separate parked partials and flags, and the consumer-reset flags make
+    back-to-back launches (and graph replays) on one stream safe."""
+    M, N, K = 1024, 2432, 256          # 304 tiles: the stream-K tail path
+    g = torch.Generator().manual_seed(21)
+    mats = []
+    for _ in range(2):
+        A = torch.randn(M, K, generator=g, dtype=torch.float64).cuda()
+        X = torch.randn(K, N, generator=g, dtype=torch.float64).cuda()
+        mats.append((A, X, A @ X))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    for rep in range(6):
+        outs = []
+        for (A, X, _), s in zip(mats, (s1, s2)):
+            Y = torch.empty(M, N, dtype=torch.float64, device="cuda")
+            with torch.cuda.stream(s):
+                L().test_gemm(A, X, Y, stream=s.cuda_stream)
+                L().test_gemm(A, X, Y, stream=s.cuda_stream)   # same stream, back to back
+            outs.append(Y)
+        torch.cuda.synchronize()
+        for (A, X, ref), Y in zip(mats, outs):
+            scale = (A.abs() @ X.abs()).max().item()
+            assert (Y - ref).abs().max().item() <= 1e-14 * scale * K ** 0.5 * 4, rep
