@@ -32,17 +32,20 @@ def main():
         b = val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")
         ms = val(r, "gpu__time_duration.sum")
         grid = int(float(r[col["launch__grid_size"]]))
-        if "k_gemm_sk" in name and cur is not None:
-            cur["dram_bytes"] += b
-            cur["ms"] += ms
-            cur["kernels"] += f" + k_gemm_sk grid {grid}"
-            calls.append(cur)
+        if "k_gemm_sk" in name:
+            if cur is not None:   # else: the tail of a call whose k_gemm was not captured
+                cur["dram_bytes"] += b
+                cur["ms"] += ms
+                cur["kernels"] += f" + k_gemm_sk grid {grid}"
+                calls.append(cur)
             cur = None
             continue
         if cur is not None:
             calls.append(cur)
         cur = dict(kernels=f"k_gemm grid {grid}", dram_bytes=b, ms=ms)
-    if cur is not None:
+    # a trailing k_gemm may still lack its stream-K tail (capture ended): drop it
+    # unless its grid is not a stream-K data-parallel part (grid % 296 != 0)
+    if cur is not None and int(cur["kernels"].split()[-1]) % 296 != 0:
         calls.append(cur)
     per = sum(c["dram_bytes"] for c in calls) / max(1, len(calls))
     json.dump({"gemm_dmma": {
