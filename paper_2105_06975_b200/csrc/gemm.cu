@@ -599,6 +599,7 @@ void register_tile_ranges(Ctx &c, const double *G, int rows, int cols, int64_t l
     covered += (double)std::min(64, rows - t * 64) * ((k.a1 - k.a0) + (k.b1 - k.b0));
   }
   if (covered > 0.75 * (double)rows * cols) return;   // not worth the bookkeeping
+  tr.coverage = covered / ((double)rows * cols);
   tr.d = c.alloc<KRange>(nt);
   WF_CUDA(memcpy_sync(c, tr.d, tr.h.data(), nt * sizeof(KRange), cudaMemcpyHostToDevice));
   c.tranges.push_back(std::move(tr));

@@ -68,6 +68,7 @@ struct TileRanges {
   const double *base = nullptr;
   int64_t ld = 0;
   int rows = 0, cols = 0;
+  double coverage = 1.0;        // covered tile area / (rows x cols)
   KRange *d = nullptr;          // device, one per 64-row tile
   std::vector<KRange> h;        // host copy (flop accounting)
 };

@@ -553,12 +553,14 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   for (int i = 0; i < nprob; ++i)
     if (probs_in[i].ncols > 0 && probs_in[i].n > 0) probs[np++] = probs_in[i];
   if (!np) return;
+  bool banded = true;   // every factor a narrow band (not just a triangle)
   for (int i = 0; i < np; ++i) {   // banded factor: its registered column ranges
     int r0 = 0, c0 = 0;
     const TileRanges *tr = (!probs[i].kr && !c.tranges.empty())
                                ? find_tile_ranges(c, probs[i].G, &r0, &c0) : nullptr;
     if (tr && r0 == 0 && c0 == 0 && tr->ld == probs[i].ldg && tr->rows >= probs[i].n)
       probs[i].kr = tr->d;
+    banded = banded && tr && tr->coverage < 0.35;
   }
   const int n = probs[0].n;
   const int blk = probs[0].blk;
@@ -586,9 +588,13 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   // from shorter panel chains: r01z measured SB = 512 4.5% faster per step there
   int total_cols = 0;
   for (int i = 0; i < np; ++i) total_cols += probs[i].ncols;
+  // a banded factor (compact-support covariance): the in-segment K loops stop at the
+  // band, so one panel walk over all rows costs no extra GEMM work and saves the
+  // coupling launches (r01at, NEXT-1 at n = 2048: 1.021 -> 0.914 ms per step)
   const int SB = sb_env > 0 ? sb_env
-                            : (n >= 4096 ? (total_cols <= 1536 ? 512 : 1024)
-                                         : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
+                 : banded ? n
+                 : (n >= 4096 ? (total_cols <= 1536 ? 512 : 1024)
+                              : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
   if (n <= SB) {
     trsm_segments(c, probs, np, upper, 0, n, n);
     return;
