@@ -591,8 +591,9 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   // a banded factor (compact-support covariance): the in-segment K loops stop at the
   // band, so one panel walk over all rows costs no extra GEMM work and saves the
   // coupling launches (r01at, NEXT-1 at n = 2048: 1.021 -> 0.914 ms per step)
+  static const int banded_sb = env_int("WF4DVAR_TRSM_BANDED_SB", 1);   // 0: size-based SB
   const int SB = sb_env > 0 ? sb_env
-                 : banded ? n
+                 : (banded && banded_sb) ? n
                  : (n >= 4096 ? (total_cols <= 1536 ? 512 : 1024)
                               : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
   if (n <= SB) {

@@ -7,7 +7,8 @@ kernels skip the zero K tiles.  Checked here: (i) applies and solves agree with 
 oracle; (ii) the skipped work is really skipped (the library's own flop counters
 drop to the band's share); (iii) the result is identical to the dense K loop
 (WF4DVAR_BANDED=0) -- the skipped terms are exact zeros and the K tiles that remain
-keep their order."""
+keep their order (at equal TRSM blocking: narrow-band factors otherwise take a single
+panel walk, which regroups the same sums)."""
 import os
 import subprocess
 import sys
@@ -114,7 +115,9 @@ np.save(sys.argv[2], np.stack(outs))
 def test_identical_to_dense_k_loop(tmp_path):
     res = {}
     for flag in ("1", "0"):
-        env = dict(os.environ, WF4DVAR_BANDED=flag)
+        # same super-block size on both sides (a narrow-band factor otherwise takes one
+        # panel walk, a different blocking of the same sums)
+        env = dict(os.environ, WF4DVAR_BANDED=flag, WF4DVAR_TRSM_BANDED_SB="0")
         out = tmp_path / f"b{flag}.npy"
         r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(out)], env=env,
                            capture_output=True, text=True, timeout=600)
