@@ -179,7 +179,7 @@ b = torch.from_numpy(prob.rhs).cuda()
 outs = []
 for _ in range(2):
     x = torch.empty_like(b)
-    ctx.solve(b, x, solver="minres", tol=0.0, maxit=40)
+    ctx.solve(b, x, solver="minres", tol=1e-300, maxit=40)
     outs.append(x.cpu().numpy())
 np.save(sys.argv[2], np.stack(outs))
 """
