@@ -244,6 +244,9 @@ struct Ctx {
   double *GR = nullptr, *GRt = nullptr;                                  // chol(R_hat base)
   double *PB = nullptr, *PBt = nullptr, *PQ = nullptr, *PQt = nullptr;  // diagonal-tile packs
   double *PR = nullptr, *PRt = nullptr;
+  // explicit inverses (G G^T)^{-1} of D_hat's blocks and of R_hat (reading A32): the
+  // preconditioner's solves become one DMMA GEMM each (nullptr: triangular solves)
+  double *IB = nullptr, *IQ = nullptr, *IR = nullptr;
   SparseFactor icB, icQ, icR;     // IC(0) factors (pc.factor == WF4DVAR_FACTOR_ICHOL)
   double *Rdiag_inv = nullptr;                                           // [p]
   std::vector<TileRanges> tranges; // registered column ranges (banded covariances / factors)

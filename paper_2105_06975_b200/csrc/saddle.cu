@@ -57,6 +57,19 @@ void dhat_inv(Ctx &c, const double *x1, double *y1) {
     c.n_Dhat_inv += c.WG;
     return;
   }
+  if (c.IQ) {   // explicit inverses: one grouped GEMM (B^-1 on window 0, Q^-1 after)
+    GemmProb g[2];
+    if (c.w0 == 0) {
+      g[0] = gp(c.IB, s, x1, ld, y1, ld, nullptr, 0, s, m, s, 1.0, 0.0);
+      g[1] = gp(c.IQ, s, x1 + m, ld, y1 + m, ld, nullptr, 0, s, (int)(ld - m), s, 1.0, 0.0);
+      launch_gemm(c, g, c.W > 1 ? 2 : 1, 1);
+    } else {
+      g[0] = gp(c.IQ, s, x1, ld, y1, ld, nullptr, 0, s, (int)ld, s, 1.0, 0.0);
+      launch_gemm(c, g, 1, 1);
+    }
+    c.n_Dhat_inv += c.WG;
+    return;
+  }
   TrsmProb f[2], b[2];
   int np;
   if (c.w0 == 0) {
@@ -86,6 +99,13 @@ void rhat_inv(Ctx &c, const double *x2, double *y2) {
   }
   if (c.pc.factor == WF4DVAR_FACTOR_ICHOL) {
     ichol_solve(c, c.icR, x2, y2, 0, (int)ld);
+    c.n_Rhat_inv += c.WG;
+    return;
+  }
+  if (c.IR) {   // explicit inverse of the R_hat base: one GEMM
+    GemmProb g = gp(c.IR, p, x2, ld, y2, ld, nullptr, 0, p, (int)ld, p, 1.0, 0.0);
+    launch_gemm(c, &g, 1, 1);
+    if (c.pc.rhat == WF4DVAR_RME) lowrank_correct(c, y2, x2);
     c.n_Rhat_inv += c.WG;
     return;
   }
@@ -337,6 +357,7 @@ void free_precond(Ctx &c) {
   dev_free(c, c.GR); dev_free(c, c.GRt); dev_free(c, c.Rdiag_inv);
   dev_free(c, c.PB); dev_free(c, c.PBt); dev_free(c, c.PQ); dev_free(c, c.PQt);
   dev_free(c, c.PR); dev_free(c, c.PRt);
+  dev_free(c, c.IB); dev_free(c, c.IQ); dev_free(c, c.IR);
   for (SparseFactor *f : {&c.icB, &c.icQ, &c.icR}) {
     int *ip[4] = {f->lrp, f->lci, f->urp, f->uci};
     for (int *q : ip) if (q) { auto it = std::find(c.allocs.begin(), c.allocs.end(), (void *)q); if (it != c.allocs.end()) c.allocs.erase(it); cudaFree(q); }
@@ -402,6 +423,40 @@ std::vector<int> algorithm1_blocks(const std::vector<double> &R, int p, const st
   return edges;
 }
 
+__global__ void k_set_identity(double *I, int n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < (int64_t)n * n) I[e] = (e / n == e % n) ? 1.0 : 0.0;
+}
+
+// Reading A32: the explicit inverse (G G^T)^{-1} = G^{-T} G^{-1} of a Cholesky factor
+// pair, by the library's own blocked TRSMs on the identity (setup, n^3 flops; the
+// block structure of an R_block factor is kept, so its inverse is block diagonal and
+// registered for zero-tile skipping).  Used for dense factors with n >= 256: the
+// preconditioner's two dependent triangular solves per apply become one DMMA GEMM
+// (configs[3]: the D_hat / R_hat solves ran at ~21 TFLOP/s as TRSM chains, the same
+// flops as a GEMM at ~32).  WF4DVAR_EXPLICIT_INV=0 keeps the triangular solves.
+static bool use_explicit_inverse(int n) {
+  static const int env = env_int("WF4DVAR_EXPLICIT_INV", 1);
+  return env && n >= 256;
+}
+
+static double *explicit_inverse(Ctx &c, const double *G, const double *Gt, const double *P,
+                                const double *Pt, int n, int blk, const std::vector<int> *segs) {
+  double *I = c.alloc<double>((size_t)n * n);
+  const int64_t nn = (int64_t)n * n;
+  k_set_identity<<<(unsigned)((nn + 255) / 256), 256, 0, c.st>>>(I, n);
+  WF_CUDA(cudaGetLastError());
+  TrsmProb f{G, n, I, n, I, n, n, n, blk};
+  TrsmProb b{Gt, n, I, n, I, n, n, n, blk};
+  f.dpack = P; b.dpack = Pt;
+  f.segs = segs; b.segs = segs;
+  launch_trsm(c, &f, 1, false);
+  launch_trsm(c, &b, 1, true);
+  WF_CUDA(cudaStreamSynchronize(c.st));
+  register_tile_ranges(c, I, n, n, n);
+  return I;
+}
+
 void setup_precond(Ctx &c) {
   const wf4dvar_precond &pc = c.pc;
   const int s = c.s, p = c.p;
@@ -449,6 +504,10 @@ void setup_precond(Ctx &c) {
     c.PBt = make_diag_pack(c, c.GBt, s, true);
     c.PQ = make_diag_pack(c, c.GQ, s, false);
     c.PQt = make_diag_pack(c, c.GQt, s, true);
+    if (use_explicit_inverse(s)) {
+      c.IB = explicit_inverse(c, c.GB, c.GBt, c.PB, c.PBt, s, 0, nullptr);
+      c.IQ = explicit_inverse(c, c.GQ, c.GQt, c.PQ, c.PQt, s, 0, nullptr);
+    }
   }
   // ---- R_hat
   std::vector<double> Rh((size_t)p * p);
@@ -568,6 +627,12 @@ void setup_precond(Ctx &c) {
     chol(c, sv, Rdev, p, c.GR, c.GRt, name);
     c.PR = make_diag_pack(c, c.GR, p, false);
     c.PRt = make_diag_pack(c, c.GRt, p, true);
+    if (use_explicit_inverse(p)) {
+      const bool seg = pc.rhat == WF4DVAR_RBLOCK && !c.rblk_starts.empty();
+      c.IR = explicit_inverse(c, c.GR, c.GRt, c.PR, c.PRt, p,
+                              pc.rhat == WF4DVAR_RBLOCK ? pc.block : 0,
+                              seg ? &c.rblk_starts : nullptr);
+    }
   } catch (...) { cudaFree(Rdev); throw; }
   cudaFree(Rdev);
 }
