@@ -1,18 +1,26 @@
 // Cholesky-factor triangular solves for D_hat^{-1} and R_hat^{-1} (
-// R_hat^{-1} "using the ... Cholesky factors").
+// R_hat^{-1} "using the ... Cholesky factors").  Dense blocks with n >= 256
+// are applied through setup-time explicit inverses (reading A32, saddle.cu), which
+// these solves compute; the solves themselves serve banded / IC(0) factors, small
+// blocks, R_block segments and WF4DVAR_EXPLICIT_INV=0.
 //
 // Blocked right-looking TRSM, B200 layout:
-//   * the triangle is cut into diagonal super-blocks of SB rows;
+//   * the triangle is cut into diagonal super-blocks of SB rows (a narrow-band
+//     factor: one super-block);
 //   * each super-block is solved by k_trsm: one CTA per NB-column panel walks
 //     the 64-row tiles of the super-block,
-//         T_i = X_i - sum_{j<i, j in block} G_ij Y_j    (DMMA tile GEMM)
-//         Y_i = G_ii^{-1} T_i                           (exact substitution,
-//                                                         one warp per column group)
+//         T_i = X_i - sum_{j<i, j in block} G_ij Y_j    (DMMA tile GEMM, K tiles
+//                                                         outside a band skipped)
+//         Y_i = G_ii^{-1} T_i                           (default: one DMMA product
+//                                                         with the setup-time inverse
+//                                                         tile, reading A31; else exact
+//                                                         shuffle substitution)
 //   * the coupling of the solved super-block to all remaining rows is one large
 //     DMMA GEMM  Y_rest -= G_rest,blk Y_blk  (gemm.cu), which is where almost
 //     all the FLOPs go.
-// R_block (Alg. 1 with uniform blocks) has a block-diagonal factor: every
-// diagonal block is an independent segment (grid.y), no GEMM coupling.
+// R_block (Alg. 1) has a block-diagonal factor: every diagonal block is an
+// independent segment (grid.y), no GEMM coupling.  Segments of <= 64 rows take the
+// thread-per-column k_trsm_small.
 #include <algorithm>
 #include <cstdlib>
 #include <type_traits>
