@@ -246,6 +246,7 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   for (auto &e : c.sk_states) {
     if (e.ws) cudaFree(e.ws);
     if (e.flags) cudaFree(e.flags);
+    if (e.splitk) cudaFree(e.splitk);
   }
   for (void *p : c.allocs) cudaFree(p);
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }

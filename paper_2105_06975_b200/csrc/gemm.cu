@@ -550,6 +550,112 @@ static void run_small(Ctx &c, const GemmProb *probs, int nprob, int batch, int m
   WF_CUDA(cudaGetLastError());
 }
 
+// ---- split-K for GEMMs with too few tiles to fill the GPU (configs[1]: 1000 x 336 x
+// 1000 is 48 tiles of 64x128 on 148 SMs).  Split z of S runs the K range
+// [z kc, (z+1) kc) of every tile and parks its 64x128 partial in a per-stream
+// workspace; the reduction adds the S partials in a fixed order and applies the
+// epilogue (deterministic, no atomics, graph-replay safe).
+template <class C, bool V16>
+__global__ void __launch_bounds__(C::NT) k_gemm_splitk(const GemmLaunch L, double *ws, int kc) {
+  extern __shared__ __align__(16) double smem[];
+  const int tiles = gridDim.x, tile = blockIdx.x, z = blockIdx.z;
+  int gi, m0, n0;
+  tile_coords<C>(L, tile, gi, m0, n0);
+  const GemmProb &P = L.p[gi];
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int kb = z * kc, ke = min(P.K, kb + kc);
+  if (ke > kb)
+    tile_mainloop<C, V16>(smem, acc, P.A, P.lda, P.X, P.ldx, m0, n0, kb, ke, P.M, P.N);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+  double *slot = ws + ((int64_t)z * tiles + tile) * (C::BM * C::BN);
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) {
+      const int rr = wm * C::WM + i * 8 + g, cc = wn * C::WN + j * 8 + 2 * t;
+      *reinterpret_cast<double2 *>(slot + rr * C::BN + cc) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+template <class C>
+__global__ void k_gemm_splitk_reduce(const GemmLaunch L, const double *ws, int tiles, int S) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)tiles * C::BM * C::BN) return;
+  const int tile = (int)(e / (C::BM * C::BN));
+  const int loc = (int)(e % (C::BM * C::BN));
+  int gi, m0, n0;
+  tile_coords<C>(L, tile, gi, m0, n0);
+  const GemmProb &P = L.p[gi];
+  const int row = m0 + loc / C::BN, col = n0 + loc % C::BN;
+  if (row >= P.M || col >= P.N) return;
+  double sum = 0.0;
+  for (int z = 0; z < S; ++z) sum += ws[((int64_t)z * tiles + tile) * (C::BM * C::BN) + loc];
+  double v = P.alpha * sum;
+  if (P.Z) v += P.beta * P.Z[(int64_t)(P.zrow ? P.zrow[row] : row) * P.ldz + col];
+  P.Y[(int64_t)row * P.ldy + col] = v;
+}
+
+// true if launched (S >= 2 splits fit); the caller falls back to the tile configs
+template <class C>
+static bool run_splitk(Ctx &c, const GemmProb *probs, int nprob, bool v16) {
+  static const int env = env_int("WF4DVAR_GEMM_SPLITK", 1);   // 0 disables
+  if (!env) return false;
+  GemmLaunch L{};
+  int tiles = 0, kmax = 0;
+  for (int i = 0; i < nprob; ++i) {
+    L.p[i] = probs[i];
+    if (probs[i].kr) return false;
+    const int t = tiles_of<C>(probs[i], L.tm[i], L.tn[i]);
+    if (i == 0) L.tiles0 = t;
+    tiles += t;
+    kmax = std::max(kmax, probs[i].K);
+  }
+  if (nprob == 1) L.tiles0 = tiles;
+  L.gm = 1;
+  const int G = 2 * 148;
+  // S splits of >= 8 k-steps each, S x tiles <= one wave of resident CTAs
+  int S = std::min(G / std::max(1, tiles), kmax / (8 * C::BK));
+  if (S < 2) return false;
+  const int nk = (kmax + C::BK - 1) / C::BK;
+  const int kc = ((nk + S - 1) / S) * C::BK;
+  S = (kmax + kc - 1) / kc;
+  if (S < 2) return false;
+  Ctx::SkState *st = nullptr;
+  for (auto &e : c.sk_states)
+    if (e.stream == c.st) st = &e;
+  if (!st) {
+    c.sk_states.push_back(Ctx::SkState{});
+    st = &c.sk_states.back();
+    st->stream = c.st;
+  }
+  const size_t need = (size_t)S * tiles * C::BM * C::BN;
+  if (st->splitk_cap < need) {
+    if (st->splitk) cudaFree(st->splitk);
+    st->splitk = nullptr;
+    st->splitk_cap = 0;
+    WF_CUDA(cudaMalloc(&st->splitk, need * 8));
+    st->splitk_cap = need;
+  }
+  const size_t smem = C::SMEM_DOUBLES * sizeof(double);
+  auto kern = v16 ? k_gemm_splitk<C, true> : k_gemm_splitk<C, false>;
+  static const cudaError_t a1 = cudaFuncSetAttribute(k_gemm_splitk<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static const cudaError_t a2 = cudaFuncSetAttribute(k_gemm_splitk<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  WF_CUDA(v16 ? a1 : a2);
+  kern<<<dim3(tiles, 1, S), C::NT, smem, c.st>>>(L, st->splitk, kc);
+  WF_CUDA(cudaGetLastError());
+  const int64_t nel = (int64_t)tiles * C::BM * C::BN;
+  k_gemm_splitk_reduce<C><<<(unsigned)((nel + 255) / 256), 256, 0, c.st>>>(L, st->splitk, tiles, S);
+  WF_CUDA(cudaGetLastError());
+  c.launches++;
+  return true;
+}
+
 // ---- tile column ranges (banded covariances and factors)
 // flag[t][j] = 1 iff G[64 t : 64 t + 64, 16 j : 16 j + 16] has a non-zero
 __global__ void k_tile_mask(const double *G, int64_t ld, int rows, int cols, unsigned char *flag) {
@@ -703,6 +809,7 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
     else if (force == 10) run<TileCfg<64, 128, 32, 32, 64, 2>>(c, ps, valid, batch, v16);
     else run<CfgHuge>(c, ps, valid, batch, v16);
   } else if (huge_tiles * batch >= 2 * 148) run<CfgHuge>(c, ps, valid, batch, v16);
+  else if (batch == 1 && huge_tiles < 148 && run_splitk<CfgHuge>(c, ps, valid, v16)) {}
   else if (big_tiles * batch >= 148) run<CfgBig>(c, ps, valid, batch, v16);
   else run<CfgSmall>(c, ps, valid, batch, v16);
   c.launches++;

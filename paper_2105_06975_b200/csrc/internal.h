@@ -290,7 +290,10 @@ struct Ctx {
   }
   int gemm_cls = K_GEMM;          // profiling class of the next launch_gemm
   // stream-K GEMM: parked partial tiles and per-CTA publish flags, one set per stream
-  struct SkState { cudaStream_t stream = nullptr; double *ws = nullptr; unsigned *flags = nullptr; size_t cap = 0; };
+  struct SkState {
+    cudaStream_t stream = nullptr; double *ws = nullptr; unsigned *flags = nullptr; size_t cap = 0;
+    double *splitk = nullptr; size_t splitk_cap = 0;   // split-K partial tiles
+  };
   std::vector<SkState> sk_states;
   Prof prof;
   std::string last_error;

@@ -203,3 +203,35 @@ def test_stream_k_inside_captured_graphs(tmp_path):
         res[graphs] = np.load(out)
     assert np.array_equal(res["1"][0], res["1"][1])   # replays are deterministic
     assert np.array_equal(res["1"][0], res["0"][0])   # and equal to eager launches
+
+
+@pytest.mark.parametrize("M,N,K", [(1000, 336, 1000), (500, 336, 500), (64, 8128, 512)])
+def test_gemm_split_k_concurrent_streams(M, N, K):
+    """Too few 64x128 tiles to fill the GPU (48, 24, 64): split-K with per-stream
+    partial workspaces and a fixed-order reduction -- same tolerance as the tile
+    kernel, bitwise reproducible, and independent launches on two streams at once."""
+    g = torch.Generator().manual_seed(M + N + K)
+    mats = []
+    for _ in range(2):
+        A = torch.randn(M, K, generator=g, dtype=torch.float64).cuda()
+        X = torch.randn(K, N, generator=g, dtype=torch.float64).cuda()
+        Z = torch.randn(M, N, generator=g, dtype=torch.float64).cuda()
+        mats.append((A, X, Z, 0.75 * (A @ X) - 2.0 * Z))
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    first = None
+    for rep in range(4):
+        outs = []
+        for (A, X, Z, _), s in zip(mats, (s1, s2)):
+            Y = torch.empty(M, N, dtype=torch.float64, device="cuda")
+            with torch.cuda.stream(s):
+                L().test_gemm(A, X, Y, alpha=0.75, beta=-2.0, Z=Z, stream=s.cuda_stream)
+            outs.append(Y)
+        torch.cuda.synchronize()
+        for (A, X, Z, ref), Y in zip(mats, outs):
+            scale = (A.abs() @ X.abs()).max().item() + 1.0
+            assert (Y - ref).abs().max().item() <= 1e-14 * scale * K ** 0.5 * 4, rep
+        if first is None:
+            first = [o.clone() for o in outs]
+        else:
+            assert all(torch.equal(a, b) for a, b in zip(first, outs))
