@@ -604,7 +604,10 @@ __global__ void k_gemm_splitk_reduce(const GemmLaunch L, const double *ws, int t
 // true if launched (S >= 2 splits fit); the caller falls back to the tile configs
 template <class C>
 static bool run_splitk(Ctx &c, const GemmProb *probs, int nprob, bool v16) {
-  static const int env = env_int("WF4DVAR_GEMM_SPLITK", 1);   // 0 disables
+  // opt-in: r01bd measured 1000 x 320 x 1000 alone 10.5 -> 12.2 TFLOP/s, but configs[1]'s
+  // step 0.318 -> 0.365 ms -- its small GEMMs already overlap on the fork/join streams,
+  // and the split grids crowd out the concurrent blocks (NEXT-1: 0.898 -> 0.889 ms)
+  static const int env = env_int("WF4DVAR_GEMM_SPLITK", 0);
   if (!env) return false;
   GemmLaunch L{};
   int tiles = 0, kmax = 0;

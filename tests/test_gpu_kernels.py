@@ -207,9 +207,10 @@ def test_stream_k_inside_captured_graphs(tmp_path):
 
 @pytest.mark.parametrize("M,N,K", [(1000, 336, 1000), (500, 336, 500), (64, 8128, 512)])
 def test_gemm_split_k_concurrent_streams(M, N, K):
-    """Too few 64x128 tiles to fill the GPU (48, 24, 64): split-K with per-stream
-    partial workspaces and a fixed-order reduction -- same tolerance as the tile
-    kernel, bitwise reproducible, and independent launches on two streams at once."""
+    """Too few 64x128 tiles to fill the GPU (48, 24, 64): the tile-config fallback by
+    default, split-K (per-stream partial workspaces, fixed-order reduction) with
+    WF4DVAR_GEMM_SPLITK=1 -- same tolerance, bitwise reproducible, and independent
+    launches on two streams at once (the split-K path: test_gemm_split_k_opt_in)."""
     g = torch.Generator().manual_seed(M + N + K)
     mats = []
     for _ in range(2):
@@ -235,3 +236,34 @@ def test_gemm_split_k_concurrent_streams(M, N, K):
             first = [o.clone() for o in outs]
         else:
             assert all(torch.equal(a, b) for a, b in zip(first, outs))
+
+
+SPLITK = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2105_06975_b200 import _lib
+g = torch.Generator().manual_seed(9)
+for (M, N, K) in ((1000, 336, 1000), (500, 336, 500), (64, 8128, 512), (300, 517, 700)):
+    A = torch.randn(M, K, generator=g, dtype=torch.float64).cuda()
+    X = torch.randn(K, N, generator=g, dtype=torch.float64).cuda()
+    Z = torch.randn(M, N, generator=g, dtype=torch.float64).cuda()
+    Y = torch.empty(M, N, dtype=torch.float64, device="cuda")
+    _lib.test_gemm(A, X, Y, alpha=0.5, beta=1.5, Z=Z)
+    Y2 = torch.empty_like(Y)
+    _lib.test_gemm(A, X, Y2, alpha=0.5, beta=1.5, Z=Z)
+    ref = 0.5 * (A @ X) + 1.5 * Z
+    scale = (A.abs() @ X.abs()).max().item() + 1.0
+    assert (Y - ref).abs().max().item() <= 1e-14 * scale * K ** 0.5 * 4, (M, N, K)
+    assert torch.equal(Y, Y2)
+print("ok")
+"""
+
+
+def test_gemm_split_k_opt_in():
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", SPLITK, root], capture_output=True, text=True,
+                       env=dict(os.environ, WF4DVAR_GEMM_SPLITK="1"), timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
