@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace wf {
@@ -327,12 +329,19 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
                                                       transpose ? c.halo_hi : c.halo_lo, c.w0,
                                                       c.WG);
   } else {
-    constexpr int TI = 32;
-    dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
-    k_heat_iir<H, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_rho,
-                                              sign * c.heat_gain, c.s, c.W, c.m, w_first, w_step,
-                                              nw, transpose ? 1 : -1,
-                                              transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+    static const int ti_env = env_int("WF4DVAR_HEAT_TI", 32);   // tuning experiments only
+    auto go = [&](auto ti_tag) {
+      constexpr int TI = decltype(ti_tag)::value;
+      dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
+      k_heat_iir<H, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_rho,
+                                                sign * c.heat_gain, c.s, c.W, c.m, w_first,
+                                                w_step, nw, transpose ? 1 : -1,
+                                                transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+    };
+    if (ti_env == 16) go(std::integral_constant<int, 16>{});
+    else if (ti_env == 64) go(std::integral_constant<int, 64>{});
+    else if (ti_env == 48) go(std::integral_constant<int, 48>{});
+    else go(std::integral_constant<int, 32>{});
   }
   WF_CUDA(cudaGetLastError());
 }
