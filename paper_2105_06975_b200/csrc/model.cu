@@ -339,6 +339,7 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
                                                 transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
     };
     if (ti_env == 16) go(std::integral_constant<int, 16>{});
+    else if (ti_env == 8) go(std::integral_constant<int, 8>{});
     else if (ti_env == 64) go(std::integral_constant<int, 64>{});
     else if (ti_env == 48) go(std::integral_constant<int, 48>{});
     else go(std::integral_constant<int, 32>{});
