@@ -329,7 +329,11 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
                                                       transpose ? c.halo_hi : c.halo_lo, c.w0,
                                                       c.WG);
   } else {
-    static const int ti_env = env_int("WF4DVAR_HEAT_TI", 32);   // tuning experiments only
+    // rows per thread: r01bf/bg per step, TI = 32 / 16 / 8: c3 30.39 / 30.09 / 30.03 ms,
+    // c1 0.318 / 0.290 / 0.276 ms, c0 0.151 / 0.137 / 0.128 ms -- the recursions are
+    // latency-bound chains; shorter chunks (the H-row warm-ups re-read from L2) give
+    // more independent chains and fewer registers (higher occupancy)
+    static const int ti_env = env_int("WF4DVAR_HEAT_TI", 8);   // tuning experiments only
     auto go = [&](auto ti_tag) {
       constexpr int TI = decltype(ti_tag)::value;
       dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
@@ -339,10 +343,10 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
                                                 transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
     };
     if (ti_env == 16) go(std::integral_constant<int, 16>{});
-    else if (ti_env == 8) go(std::integral_constant<int, 8>{});
     else if (ti_env == 64) go(std::integral_constant<int, 64>{});
     else if (ti_env == 48) go(std::integral_constant<int, 48>{});
-    else go(std::integral_constant<int, 32>{});
+    else if (ti_env == 32) go(std::integral_constant<int, 32>{});
+    else go(std::integral_constant<int, 8>{});
   }
   WF_CUDA(cudaGetLastError());
 }
