@@ -204,13 +204,20 @@ template <int NS>
 static void heat_explicit_launch(Ctx &c, bool transpose, double sign, const double *in,
                                  const double *base, double *out, int w_first, int w_step,
                                  int nw, const double *add2, const int *row_map) {
-  constexpr int TI = 32;
+  static const int ti_env = env_int("WF4DVAR_HEAT_EXPL_TI", 32);   // tuning experiments only
   int cols = nw * c.m;
-  dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
-  k_heat_explicit<NS, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_r, sign,
-                                                   c.s, c.W, c.m, w_first, w_step, nw,
-                                                   transpose ? 1 : -1,
-                                                   transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+  auto go = [&](auto ti_tag) {
+    constexpr int TI = decltype(ti_tag)::value;
+    dim3 grid((cols + 127) / 128, (c.s + TI - 1) / TI);
+    k_heat_explicit<NS, TI><<<grid, 128, 0, c.st>>>(out, base, in, add2, row_map, c.heat_r,
+                                                     sign, c.s, c.W, c.m, w_first, w_step, nw,
+                                                     transpose ? 1 : -1,
+                                                     transpose ? c.halo_hi : c.halo_lo, c.w0,
+                                                     c.WG);
+  };
+  if (ti_env == 8) go(std::integral_constant<int, 8>{});
+  else if (ti_env == 16) go(std::integral_constant<int, 16>{});
+  else go(std::integral_constant<int, 32>{});
   WF_CUDA(cudaGetLastError());
 }
 
