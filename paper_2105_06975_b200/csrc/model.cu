@@ -204,7 +204,8 @@ template <int NS>
 static void heat_explicit_launch(Ctx &c, bool transpose, double sign, const double *in,
                                  const double *base, double *out, int w_first, int w_step,
                                  int nw, const double *add2, const int *row_map) {
-  static const int ti_env = env_int("WF4DVAR_HEAT_EXPL_TI", 32);   // tuning experiments only
+  // r01bh, NEXT-1 per step: TI = 32 / 16 / 8 -> 0.901 / 0.887 / 0.876 ms
+  static const int ti_env = env_int("WF4DVAR_HEAT_EXPL_TI", 8);   // tuning experiments only
   int cols = nw * c.m;
   auto go = [&](auto ti_tag) {
     constexpr int TI = decltype(ti_tag)::value;
@@ -215,9 +216,9 @@ static void heat_explicit_launch(Ctx &c, bool transpose, double sign, const doub
                                                      transpose ? c.halo_hi : c.halo_lo, c.w0,
                                                      c.WG);
   };
-  if (ti_env == 8) go(std::integral_constant<int, 8>{});
+  if (ti_env == 32) go(std::integral_constant<int, 32>{});
   else if (ti_env == 16) go(std::integral_constant<int, 16>{});
-  else go(std::integral_constant<int, 32>{});
+  else go(std::integral_constant<int, 8>{});
   WF_CUDA(cudaGetLastError());
 }
 
