@@ -131,6 +131,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
     WF_CUDA(cudaStreamCreateWithFlags(&c.cpy, cudaStreamNonBlocking));
     for (auto &e : c.ev_in) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &e : c.ev_chunk) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c.s = p.s; c.p = p.p; c.N = p.N; c.WG = p.N + 1; c.m = p.m; c.model = p.model;
     int wb = 0, we = c.WG;
     wf::partition(c.WG, world, rank, &wb, &we);
@@ -239,6 +240,7 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.cpy) { cudaStreamSynchronize(c.cpy); cudaStreamDestroy(c.cpy); }
   for (auto &e : c.ev_in) if (e) cudaEventDestroy(e);
+  for (auto &e : c.ev_chunk) if (e) cudaEventDestroy(e);
   c.drop_graphs();
   if (c.own_st) { cudaStreamSynchronize(c.own_st); cudaStreamDestroy(c.own_st); }
   delete c.comm;

@@ -218,6 +218,7 @@ struct Ctx {
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   cudaStream_t cpy = nullptr;          // host path: block-wise H2D of apply_P's input
   cudaEvent_t ev_in[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_chunk[4] = {nullptr, nullptr, nullptr, nullptr};   // host path column chunks
   bool aux_priority = true;       // env WF4DVAR_AUX_PRIORITY=0 disables (experiments)
   int device = 0;
   // device data

@@ -28,21 +28,45 @@ static GemmProb gp(const double *A, int64_t lda, const double *X, int64_t ldx, d
   return g;
 }
 
+// Y = alpha * Dblk X + beta * Z on the segment columns [c0, c1): the window-0 block
+// (B, or its inverse) on this rank's window-0 columns, the Q block elsewhere.
+static void d_gemm_cols(Ctx &c, const double *Bm, const double *Qm, const double *X, double *Y,
+                        const double *Z, double alpha, double beta, int64_t c0, int64_t c1) {
+  const int s = c.s;
+  const int64_t ld = c.ncol;
+  const int64_t bsplit = (c.w0 == 0) ? c.m : 0;   // columns < bsplit belong to window 0
+  GemmProb g[2];
+  int np = 0;
+  if (c0 < bsplit) {
+    const int64_t e = std::min(c1, bsplit);
+    g[np++] = gp(Bm, s, X + c0, ld, Y + c0, ld, Z ? Z + c0 : nullptr, ld, s, (int)(e - c0), s,
+                 alpha, beta);
+  }
+  const int64_t q0 = std::max(c0, bsplit);
+  if (c1 > q0)
+    g[np++] = gp(Qm, s, X + q0, ld, Y + q0, ld, Z ? Z + q0 : nullptr, ld, s, (int)(c1 - q0), s,
+                 alpha, beta);
+  launch_gemm(c, g, np, 1);
+}
+
 // Y = alpha * D X + beta * Z over an s x (W m) segment: B on window-0 columns, Q elsewhere.
 static void d_product(Ctx &c, const double *X, double *Y, const double *Z, double alpha,
                       double beta) {
-  const int s = c.s, m = c.m;
-  const int64_t ld = c.ncol;
-  GemmProb g[2];
-  if (c.w0 == 0) {   // this rank owns window 0 (B); Q on the rest
-    g[0] = gp(c.B, s, X, ld, Y, ld, Z, ld, s, m, s, alpha, beta);
-    g[1] = gp(c.Q, s, X + m, ld, Y + m, ld, Z ? Z + m : nullptr, ld, s, (int)(ld - m), s, alpha, beta);
-    launch_gemm(c, g, c.W > 1 ? 2 : 1, 1);
-  } else {
-    g[0] = gp(c.Q, s, X, ld, Y, ld, Z, ld, s, (int)ld, s, alpha, beta);
-    launch_gemm(c, g, 1, 1);
-  }
+  d_gemm_cols(c, c.B, c.Q, X, Y, Z, alpha, beta, 0, c.ncol);
   c.n_D += c.WG;
+}
+
+// Host path: the segment's columns in kHostChunks window-aligned chunks, so the first
+// block's copies and products pipeline (chunk k's product runs while chunk k+1 is on
+// the link).
+constexpr int kHostChunks = 4;
+static void host_chunks(const Ctx &c, int64_t *bounds) {
+  const int64_t ld = c.ncol, m = c.m;
+  for (int k = 0; k <= kHostChunks; ++k) {
+    int64_t b = (ld * k / kHostChunks + m - 1) / m * m;   // window-aligned
+    bounds[k] = std::min(ld, b);
+  }
+  bounds[kHostChunks] = ld;
 }
 
 void dhat_inv(Ctx &c, const double *x1, double *y1) {
@@ -58,15 +82,7 @@ void dhat_inv(Ctx &c, const double *x1, double *y1) {
     return;
   }
   if (c.IQ) {   // explicit inverses: one grouped GEMM (B^-1 on window 0, Q^-1 after)
-    GemmProb g[2];
-    if (c.w0 == 0) {
-      g[0] = gp(c.IB, s, x1, ld, y1, ld, nullptr, 0, s, m, s, 1.0, 0.0);
-      g[1] = gp(c.IQ, s, x1 + m, ld, y1 + m, ld, nullptr, 0, s, (int)(ld - m), s, 1.0, 0.0);
-      launch_gemm(c, g, c.W > 1 ? 2 : 1, 1);
-    } else {
-      g[0] = gp(c.IQ, s, x1, ld, y1, ld, nullptr, 0, s, (int)ld, s, 1.0, 0.0);
-      launch_gemm(c, g, 1, 1);
-    }
+    d_gemm_cols(c, c.IB, c.IQ, x1, y1, nullptr, 1.0, 0.0, 0, ld);
     c.n_Dhat_inv += c.WG;
     return;
   }
@@ -201,9 +217,26 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
   }
   // c1 = L x3 + D x1
   model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
-  d_product(c, x1, y1, y1, 1.0, 1.0);
-  if (host_y)
-    WF_CUDA(cudaMemcpyAsync(host_y, y1, (size_t)s * ld * 8, cudaMemcpyDeviceToHost, c.st));
+  if (host_y) {
+    // column chunks: each chunk leaves for the host while the next one's product runs
+    int64_t cb[kHostChunks + 1];
+    host_chunks(c, cb);
+    // (the copies go on the copy stream: in stream order they would hold back the next
+    // chunk's product)
+    for (int k = 0; k < kHostChunks; ++k) {
+      if (cb[k + 1] <= cb[k]) continue;
+      d_gemm_cols(c, c.B, c.Q, x1, y1, y1, 1.0, 1.0, cb[k], cb[k + 1]);
+      WF_CUDA(cudaEventRecord(c.ev_chunk[k], c.st));
+      WF_CUDA(cudaStreamWaitEvent(c.cpy, c.ev_chunk[k], 0));
+      WF_CUDA(cudaMemcpy2DAsync(host_y + cb[k], ld * 8, y1 + cb[k], ld * 8,
+                                (cb[k + 1] - cb[k]) * 8, s, cudaMemcpyDeviceToHost, c.cpy));
+    }
+    WF_CUDA(cudaEventRecord(c.ev_in[3], c.cpy));
+    WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_in[3], 0));
+    c.n_D += c.WG;
+  } else {
+    d_product(c, x1, y1, y1, 1.0, 1.0);
+  }
   join(c);
   c.n_R += c.WG;
   c.n_M += 2 * c.N;
@@ -220,12 +253,28 @@ void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
   auto wait_in = [&](int b) {
     if (host_x) WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_in[b], 0));
   };
+  // explicit D_hat inverses (P_D): the first block is copied and multiplied in column
+  // chunks (ev_chunk[k]), so the GEMM starts after a quarter of the block has landed
+  const bool chunked = host_x && c.IQ && c.pc.shape == WF4DVAR_PD;
+  int64_t cb[kHostChunks + 1];
+  if (chunked) host_chunks(c, cb);
   if (host_x) {
     WF_CUDA(cudaEventRecord(c.ev_in[3], c.st));
     WF_CUDA(cudaStreamWaitEvent(c.cpy, c.ev_in[3], 0));
     const int64_t off[3] = {0, (int64_t)(s + p) * ld, (int64_t)s * ld};
     const int64_t len[3] = {(int64_t)s * ld, (int64_t)s * ld, (int64_t)p * ld};
     for (int b = 0; b < 3; ++b) {
+      if (b == 0 && chunked) {
+        for (int k = 0; k < kHostChunks; ++k) {
+          if (cb[k + 1] > cb[k])
+            WF_CUDA(cudaMemcpy2DAsync(const_cast<double *>(x) + cb[k], ld * 8, host_x + cb[k],
+                                      ld * 8, (cb[k + 1] - cb[k]) * 8, s,
+                                      cudaMemcpyHostToDevice, c.cpy));
+          WF_CUDA(cudaEventRecord(c.ev_chunk[k], c.cpy));
+        }
+        WF_CUDA(cudaEventRecord(c.ev_in[0], c.cpy));
+        continue;
+      }
       WF_CUDA(cudaMemcpyAsync(const_cast<double *>(x) + off[b], host_x + off[b], len[b] * 8,
                               cudaMemcpyHostToDevice, c.cpy));
       WF_CUDA(cudaEventRecord(c.ev_in[b], c.cpy));
@@ -241,8 +290,16 @@ void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
     }
     {
       OnStream os(c, c.aux[1]);
-      wait_in(0);
-      dhat_inv(c, x1, y1);                     // latency-bound TRSM chain: priority stream
+      if (chunked) {
+        for (int k = 0; k < kHostChunks; ++k) {
+          WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_chunk[k], 0));
+          if (cb[k + 1] > cb[k]) d_gemm_cols(c, c.IB, c.IQ, x1, y1, nullptr, 1.0, 0.0, cb[k], cb[k + 1]);
+        }
+        c.n_Dhat_inv += c.WG;
+      } else {
+        wait_in(0);
+        dhat_inv(c, x1, y1);                   // latency-bound TRSM chain: priority stream
+      }
     }
     double *t = c.ws_seg;
     wait_in(1);
