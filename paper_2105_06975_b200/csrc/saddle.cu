@@ -60,6 +60,9 @@ static void d_product(Ctx &c, const double *X, double *Y, const double *Z, doubl
 // block's copies and products pipeline (chunk k's product runs while chunk k+1 is on
 // the link).
 constexpr int kHostChunks = 4;
+// only worth it when a block's copy is long against the per-chunk launch latencies
+// (configs[3]: 268 MB per block, 4.9 ms over PCIe; configs[1]: 2.7 MB)
+static bool host_chunking(const Ctx &c) { return (double)c.s * c.ncol * 8 >= 64e6; }
 static void host_chunks(const Ctx &c, int64_t *bounds) {
   const int64_t ld = c.ncol, m = c.m;
   for (int k = 0; k <= kHostChunks; ++k) {
@@ -217,7 +220,7 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
   }
   // c1 = L x3 + D x1
   model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
-  if (host_y) {
+  if (host_y && host_chunking(c)) {
     // column chunks: each chunk leaves for the host while the next one's product runs
     int64_t cb[kHostChunks + 1];
     host_chunks(c, cb);
@@ -236,6 +239,8 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
     c.n_D += c.WG;
   } else {
     d_product(c, x1, y1, y1, 1.0, 1.0);
+    if (host_y)
+      WF_CUDA(cudaMemcpyAsync(host_y, y1, (size_t)s * ld * 8, cudaMemcpyDeviceToHost, c.st));
   }
   join(c);
   c.n_R += c.WG;
@@ -255,7 +260,7 @@ void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
   };
   // explicit D_hat inverses (P_D): the first block is copied and multiplied in column
   // chunks (ev_chunk[k]), so the GEMM starts after a quarter of the block has landed
-  const bool chunked = host_x && c.IQ && c.pc.shape == WF4DVAR_PD;
+  const bool chunked = host_x && c.IQ && c.pc.shape == WF4DVAR_PD && host_chunking(c);
   int64_t cb[kHostChunks + 1];
   if (chunked) host_chunks(c, cb);
   if (host_x) {
