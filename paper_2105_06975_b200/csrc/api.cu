@@ -118,6 +118,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
     }
     WF_CUDA(cudaSetDevice(c.device));
     if (const char *e = getenv("WF4DVAR_AUX_PRIORITY")) c.aux_priority = atoi(e) != 0;
+    if (const char *e = getenv("WF4DVAR_FORK")) c.fork_on = atoi(e) != 0;
     for (int i = 0; i < 2; ++i) {
       // the aux streams carry the latency-bound triangular solves (D_hat^{-1},
       // R_hat^{-1}): highest priority, so their CTAs take SM slots as soon as

@@ -220,6 +220,7 @@ struct Ctx {
   cudaEvent_t ev_in[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_chunk[4] = {nullptr, nullptr, nullptr, nullptr};   // host path column chunks
   bool aux_priority = true;       // env WF4DVAR_AUX_PRIORITY=0 disables (experiments)
+  bool fork_on = true;            // fork/join concurrency of the operator blocks
   int device = 0;
   // device data
   double *B = nullptr, *Q = nullptr, *R = nullptr;
@@ -360,7 +361,7 @@ inline cudaError_t memcpy_sync(Ctx &c, void *dst, const void *src, size_t bytes,
 // concurrently running kernels would overlap and misstate each kernel's rate.
 struct OnStream {
   Ctx &c; cudaStream_t saved;
-  OnStream(Ctx &c_, cudaStream_t s) : c(c_), saved(c_.st) { if (!c.prof.on) c.st = s; }
+  OnStream(Ctx &c_, cudaStream_t s) : c(c_), saved(c_.st) { if (!c.prof.on && c.fork_on) c.st = s; }
   ~OnStream() { c.st = saved; }
 };
 void fork(Ctx &c);   // aux streams wait for the work enqueued so far on c.st

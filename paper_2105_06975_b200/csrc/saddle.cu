@@ -152,13 +152,13 @@ static int n_model_blocks(const Ctx &c) {
 }
 
 void fork(Ctx &c) {
-  if (c.prof.on) return;   // serialised while profiling (see OnStream)
+  if (c.prof.on || !c.fork_on) return;   // serialised while profiling (see OnStream)
   WF_CUDA(cudaEventRecord(c.ev_fork, c.st));
   for (int i = 0; i < 2; ++i) WF_CUDA(cudaStreamWaitEvent(c.aux[i], c.ev_fork, 0));
 }
 
 void join(Ctx &c) {
-  if (c.prof.on) return;
+  if (c.prof.on || !c.fork_on) return;
   for (int i = 0; i < 2; ++i) {
     WF_CUDA(cudaEventRecord(c.ev_join[i], c.aux[i]));
     WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_join[i], 0));
