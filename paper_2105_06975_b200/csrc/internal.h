@@ -285,10 +285,12 @@ struct Ctx {
   Counters mg_delta[6];
   const void *mg_key[4] = {nullptr, nullptr, nullptr, nullptr};
   double mg_tol = -1, mg_mark = -1;
+  bool mg_warm = false;            // an eager MINRES iteration ran since the last drop
   void drop_graphs() {
     for (auto &e : mg_exec)
       if (e) { cudaGraphExecDestroy(e); e = nullptr; }
     for (auto &k : mg_key) k = nullptr;
+    mg_warm = false;
   }
   int gemm_cls = K_GEMM;          // profiling class of the next launch_gemm
   // stream-K GEMM: parked partial tiles and per-CTA publish flags, one set per stream

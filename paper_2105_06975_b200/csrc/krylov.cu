@@ -283,26 +283,41 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   }
   for (j = 1; j <= o.maxit; ++j) {
     const int phase = (j - 1) % 6;
-    if (graphs && j > 6) {
-      // phases repeat every 6 iterations: j > 6 means this phase already ran eagerly
-      // (all lazy allocations and kernel attributes are done) -> capture once, replay
+    if (graphs && c.mg_warm) {
+      // one eager iteration since the cache was (re)built has run every kernel path
+      // and lazy allocation, so every phase can be captured: capture all missing
+      // phases at once (capture does not execute), from the pointer sets the 6-periodic
+      // rotation gives, so a later solve on the same buffers (the bench's timed one
+      // after its warm-up) only replays
       if (!c.mg_exec[phase]) {
-        // capture does not execute: record the counter increments of one iteration
-        // (launches, per-window constituent products) and add them on every replay
-        cudaGraph_t g = nullptr;
-        const Ctx::Counters before = c.counters();
-        WF_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
-        body(vp, v, vn, z, zn, wp, w, awp, aw);
-        WF_CUDA(cudaStreamEndCapture(c.st, &g));
-        c.mg_delta[phase] = c.counters() - before;
-        c.set_counters(before);
-        WF_CUDA(cudaGraphInstantiate(&c.mg_exec[phase], g, 0));
-        cudaGraphDestroy(g);
+        double *q_vp = vp, *q_v = v, *q_vn = vn, *q_z = z, *q_zn = zn;
+        double *q_wp = wp, *q_w = w, *q_awp = awp, *q_aw = aw;
+        for (int q = 0; q < 6; ++q) {
+          const int ph = (phase + q) % 6;
+          if (!c.mg_exec[ph]) {
+            // record the counter increments of one iteration (launches, per-window
+            // constituent products) and add them on every replay
+            cudaGraph_t g = nullptr;
+            const Ctx::Counters before = c.counters();
+            WF_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
+            body(q_vp, q_v, q_vn, q_z, q_zn, q_wp, q_w, q_awp, q_aw);
+            WF_CUDA(cudaStreamEndCapture(c.st, &g));
+            c.mg_delta[ph] = c.counters() - before;
+            c.set_counters(before);
+            WF_CUDA(cudaGraphInstantiate(&c.mg_exec[ph], g, 0));
+            cudaGraphDestroy(g);
+          }
+          std::swap(q_vp, q_v); std::swap(q_v, q_vn);
+          std::swap(q_z, q_zn);
+          std::swap(q_wp, q_w);
+          std::swap(q_awp, q_aw);
+        }
       }
       WF_CUDA(cudaGraphLaunch(c.mg_exec[phase], c.st));
       c.set_counters(c.counters() + c.mg_delta[phase]);
     } else {
       body(vp, v, vn, z, zn, wp, w, awp, aw);
+      if (graphs) c.mg_warm = true;
     }
     WF_CUDA(cudaEventRecord(c.iter_event(j), c.st));
     // rotate: v_prev <- v, v <- v_new, z <- z_new, w_prev <- w, w <- w_new(in wp), same for Aw
@@ -639,8 +654,13 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
   const int jmax = mr + 1;
 
   const size_t vecb = ((size_t)n * 8 + 255) / 256 * 256;
-  c.kws_reset((size_t)(mr + 3) * vecb + (size_t)gy * jmax * m * 8 +
-              (size_t)m * ((mr + 1) * mr + (mr + 1) + 2 * mr + 4 + 3 * jmax) * 8 +
+  // reserve for the restart length even when maxit is shorter, so a short solve (a
+  // warm-up) and a longer one share the arena instead of reallocating it on the second
+  // call (r01bl: a multi-GB cudaFree/cudaMalloc inside the bench's timed solve was the
+  // 13.5 -> 18-21 ms spread of configs[4])
+  const int ma = o.restart > 0 ? std::max(mr, o.restart) : mr, jma = ma + 1;
+  c.kws_reset((size_t)(ma + 3) * vecb + (size_t)gy * jma * m * 8 +
+              (size_t)m * ((ma + 1) * ma + (ma + 1) + 2 * ma + 4 + 3 * jma) * 8 +
               (size_t)(5 * m + 4) * 4 + ((rep && rep->history) ? (size_t)(o.maxit + 1) * m * 8 : 0) +
               64 * 256);
   double *V = c.kws_take<double>((size_t)(mr + 1) * n);
