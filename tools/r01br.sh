@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r01br.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_banded.py tests/test_gpu_ichol.py tests/test_gpu_paper_heat.py tests/test_gpu_rblock.py tests/test_gpu_parity.py -q > gpurun_out/pytest_r01br.log 2>&1; echo "p=$?" >> gpurun_out/status_r01br
+for r in 1 2; do timeout 300 python bench.py --config 5 --steps 30 --tts-maxit 0 --no-cpu-baseline --e2e-steps 1 > gpurun_out/c5_${r}_r01br.log 2>&1; done
+timeout 300 python tools/kbench.py --trsm-only > gpurun_out/kb_trsm_r01br.json 2>&1
+echo done >> gpurun_out/status_r01br
