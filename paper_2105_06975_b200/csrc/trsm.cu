@@ -68,11 +68,7 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   extern __shared__ __align__(16) double smem[];
   double *sPipe = smem;                        // C::SMEM_DOUBLES
   double *sT = smem + C::SMEM_DOUBLES;         // [64][NB+1]
-  // diagonal-tile pack buffers: one (substitution form), two alternating (inverse
-  // form: the next tile's pack is prefetched under this tile's work)
-  double *const sGbuf0 = sT + TB * (NB + 1);
-  double *const sGbuf1 = sGbuf0 + (INV ? kDiagPack : 0);
-  double *sG = sGbuf0;                         // [64][65] diagonal tile, transposed
+  double *sG = sT + TB * (NB + 1);             // [64][65] diagonal tile, transposed
   double *sD = sG + TB * (TB + 1);             // [64] reciprocal diagonal
 
   int panel = blockIdx.x, gi = 0;
@@ -91,28 +87,18 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   const double *X = P.X;
   const int ncols = P.ncols;
 
-  auto pack_of = [&](int t_it) -> const double * {
-    const int t_ti = UPPER ? (ntile - 1 - t_it) : t_it;
-    const int t_r0 = slo + t_ti * TB;
-    return (P.dpack && (t_r0 % TB) == 0) ? P.dpack + (int64_t)(t_r0 / TB) * kDiagPack : nullptr;
-  };
-  bool cur_in_flight = false;   // this tile's pack was prefetched by the previous tile
   for (int it = 0; it < ntile; ++it) {
     const int ti = UPPER ? (ntile - 1 - it) : it;
     const int r0 = slo + ti * TB, r1 = min(shi, r0 + TB), nr = r1 - r0;
-    if (INV) {
-      sG = (it & 1) ? sGbuf1 : sGbuf0;
-      sD = sG + TB * (TB + 1);
-    }
     // ---- setup-time pack of this diagonal tile (ncu r01g: building it in-kernel from
     // strided global loads + reciprocals was the top stall of k_trsm): one contiguous
     // 33 KB cp.async copy straight into sG|sD, overlapped with the tile GEMM below
-    const double *dpk = pack_of(it);
-    if (dpk && !cur_in_flight) {
+    const double *dpk = (P.dpack && (r0 % TB) == 0) ? P.dpack + (int64_t)(r0 / TB) * kDiagPack
+                                                      : nullptr;
+    if (dpk) {
       for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(sG + e, dpk + e, 16);
+      cp_async_commit();
     }
-    cur_in_flight = false;
-    cp_async_commit();
     // ---- in-segment off-diagonal update: acc = G[r0:r1, K] * Y[K, panel]
     const int kbeg = UPPER ? r1 : slo;
     const int kend = UPPER ? shi : r0;
@@ -153,20 +139,6 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
       // the 8-row blocks w and w + 4 across all NB columns.
       cp_async_wait<0>();
       __syncthreads();
-      if (it + 1 < ntile) {
-        // the next tile's pack into the other buffer (its last reader, the previous
-        // tile's product, finished before that tile's closing barrier): it lands under
-        // this product, the stores and the next tile's GEMM prologue instead of costing
-        // the next tile an L2 round trip (ncu r01bp: the banded NEXT-1 walk paid one
-        // per 64-row tile)
-        const double *npk = pack_of(it + 1);
-        if (npk) {
-          double *nb = (it & 1) ? sGbuf0 : sGbuf1;
-          for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(nb + e, npk + e, 16);
-          cur_in_flight = true;
-        }
-        cp_async_commit();
-      }
       constexpr int NJ = NB / 8;
       double ya[2][NJ][2];
 #pragma unroll
@@ -351,7 +323,7 @@ double *make_diag_pack(Ctx &c, const double *G, int n, bool upper) {
 template <int NB, bool UPPER, bool INV>
 static void run_inv(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   using C = TrsmCfg<NB>;
-  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + (INV ? 2 : 1) * kDiagPack) * sizeof(double);
+  size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + kDiagPack) * sizeof(double);
   auto kern = v16 ? k_trsm<NB, UPPER, true, INV> : k_trsm<NB, UPPER, false, INV>;
   // one-time (thread-safe static initialisation) opt-in to the large dynamic smem
   static const cudaError_t attr_v =
