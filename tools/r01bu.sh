@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_r01bu.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_banded.py tests/test_gpu_ichol.py tests/test_gpu_paper_heat.py -q > gpurun_out/pytest_r01bu.log 2>&1; echo "p=$?" >> gpurun_out/status_r01bu
+for r in 1 2; do timeout 300 python bench.py --config 5 --steps 30 --tts-maxit 0 --no-cpu-baseline --e2e-steps 1 > gpurun_out/c5_${r}_r01bu.log 2>&1; done
+echo done >> gpurun_out/status_r01bu
