@@ -42,7 +42,8 @@ CELLS = {
     5: dict(shape="PD", lhat="LM", k=4, rhat="block", solver="minres", factor="ichol",
             ridge=0.01, block_tol=0.05),
 }
-PC_KEYS = ("shape", "lhat", "k", "rhat", "factor", "ridge", "block_tol", "pvec")
+PC_KEYS = ("shape", "lhat", "k", "rhat", "factor", "ridge", "block_tol", "pvec", "block",
+           "apply_mode")
 
 
 FP64_ALU_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12   # TFLOP/s, FP64 DFMA pipe at max SM clock
@@ -51,7 +52,10 @@ FP64_ALU_PEAK = 148 * 64 * 2 * 1.965e9 / 1e12   # TFLOP/s, FP64 DFMA pipe at max
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed Krylov iterations (default 20; GMRES: one restart cycle, 50; "
+                         "GMRES step counts are rounded up to whole restart cycles so the "
+                         "CGS2 cost is averaged over complete cycles)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=3)
@@ -62,6 +66,11 @@ def parse():
     ap.add_argument("--lhat", default=None)
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--rhat", default=None)
+    ap.add_argument("--block", type=int, default=None, help="R_block uniform block size")
+    ap.add_argument("--apply-mode", default=None, choices=["trsm", "inverse"],
+                    help="dense D_hat/R_hat blocks: triangular solves (default) or the opt-in "
+                         "explicit inverses (DESIGN.md reading A32)")
+    ap.add_argument("--restart", type=int, default=50)
     ap.add_argument("--tts-maxit", type=int, default=400,
                     help="cap for the time-to-1e-8 solve (0 disables it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -81,49 +90,102 @@ def dist_setup():
 
 
 class Clocks:
-    """nvidia-smi sampler (the recipe's clocks line) running during the timed region."""
+    """SM clock / throttle-reason sampler running during the timed region (the recipe's
+    clocks line).  NVML (nvidia-ml-py) in a thread every 20 ms; nvidia-smi writing to a
+    file as the fallback (a pipe would lose its block-buffered output when the sampler
+    is terminated after a sub-second timed region -- the round-1 bench lines carried no
+    clock record for that reason)."""
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device):
-        self.device = device
-        self.p = None
+    def __init__(self, torch, device):
+        self.torch, self.device = torch, device
+        self.samples, self.mx, self.reasons, self.err = [], None, set(), None
+        self.proc = None
+
+    def _nvml_handle(self):
+        import pynvml as N
+        N.nvmlInit()
+        pr = self.torch.cuda.get_device_properties(self.device)
+        want = (getattr(pr, "pci_domain_id", 0), pr.pci_bus_id, pr.pci_device_id)
+        for i in range(N.nvmlDeviceGetCount()):
+            h = N.nvmlDeviceGetHandleByIndex(i)
+            pci = N.nvmlDeviceGetPciInfo(h)
+            if (pci.domain, pci.bus, pci.device) == want:
+                return N, h
+        return N, N.nvmlDeviceGetHandleByIndex(self.device)
 
     def __enter__(self):
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+        self.stop = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.p = None
+            N, h = self._nvml_handle()
+            get_r = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+
+            def loop():
+                while True:
+                    try:
+                        self.samples.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+                        bits = int(get_r(h))
+                        for bit, nm in self.REASONS.items():
+                            if bits & bit:
+                                self.reasons.add(nm)
+                    except Exception as e:   # pragma: no cover
+                        self.err = repr(e)
+                    if self.stop.wait(0.02):
+                        break
+            self.th = threading.Thread(target=loop, daemon=True)
+            self.th.start()
+            self.src = "nvml"
+        except Exception as e:
+            self.err = repr(e)
+            self.th = None
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            self.fname = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits", "-lms", "50",
+                                              "-f", self.fname], stderr=subprocess.DEVNULL)
+                self.src = "nvidia-smi"
+            except Exception as e2:
+                self.err += " / " + repr(e2)
         return self
 
     def __exit__(self, *a):
-        self.lines = []
-        if self.p:
-            time.sleep(0.25)
-            self.p.terminate()
-            out = self.p.communicate()[0]
-            self.lines = [l for l in out.strip().splitlines() if l.strip()]
+        if self.th is not None:
+            time.sleep(0.03)
+            self.stop.set()
+            self.th.join()
+        elif self.proc is not None:
+            time.sleep(0.3)
+            self.proc.terminate()
+            self.proc.wait()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            try:
+                for l in open(self.fname):
+                    f = [x.strip() for x in l.split(",")]
+                    try:
+                        self.samples.append(float(f[0]))
+                        self.mx = float(f[1])
+                    except (ValueError, IndexError):
+                        continue
+                    for nm, v in zip(names, f[2:6]):
+                        if v.lower().startswith("active"):
+                            self.reasons.add(nm)
+            except OSError as e:
+                self.err = repr(e)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
-            f = [x.strip() for x in l.split(",")]
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": [],
+                    "error": f"no clock samples ({self.err})"}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "source": getattr(self, "src", None)}
 
 
 def measure_dgemm_peak(torch, dev):
@@ -148,13 +210,22 @@ def measure_dgemm_peak(torch, dev):
 
 def cell_of(args):
     cell = dict(CELLS[args.config])
-    for key in ("shape", "lhat", "k", "rhat"):
+    for key in ("shape", "lhat", "k", "rhat", "block", "apply_mode"):
         v = getattr(args, key)
         if v is not None:
             cell[key] = v
     if cell["shape"] == "PI":
         cell["solver"] = "gmres"
     return cell
+
+
+def steps_for(args, cell):
+    """Timed steps: --steps, default 20; for GMRES(m_r) whole restart cycles (>= one),
+    so the CGS2 work (growing with the Arnoldi index) is averaged over full cycles."""
+    k = args.steps if args.steps is not None else (args.restart if cell["solver"] == "gmres" else 20)
+    if cell["solver"] == "gmres" and k % args.restart:
+        k = (k // args.restart + 1) * args.restart
+    return k
 
 
 def workload_name(config):
@@ -203,6 +274,7 @@ def run_reference(args):
         return
     from synth import configs as SC
     cell = cell_of(args)
+    args.steps = steps_for(args, cell)
     prob, wscale = sample_problem(SC, args.config)
     if cell["rhat"] == "block" and "pvec" not in cell and "pvec" in prob.extra:
         cell["pvec"] = prob.extra["pvec"]
@@ -246,6 +318,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     cell = cell_of(args)
+    args.steps = steps_for(args, cell)
     cfgm = SC.CONFIGS[args.config]["m"]
     m = args.m or cfgm
     time_shard = ws > 1 and args.shard == "time"
@@ -268,7 +341,7 @@ def main():
     b = torch.from_numpy(rhs).to(dev)
     x = torch.empty_like(b)
     solver = cell["solver"]
-    kw = dict(solver=solver, tol=1e-300, restart=50, mark_tol=1e-8)
+    kw = dict(solver=solver, tol=1e-300, restart=args.restart, mark_tol=1e-8)
 
     # warm-up (also allocates the Krylov workspace)
     with torch.cuda.stream(stream):
@@ -282,7 +355,7 @@ def main():
     l0 = ctx.launch_count
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
+    with Clocks(torch, local) as clk:
         barrier()
         torch.cuda.synchronize(dev)
         e0.record(stream)
@@ -330,7 +403,7 @@ def main():
     # time-to-1e-8 (one real solve; reported, capped)
     tts = None
     if args.tts_maxit > 0:
-        r = ctx.solve(b, x, solver=solver, tol=1e-8, maxit=args.tts_maxit, restart=50,
+        r = ctx.solve(b, x, solver=solver, tol=1e-8, maxit=args.tts_maxit, restart=args.restart,
                       mark_tol=1e-8, check_every=10)
         tts = dict(seconds=r["seconds_to_mark"] if r["seconds_to_mark"] >= 0 else None,
                    iterations=int(r["iters_to_mark"]) if r["iters_to_mark"] >= 0 else None,

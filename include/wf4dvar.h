@@ -149,7 +149,17 @@ typedef struct {
      'nofill'): the preconditioner blocks become L L^T, applied as
      sparse triangular solves.  For compact-support covariances; not with R_ME. */
   int32_t factor;
+  /* How dense D_hat / R_hat blocks (n >= 256, exact Cholesky factors, not banded) are
+     applied.  WF4DVAR_APPLY_TRSM (0, default): the two triangular solves with the
+     Cholesky factors, backward stable (the per-block parity test
+     checks ||C y - x|| / (||C|| ||y||) <= 1e-14).  WF4DVAR_APPLY_INVERSE (1): one GEMM
+     with the setup-time explicit inverse (G G^T)^{-1} (reading A32); the
+     same flops at GEMM rate, but NOT backward stable (backward error up to ~kappa u on
+     smooth vectors), which costs Krylov iterations.  Env WF4DVAR_EXPLICIT_INV=0/1
+     overrides this field. */
+  int32_t apply_mode;
 } wf4dvar_precond;
+typedef enum { WF4DVAR_APPLY_TRSM = 0, WF4DVAR_APPLY_INVERSE = 1 } wf4dvar_apply_mode;
 typedef enum { WF4DVAR_FACTOR_CHOL = 0, WF4DVAR_FACTOR_ICHOL = 1 } wf4dvar_factor;
 
 /* Time-window sharding ("the model propagations M_i can be

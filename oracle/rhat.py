@@ -13,9 +13,13 @@
            (relative gap 1e-10; reading A6).
   D_hat    P:L572: ridge B + delta I, Q + delta I (delta = 0.01 in the paper);
            default D_hat = D (reading A4).
-Every function returns the dense matrix of the definition; inverse applies in
-the oracle are dense solves against these matrices (no Woodbury, no factor
-reuse), so they are independent of the CUDA path's factorisations.
+Every function returns the dense matrix of the definition (R_ME by its
+eigendecomposition, no Woodbury).  The oracle applies their inverses with LAPACK
+Cholesky solves against these matrices (oracle/saddle.py: scipy cho_factor once per
+distinct block, cho_solve per window -- the paper applies R_hat^{-1} "using the
+Cholesky factors", and D_hat^{-1} by its factors); the explicit
+route (oracle/saddle.py explicit_apply_Pinv) is an LU solve with the assembled P.
+Both are independent of the CUDA path's factorisations and kernels.
 """
 import numpy as np
 

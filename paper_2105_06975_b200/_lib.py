@@ -45,7 +45,7 @@ class Precond(C.Structure):
                 ("gamma", C.c_double), ("T", C.c_double), ("block", C.c_int32),
                 ("dhat_ridge", C.c_double), ("pvec", _ip), ("npvec", C.c_int32),
                 ("block_tol", C.c_double), ("maxsize", C.c_int32), ("numproc", C.c_int32),
-                ("factor", C.c_int32)]
+                ("factor", C.c_int32), ("apply_mode", C.c_int32)]
 
 
 TRANSPORT_NONE, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
@@ -245,7 +245,7 @@ RHATS = {"diag": RDIAG, "block": RBLOCK, "rr": RRR, "me": RME, "exact": REXACT}
 
 def make_precond(shape="PD", lhat="LM", k=4, rhat="exact", gamma=-1.0, T=-1.0, block=0,
                  ridge=0.0, pvec=None, block_tol=float("inf"), maxsize=0, numproc=0,
-                 factor="chol"):
+                 factor="chol", apply_mode="trsm"):
     pc = Precond(SHAPES[shape], LHATS[lhat], int(k or 1), RHATS[rhat], float(gamma), float(T),
                  int(block or 0), float(ridge))
     if pvec is not None:
@@ -257,6 +257,7 @@ def make_precond(shape="PD", lhat="LM", k=4, rhat="exact", gamma=-1.0, T=-1.0, b
     pc.maxsize = int(maxsize or 0)
     pc.numproc = int(numproc or 0)
     pc.factor = {"chol": 0, "ichol": 1}[factor]
+    pc.apply_mode = {"trsm": 0, "inverse": 1}[apply_mode]
     return pc
 
 

@@ -251,6 +251,7 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (e.flags) cudaFree(e.flags);
     if (e.splitk) cudaFree(e.splitk);
   }
+  for (void *p : c.retired) cudaFree(p);
   for (void *p : c.allocs) cudaFree(p);
   for (auto &pe : c.prof.pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : c.prof.pool) cudaEventDestroy(e);

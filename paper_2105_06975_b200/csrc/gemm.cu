@@ -413,8 +413,8 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
       st->stream = c.st;
     }
     if (st->cap < need) {
-      if (st->ws) cudaFree(st->ws);
-      if (st->flags) cudaFree(st->flags);
+      if (st->ws) c.retired.push_back(st->ws);
+      if (st->flags) c.retired.push_back(st->flags);
       st->ws = nullptr; st->flags = nullptr; st->cap = 0;
       WF_CUDA(cudaMalloc(&st->ws, need * 8));
       WF_CUDA(cudaMalloc(&st->flags, G * sizeof(unsigned)));
@@ -639,7 +639,7 @@ static bool run_splitk(Ctx &c, const GemmProb *probs, int nprob, bool v16) {
   }
   const size_t need = (size_t)S * tiles * C::BM * C::BN;
   if (st->splitk_cap < need) {
-    if (st->splitk) cudaFree(st->splitk);
+    if (st->splitk) c.retired.push_back(st->splitk);
     st->splitk = nullptr;
     st->splitk_cap = 0;
     WF_CUDA(cudaMalloc(&st->splitk, need * 8));

@@ -299,6 +299,10 @@ struct Ctx {
     double *splitk = nullptr; size_t splitk_cap = 0;   // split-K partial tiles
   };
   std::vector<SkState> sk_states;
+  // workspaces replaced by a larger one: captured MINRES graphs may still reference
+  // them, so they are freed only with the context (freeing on growth left
+  // cached graph execs pointing at freed memory)
+  std::vector<void *> retired;
   Prof prof;
   std::string last_error;
   std::vector<void *> allocs;

@@ -504,13 +504,22 @@ __global__ void k_symmetrize(double *Z, int n) {
 // Reading A32: the explicit inverse (G G^T)^{-1} = G^{-T} G^{-1} of a Cholesky factor
 // pair, by the library's own blocked TRSMs on the identity (setup, n^3 flops; the
 // block structure of an R_block factor is kept, so its inverse is block diagonal and
-// registered for zero-tile skipping).  Used for dense factors with n >= 256: the
-// preconditioner's two dependent triangular solves per apply become one DMMA GEMM
-// (configs[3]: the D_hat / R_hat solves ran at ~21 TFLOP/s as TRSM chains, the same
-// flops as a GEMM at ~32).  WF4DVAR_EXPLICIT_INV=0 keeps the triangular solves.
-static bool use_explicit_inverse(int n) {
-  static const int env = env_int("WF4DVAR_EXPLICIT_INV", 1);
-  return env && n >= 256;
+// registered for zero-tile skipping).  Opt-in (wf4dvar_precond.apply_mode =
+// WF4DVAR_APPLY_INVERSE, or env WF4DVAR_EXPLICIT_INV=1): the preconditioner's two
+// dependent triangular solves per apply become one DMMA GEMM at GEMM rate, but the
+// product with a computed inverse is not backward stable -- on smooth vectors (the
+// ones a Krylov method produces) its backward error reaches ~kappa u (1e-8 on
+// configs[3]'s B against 1e-14 required), so the default is the
+// triangular solves ("using the Cholesky factors").
+// Never for banded factors (tile coverage < 0.35): their triangular solves skip the
+// zero tiles (O(n bw) per column) and a dense inverse would be O(n^2).
+static bool use_explicit_inverse(const Ctx &c, const double *G, int n) {
+  static const int env = env_int("WF4DVAR_EXPLICIT_INV", -1);   // -1: the precond field
+  const int on = env >= 0 ? env : (c.pc.apply_mode == WF4DVAR_APPLY_INVERSE);
+  if (!on || n < 256) return false;
+  int r0 = 0, c0 = 0;
+  const TileRanges *tr = find_tile_ranges(c, G, &r0, &c0);
+  return !(tr && r0 == 0 && c0 == 0 && tr->coverage < 0.35);
 }
 
 static double *explicit_inverse(Ctx &c, const double *G, const double *Gt, const double *P,
@@ -582,7 +591,7 @@ void setup_precond(Ctx &c) {
     c.PBt = make_diag_pack(c, c.GBt, s, true);
     c.PQ = make_diag_pack(c, c.GQ, s, false);
     c.PQt = make_diag_pack(c, c.GQt, s, true);
-    if (use_explicit_inverse(s)) {
+    if (use_explicit_inverse(c, c.GQ, s)) {
       c.IB = explicit_inverse(c, c.GB, c.GBt, c.PB, c.PBt, s, 0, nullptr);
       c.IQ = explicit_inverse(c, c.GQ, c.GQt, c.PQ, c.PQt, s, 0, nullptr);
     }
@@ -705,7 +714,7 @@ void setup_precond(Ctx &c) {
     chol(c, sv, Rdev, p, c.GR, c.GRt, name);
     c.PR = make_diag_pack(c, c.GR, p, false);
     c.PRt = make_diag_pack(c, c.GRt, p, true);
-    if (use_explicit_inverse(p)) {
+    if (use_explicit_inverse(c, c.GR, p)) {
       const bool seg = pc.rhat == WF4DVAR_RBLOCK && !c.rblk_starts.empty();
       c.IR = explicit_inverse(c, c.GR, c.GRt, c.PR, c.PRt, p,
                               pc.rhat == WF4DVAR_RBLOCK ? pc.block : 0,

@@ -139,6 +139,49 @@ def test_theorem31_collapse_when_S_hat_exact():
     assert np.all(np.min(np.abs(ev[:, None] - targets[None, :]), axis=1) < 1e-8)
 
 
+def _attained_case(a, b, c=2.5, s=4, p=3, N=2, seed=3):
+    """A saddle system on which every bound of Theorem 3.1 is attained: D = c I
+    (kappa(D) = 1), D_hat = D / a and R_hat = R / a (D_hat^{-1} D = R_hat^{-1} R = a I),
+    L_hat = L / sqrt(b) ((L_hat^T L_hat)^{-1} L^T L = b I), H = 0 (S = S_tilde).  Then
+    P_D^{-1} A has exactly the eigenvalues a and (a -+ sqrt(a^2 + 4 a b)) / 2 (the
+    eta/x block: [[a I, a L D^-1 ...]] reduces to lambda^2 - a lambda - a b = 0).
+    Returns the dense eigenvalues (computed here, independently of the formula)."""
+    import scipy.linalg as sla
+    rng = np.random.default_rng(seed)
+    W = N + 1
+    Ms = [rng.standard_normal((s, s)) * 0.5 for _ in range(N)]
+    L = LH.assemble("L", Ms, s)
+    D = c * np.eye(s * W)
+    G = rng.standard_normal((p, p))
+    R1 = G @ G.T + p * np.eye(p)
+    R = sla.block_diag(*([R1] * W))
+    Z = np.zeros
+    A = np.block([[D, Z((s * W, p * W)), L], [Z((p * W, s * W)), R, Z((p * W, s * W))],
+                  [L.T, Z((s * W, p * W)), Z((s * W, s * W))]])
+    Lh = L / math.sqrt(b)
+    P = sla.block_diag(D / a, R / a, Lh.T @ np.linalg.solve(D, Lh))
+    return np.sort(np.real(sla.eigvals(A, P)))
+
+
+@pytest.mark.parametrize("a,b", [(1.0, 1.0), (0.7, 1.9), (2.3, 0.4)])
+def test_theorem31_intervals_attained(a, b):
+    """theorem31_intervals pinned by value: in the attained case each of the three
+    intervals degenerates to a point, and the points are the dense eigenvalues of
+    P_D^{-1} A (a = b = 1 is the S:L545 collapse {(1-sqrt5)/2, 1, (1+sqrt5)/2})."""
+    ev = _attained_case(a, b)
+    iv = SP.theorem31_intervals(a, a, a, a, 1.0, 1.0, b, b, 1.0)
+    for lo, hi in iv:
+        assert abs(hi - lo) <= 1e-15 * max(1.0, abs(lo))
+    pts = np.array([iv[0][0], iv[1][0], iv[2][0]])
+    # every eigenvalue is one of the three points, and each point is attained
+    d = np.abs(ev[:, None] - pts[None, :])
+    assert np.all(d.min(axis=1) < 1e-9 * max(1.0, np.abs(ev).max())), (ev, pts)
+    assert np.all(d.min(axis=0) < 1e-9 * max(1.0, np.abs(ev).max())), (ev, pts)
+    if a == 1.0 and b == 1.0:
+        np.testing.assert_allclose(pts, [(1 - math.sqrt(5)) / 2, 1.0, (1 + math.sqrt(5)) / 2],
+                                   rtol=0, atol=1e-15)
+
+
 def test_saddle_equals_primal_normal_equations(c0):
     # P:L144-147: the saddle solution's dx solves the primal normal equations.
     prob, sad = c0
