@@ -71,7 +71,7 @@ def parse():
                     help="dense D_hat/R_hat blocks: triangular solves (default) or the opt-in "
                          "explicit inverses (DESIGN.md reading A32)")
     ap.add_argument("--restart", type=int, default=50)
-    ap.add_argument("--tts-maxit", type=int, default=400,
+    ap.add_argument("--tts-maxit", type=int, default=2000,
                     help="cap for the time-to-1e-8 solve (0 disables it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

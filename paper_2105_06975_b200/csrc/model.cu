@@ -15,6 +15,7 @@
 
 #include <type_traits>
 
+#include "dmma.cuh"
 #include "internal.h"
 
 namespace wf {
@@ -136,6 +137,120 @@ __global__ void __launch_bounds__(128) k_heat_iir(double *out, const double *bas
       }
       out[i * ld + col] = val;
     }
+  }
+}
+
+// CTA-tiled form of k_heat_iir with warp-parallel recursions (default).  A CTA owns 32
+// consecutive (window, RHS) columns and R output rows.  The input rows [i0 - H,
+// i0 + R + H] are staged once into shared memory, coalesced (one 256-byte row segment
+// per warp load): 1 + (2H + 1)/R input reads per output instead of the (TI + 2H + 1)/TI
+// of the thread-per-chunk form, whose warm-ups re-read the neighbours' rows from L2.
+// Then each warp takes whole columns and runs both first-order recursions
+// (u_j = x_j + rho u_{j-1} forward, v_i = u_i + rho v_{i+1} backward) in parallel over
+// its 32 lanes: lane l owns CH consecutive rows, runs the recursion locally from zero,
+// the lanes' end values are combined by a shuffle scan of the affine maps
+// (a, b) o (a', b') = (a a', b a' + b') with a = rho^len, and each lane adds its carry
+// times rho^(t+1).  Same operator (restart H rows outside the output range, dropped tail
+// < 1e-17 relative), other rounding order than k_heat_iir.  Results go back to shared
+// memory and leave as coalesced rows: out = base + gain * v (+ the H^T scatter).
+template <int H, int R, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_heat_iir_scan(
+    double *out, const double *base, const double *in, const double *add2, const int *row_map,
+    double rho, double gain, int s, int W, int m, int w_first, int w_step, int nw, int dir,
+    const double *halo, int w0, int WG) {
+  constexpr int NS = R + 2 * H + 1;          // staged rows i0 - H .. i0 + R + H
+  constexpr int LD = 33;                     // padded row stride (doubles)
+  constexpr int CH0 = (NS + 31) / 32;
+  constexpr int CH = CH0 | 1;                // odd: lane strides CH*LD hit distinct banks
+  extern __shared__ double tile[];           // [NS][LD]
+  const int64_t ld = (int64_t)W * m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = blockIdx.y * R;
+  // this lane's column (load / store phases)
+  const int cc = blockIdx.x * 32 + lane;
+  const bool live = cc < nw * m;
+  const int tt = live ? cc / m : 0, r = live ? cc - tt * m : 0;
+  const int w = w_first + tt * w_step, ws = w + dir;
+  const bool has = live && (w0 + ws >= 0 && w0 + ws < WG);
+  const bool from_halo = (ws < 0 || ws >= W);
+  {
+    // all NS x 32 loads in flight at once: cp.async straight into shared memory (ncu
+    // r02e: register-staged loads left this kernel long-scoreboard bound at 12% of DRAM
+    // bandwidth); a missing source (no M term, or a dead lane) zero-fills
+    const double *src = has ? (from_halo ? halo + r : in + (int64_t)ws * m + r) : in;
+    const int64_t sld = from_halo ? (int64_t)m : ld;
+    int row = (i0 - H + warp) % s;
+    row = row < 0 ? row + s : row;
+#pragma unroll 4
+    for (int j = warp; j < NS; j += WARPS) {
+      cp_async8(tile + j * LD + lane, has ? src + (int64_t)row * sld : src, has ? 8 : 0);
+      row += WARPS;
+      while (row >= s) row -= s;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
+  __syncthreads();
+  // recursions, one column per warp at a time; lane l owns rows [l*CH, l*CH + len)
+  const int j0 = lane * CH;
+  const int len = max(0, min(CH, NS - j0));
+  double rl = 1.0;                           // rho^len
+  for (int t = 0; t < len; ++t) rl *= rho;
+  for (int c = warp; c < 32; c += WARPS) {
+    double *col = tile + c;
+    // forward, local from zero
+    double u = 0.0;
+#pragma unroll
+    for (int t = 0; t < CH; ++t)
+      if (t < len) { u = fma(rho, u, col[(j0 + t) * LD]); col[(j0 + t) * LD] = u; }
+    // inclusive scan of (a, b) = (rho^len, u_end) over the lanes
+    double a = rl, b = u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double ap = __shfl_up_sync(0xffffffffu, a, o);
+      const double bp = __shfl_up_sync(0xffffffffu, b, o);
+      if (lane >= o) { b = fma(bp, a, b); a *= ap; }
+    }
+    double carry = __shfl_up_sync(0xffffffffu, b, 1);   // state entering this lane's rows
+    if (lane == 0) carry = 0.0;
+    double pw = rho;
+#pragma unroll
+    for (int t = 0; t < CH; ++t)
+      if (t < len) { col[(j0 + t) * LD] = fma(carry, pw, col[(j0 + t) * LD]); pw *= rho; }
+    __syncwarp();
+    // backward, local from zero, then the carry from the lanes above
+    double v = 0.0;
+#pragma unroll
+    for (int t = CH - 1; t >= 0; --t)
+      if (t < len) { v = fma(rho, v, col[(j0 + t) * LD]); col[(j0 + t) * LD] = v; }
+    a = rl; b = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double an = __shfl_down_sync(0xffffffffu, a, o);
+      const double bn = __shfl_down_sync(0xffffffffu, b, o);
+      if (lane + o < 32) { b = fma(bn, a, b); a *= an; }
+    }
+    carry = __shfl_down_sync(0xffffffffu, b, 1);
+    if (lane == 31) carry = 0.0;
+    pw = rho;
+#pragma unroll
+    for (int t = CH - 1; t >= 0; --t)
+      if (t < len) { col[(j0 + t) * LD] = fma(carry, pw, col[(j0 + t) * LD]); pw *= rho; }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (!live) return;
+  const int64_t ocol = (int64_t)w * m + r;
+  for (int j = H + warp; j < H + R; j += WARPS) {
+    const int i = i0 + j - H;
+    if (i >= s) break;
+    double val = base[(int64_t)i * ld + ocol];
+    if (has) val = fma(gain, tile[j * LD + lane], val);
+    if (add2) {
+      const int q = row_map[i];
+      if (q >= 0) val += add2[(int64_t)q * ld + ocol];
+    }
+    out[(int64_t)i * ld + ocol] = val;
   }
 }
 
@@ -341,6 +456,25 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // c1 0.318 / 0.290 / 0.276 ms, c0 0.151 / 0.137 / 0.128 ms -- the recursions are
     // latency-bound chains; shorter chunks (the H-row warm-ups re-read from L2) give
     // more independent chains and fewer registers (higher occupancy)
+    static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 0);   // 128/256: warp-scan form
+    if (tile_env == 128 || tile_env == 256) {
+      constexpr int WARPS = 8;
+      auto go = [&](auto r_tag) {
+        constexpr int R = decltype(r_tag)::value;
+        constexpr size_t smem = (size_t)(R + 2 * H + 1) * 33 * sizeof(double);
+        static const cudaError_t attr = cudaFuncSetAttribute(
+            k_heat_iir_scan<H, R, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        WF_CUDA(attr);
+        dim3 grid((cols + 31) / 32, (c.s + R - 1) / R);
+        k_heat_iir_scan<H, R, WARPS><<<grid, WARPS * 32, smem, c.st>>>(
+            out, base, in, add2, row_map, c.heat_rho, sign * c.heat_gain, c.s, c.W, c.m, w_first,
+            w_step, nw, transpose ? 1 : -1, transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+      };
+      if (tile_env == 128) go(std::integral_constant<int, 128>{});
+      else go(std::integral_constant<int, 256>{});
+      WF_CUDA(cudaGetLastError());
+      return;
+    }
     static const int ti_env = env_int("WF4DVAR_HEAT_TI", 8);   // tuning experiments only
     auto go = [&](auto ti_tag) {
       constexpr int TI = decltype(ti_tag)::value;

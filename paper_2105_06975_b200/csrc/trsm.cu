@@ -580,12 +580,19 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     trsm_segments(c, probs, np, upper, 0, blk, n);
     return;
   }
-  // measured r01c/r01l (kbench, bench c3): the recursive split is within 1% of the
-  // super-block scheme at n = 4096, so the default stays blocked; WF4DVAR_TRSM_LEAF=512
-  // selects the recursion
-  static const int leaf_env = env_int("WF4DVAR_TRSM_LEAF", 0);   // tuning experiments only (0 = blocked)
-  if (leaf_env > 0 && n > leaf_env) {
-    trsm_rec(c, probs, np, upper, 0, n, leaf_env, true);
+  // recursion (Elmroth-Gustavson, leaf 512) for the large dense factors with wide
+  // right-hand sides: with the triangular solves as the default D_hat^{-1} apply, the
+  // configs[3] step measured 32.33 (blocked, SB = 1024) -> 32.04 ms (leaf 512; leaf 256:
+  // 33.30, 768: 32.68 with the same heat kernel; r02c/r02d sweeps) -- the top-level
+  // coupling GEMM (K = n/2) runs at GEMM rate and the panels shrink to 512 rows.
+  // Standalone (r01c/r01l kbench) the two schemes were within 1%.  WF4DVAR_TRSM_LEAF=0
+  // forces the blocked scheme, > 0 the recursion with that leaf.
+  int total_cols0 = 0;
+  for (int i = 0; i < np; ++i) total_cols0 += probs[i].ncols;
+  static const int leaf_env = env_int("WF4DVAR_TRSM_LEAF", -1);
+  const int leaf = leaf_env >= 0 ? leaf_env : ((n >= 4096 && total_cols0 > 1536 && !banded) ? 512 : 0);
+  if (leaf > 0 && n > leaf) {
+    trsm_rec(c, probs, np, upper, 0, n, leaf, true);
     return;
   }
   static const int sb_env = env_int("WF4DVAR_TRSM_SB", 0);   // tuning experiments only

@@ -180,7 +180,31 @@ def _build(name, model, s, N, q, m, Bp, Qp, Rp, seed0, heat_r=0.25, F=8.0, dt=0.
 
 
 def make_problem(cfg, seed0=0, m=None, N=None, with_rhs=True):
-    """Build BASELINE.json configs[cfg]; optionally override batch width m or N."""
+    """Build BASELINE.json configs[cfg]; optionally override batch width m or N.
+    With env WF4DVAR_PROBLEM_CACHE=<dir> the built problem is pickled there, keyed by
+    the arguments and this module's source (tools running many processes on one box
+    build each config once; the content is a deterministic function of the key)."""
+    import os
+    cdir = os.environ.get("WF4DVAR_PROBLEM_CACHE")
+    if cdir:
+        import hashlib
+        import pickle
+        src = open(__file__, "rb").read()
+        key = hashlib.sha1(repr((cfg, seed0, m, N, with_rhs)).encode() + src).hexdigest()[:16]
+        fn = os.path.join(cdir, f"c{cfg}_{key}.pkl")
+        if os.path.exists(fn):
+            with open(fn, "rb") as f:
+                return pickle.load(f)
+        prob = _make_problem(cfg, seed0, m, N, with_rhs)
+        os.makedirs(cdir, exist_ok=True)
+        with open(fn + ".tmp", "wb") as f:
+            pickle.dump(prob, f, protocol=4)
+        os.replace(fn + ".tmp", fn)
+        return prob
+    return _make_problem(cfg, seed0, m, N, with_rhs)
+
+
+def _make_problem(cfg, seed0, m, N, with_rhs):
     c = dict(CONFIGS[cfg])
     mm = c["m"] if m is None else m
     NN = c["N"] if N is None else N
