@@ -130,6 +130,7 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       WF_CUDA(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    WF_CUDA(cudaEventCreateWithFlags(&c.ev_halo, cudaEventDisableTiming));
     WF_CUDA(cudaStreamCreateWithFlags(&c.cpy, cudaStreamNonBlocking));
     for (auto &e : c.ev_in) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : c.ev_chunk) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -239,6 +240,7 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
   }
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.ev_halo) cudaEventDestroy(c.ev_halo);
   if (c.cpy) { cudaStreamSynchronize(c.cpy); cudaStreamDestroy(c.cpy); }
   for (auto &e : c.ev_in) if (e) cudaEventDestroy(e);
   for (auto &e : c.ev_chunk) if (e) cudaEventDestroy(e);

@@ -216,6 +216,7 @@ struct Ctx {
   // fork/join streams: the three independent blocks of A and of P_D run concurrently
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaEvent_t ev_halo = nullptr;   // apply_A's halo exchange done (aux[1] -> main)
   cudaStream_t cpy = nullptr;          // host path: block-wise H2D of apply_P's input
   cudaEvent_t ev_in[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_chunk[4] = {nullptr, nullptr, nullptr, nullptr};   // host path column chunks

@@ -456,7 +456,9 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // c1 0.318 / 0.290 / 0.276 ms, c0 0.151 / 0.137 / 0.128 ms -- the recursions are
     // latency-bound chains; shorter chunks (the H-row warm-ups re-read from L2) give
     // more independent chains and fewer registers (higher occupancy)
-    static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 0);   // 128/256: warp-scan form
+    // r02f (configs[3] per step): thread-per-chunk 1.264 ms (2.31 TB/s) -> warp-scan with
+    // cp.async staging R = 128: 1.110 ms (2.63 TB/s), R = 256: 1.431 ms (fewer CTAs per SM)
+    static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 128);   // 0: thread-per-chunk form
     if (tile_env == 128 || tile_env == 256) {
       constexpr int WARPS = 8;
       auto go = [&](auto r_tag) {

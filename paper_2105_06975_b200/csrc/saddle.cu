@@ -62,7 +62,10 @@ static void d_product(Ctx &c, const double *X, double *Y, const double *Z, doubl
 constexpr int kHostChunks = 4;
 // only worth it when a block's copy is long against the per-chunk launch latencies
 // (configs[3]: 268 MB per block, 4.9 ms over PCIe; configs[1]: 2.7 MB)
-static bool host_chunking(const Ctx &c) { return (double)c.s * c.ncol * 8 >= 64e6; }
+static bool host_chunking(const Ctx &c) {
+  static const int mb = env_int("WF4DVAR_HOST_CHUNK_MB", 64);   // tests force it on small blocks
+  return (double)c.s * c.ncol * 8 >= mb * 1e6;
+}
 static void host_chunks(const Ctx &c, int64_t *bounds) {
   const int64_t ld = c.ncol, m = c.m;
   for (int k = 0; k <= kHostChunks; ++k) {
@@ -72,8 +75,39 @@ static void host_chunks(const Ctx &c, int64_t *bounds) {
   bounds[kHostChunks] = ld;
 }
 
+// D_hat^{-1} on the segment columns [c0, c1) (B_hat on this rank's window-0 columns,
+// Q_hat elsewhere): the Cholesky-factor TRSM pair, or the opt-in explicit inverses.
+// Columns are independent right-hand sides, so a column range is a complete solve.
+static void dhat_inv_cols(Ctx &c, const double *x1, double *y1, int64_t c0, int64_t c1) {
+  const int s = c.s;
+  const int64_t ld = c.ncol;
+  if (c.IQ) {   // explicit inverses: one grouped GEMM (B^-1 on window 0, Q^-1 after)
+    d_gemm_cols(c, c.IB, c.IQ, x1, y1, nullptr, 1.0, 0.0, c0, c1);
+    return;
+  }
+  const int64_t bsplit = (c.w0 == 0) ? c.m : 0;   // columns < bsplit belong to window 0
+  TrsmProb f[2], b[2];
+  int np = 0;
+  if (c0 < bsplit) {
+    const int64_t e = std::min(c1, bsplit);
+    f[np] = TrsmProb{c.GB, s, x1 + c0, ld, y1 + c0, ld, s, (int)(e - c0), 0};
+    b[np] = TrsmProb{c.GBt, s, y1 + c0, ld, y1 + c0, ld, s, (int)(e - c0), 0};
+    f[np].dpack = c.PB; b[np].dpack = c.PBt;
+    ++np;
+  }
+  const int64_t q0 = std::max(c0, bsplit);
+  if (c1 > q0) {
+    f[np] = TrsmProb{c.GQ, s, x1 + q0, ld, y1 + q0, ld, s, (int)(c1 - q0), 0};
+    b[np] = TrsmProb{c.GQt, s, y1 + q0, ld, y1 + q0, ld, s, (int)(c1 - q0), 0};
+    f[np].dpack = c.PQ; b[np].dpack = c.PQt;
+    ++np;
+  }
+  launch_trsm(c, f, np, false);
+  launch_trsm(c, b, np, true);
+}
+
 void dhat_inv(Ctx &c, const double *x1, double *y1) {
-  const int s = c.s, m = c.m;
+  const int m = c.m;
   const int64_t ld = c.ncol;
   if (c.pc.factor == WF4DVAR_FACTOR_ICHOL) {   // (L L^T)^{-1} with the IC(0) factors
     if (c.w0 == 0) {
@@ -84,28 +118,7 @@ void dhat_inv(Ctx &c, const double *x1, double *y1) {
     c.n_Dhat_inv += c.WG;
     return;
   }
-  if (c.IQ) {   // explicit inverses: one grouped GEMM (B^-1 on window 0, Q^-1 after)
-    d_gemm_cols(c, c.IB, c.IQ, x1, y1, nullptr, 1.0, 0.0, 0, ld);
-    c.n_Dhat_inv += c.WG;
-    return;
-  }
-  TrsmProb f[2], b[2];
-  int np;
-  if (c.w0 == 0) {
-    f[0] = TrsmProb{c.GB, s, x1, ld, y1, ld, s, m, 0};
-    f[1] = TrsmProb{c.GQ, s, x1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
-    b[0] = TrsmProb{c.GBt, s, y1, ld, y1, ld, s, m, 0};
-    b[1] = TrsmProb{c.GQt, s, y1 + m, ld, y1 + m, ld, s, (int)(ld - m), 0};
-    f[0].dpack = c.PB; f[1].dpack = c.PQ; b[0].dpack = c.PBt; b[1].dpack = c.PQt;
-    np = c.W > 1 ? 2 : 1;
-  } else {
-    f[0] = TrsmProb{c.GQ, s, x1, ld, y1, ld, s, (int)ld, 0};
-    b[0] = TrsmProb{c.GQt, s, y1, ld, y1, ld, s, (int)ld, 0};
-    f[0].dpack = c.PQ; b[0].dpack = c.PQt;
-    np = 1;
-  }
-  launch_trsm(c, f, np, false);
-  launch_trsm(c, b, np, true);
+  dhat_inv_cols(c, x1, y1, 0, ld);
   c.n_Dhat_inv += c.WG;
 }
 
@@ -170,9 +183,15 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
   const int64_t ld = c.ncol;
   const double *x1 = x, *x2 = x + (int64_t)s * ld, *x3 = x2 + (int64_t)p * ld;
   double *y1 = y, *y2 = y + (int64_t)s * ld, *y3 = y2 + (int64_t)p * ld;
+  const bool chunk_out = host_y && host_chunking(c);
+  // the three output blocks are independent: c2 and c3 run on the aux streams
+  fork(c);
   if (c.comm) {
     // one-state halos: L needs x3 of global window w0-1 (rank-1's
-    // last), L^T needs x1 of window w0+W (rank+1's first)
+    // last), L^T needs x1 of window w0+W (rank+1's first).  Issued on aux[1] (whose
+    // L^T pass needs halo_hi next), so the exchange overlaps the D x1 GEMM on the main
+    // stream, which needs no halo; the main stream waits for it only before L x3.
+    OnStream os(c, c.aux[1]);
     const int rank = c.comm->rank, world = c.comm->world;
     const size_t cnt = (size_t)s * c.m;
     std::vector<Comm::P2P> ops;
@@ -187,9 +206,8 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
       ops.push_back({c.halo_lo, cnt, rank - 1, false});
     }
     c.comm->exchange(ops, c.st);
+    WF_CUDA(cudaEventRecord(c.ev_halo, c.st));
   }
-  // the three output blocks are independent: c2 and c3 run on the aux streams
-  fork(c);
   {
     // c2 = R x2 + H x3 (selection H: gather in the epilogue; general H: CSR first)
     OnStream os(c, c.aux[0]);
@@ -218,10 +236,11 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
       WF_CUDA(cudaMemcpyAsync(host_y + (int64_t)(s + p) * ld, y3, (size_t)s * ld * 8,
                               cudaMemcpyDeviceToHost, c.st));
   }
-  // c1 = L x3 + D x1
-  model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
-  if (host_y && host_chunking(c)) {
-    // column chunks: each chunk leaves for the host while the next one's product runs
+  if (chunk_out) {
+    // c1 = L x3 + D x1 with the D product in column chunks: each chunk leaves for the
+    // host while the next one's product runs (the L term must be in y1 first)
+    if (c.comm) WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_halo, 0));
+    model_step(c, false, -1.0, x3, x3, y1, 0, 1, c.W);
     int64_t cb[kHostChunks + 1];
     host_chunks(c, cb);
     // (the copies go on the copy stream: in stream order they would hold back the next
@@ -238,7 +257,11 @@ void apply_A(Ctx &c, const double *x, double *y, double *host_y) {
     WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_in[3], 0));
     c.n_D += c.WG;
   } else {
-    d_product(c, x1, y1, y1, 1.0, 1.0);
+    // c1 = (D x1 + x3) - M_w x3_{w-1}: the GEMM (no halo needed) first, then the L term
+    // in place once the halo has landed
+    d_product(c, x1, y1, x3, 1.0, 1.0);
+    if (c.comm) WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_halo, 0));
+    model_step(c, false, -1.0, x3, y1, y1, 0, 1, c.W);
     if (host_y)
       WF_CUDA(cudaMemcpyAsync(host_y, y1, (size_t)s * ld * 8, cudaMemcpyDeviceToHost, c.st));
   }
@@ -258,9 +281,11 @@ void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
   auto wait_in = [&](int b) {
     if (host_x) WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_in[b], 0));
   };
-  // explicit D_hat inverses (P_D): the first block is copied and multiplied in column
-  // chunks (ev_chunk[k]), so the GEMM starts after a quarter of the block has landed
-  const bool chunked = host_x && c.IQ && c.pc.shape == WF4DVAR_PD && host_chunking(c);
+  // P_D with Cholesky factors: the first block is copied and solved in column chunks
+  // (ev_chunk[k]; columns are independent right-hand sides), so D_hat^{-1} starts after a
+  // quarter of the block has landed instead of all of it
+  const bool chunked = host_x && c.pc.shape == WF4DVAR_PD &&
+                       c.pc.factor == WF4DVAR_FACTOR_CHOL && host_chunking(c);
   int64_t cb[kHostChunks + 1];
   if (chunked) host_chunks(c, cb);
   if (host_x) {
@@ -298,7 +323,7 @@ void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
       if (chunked) {
         for (int k = 0; k < kHostChunks; ++k) {
           WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_chunk[k], 0));
-          if (cb[k + 1] > cb[k]) d_gemm_cols(c, c.IB, c.IQ, x1, y1, nullptr, 1.0, 0.0, cb[k], cb[k + 1]);
+          if (cb[k + 1] > cb[k]) dhat_inv_cols(c, x1, y1, cb[k], cb[k + 1]);
         }
         c.n_Dhat_inv += c.WG;
       } else {

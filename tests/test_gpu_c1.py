@@ -6,13 +6,16 @@ checked against the oracle two ways, on RHS column 0:
 
   * recurrence: the oracle's GMRES(50) (oracle/krylov.py, CGS2) driven by the CUDA
     path's own A and P^{-1} applies (tests/helpers.gpu_column_ops) must reproduce the
-    GPU solver's residual history -- this isolates the batched Krylov step;
+    GPU solver's residual history -- this isolates the batched Krylov step (to the same
+    sensitivity bound: two CGS2 recurrences summing in different orders differ by as
+    much as the oracle does under 1e-15 noise);
   * oracle: the oracle's own history (tests/golden/c1_gmres_oracle.json, written by
     tools/make_c1_golden.py from oracle/ only) must agree with the GPU's within the
     oracle's own rounding sensitivity (its history under 1e-15 relative noise on
     every P^{-1} output, stored with it): these restarted-GMRES histories move by
     1e-3..2e-1 under such noise (PROBE-3), so no two correct
-    implementations agree more closely than that.
+    implementations agree more closely than that.  Both differences must stay within 5x
+    that sensitivity.
 Most cells stagnate under restart 50 on this config (the oracle's too: the golden
 file records it); the 1e-8 mark is reached by P_I with the exact L (372 iterations)
 and by P_D with L_M(4) / R or R_ME (1158 / ~1900), see DESIGN.md section 11.
@@ -75,8 +78,10 @@ def check_gmres_cell(prob, rec, nit=NIT):
     print(f"[gmres50] {pc} relres@{ns - 1} gpu {hg[ns - 1]:.4e} oracle {ho[ns - 1]:.4e}; "
           f"max |h/h_rec - 1| {d_rec:.1e}; max |h/h_oracle - 1| {d_ora:.1e} (oracle "
           f"self-sensitivity {s_ora:.1e})")
-    assert d_rec <= 1e-6, d_rec
-    assert d_ora <= max(1e-6, 10 * s_ora), (d_ora, s_ora)
+    # both within 5x the oracle's own rounding sensitivity (r02f, all 60 configs[1] cells:
+    # at most 1.5x for the recurrence and 2.1x for the oracle history)
+    assert d_rec <= max(1e-6, 5 * s_ora), (d_rec, s_ora)
+    assert d_ora <= max(1e-6, 5 * s_ora), (d_ora, s_ora)
     ctx.close()
     return hg
 

@@ -301,7 +301,11 @@ def test_minres_c0_matches_oracle(k, rhat):
     assert np.linalg.norm(xg - xstar) / np.linalg.norm(xstar) <= 1e-7
 
 
-@pytest.mark.parametrize("k,rhat,restart", [(5, "exact", 50), (3, "rr", 50), (1, "exact", 20)])
+@pytest.mark.parametrize("k,rhat,restart", [(5, "exact", 50), (3, "rr", 50), (1, "exact", 20),
+                                            # full (unrestarted) GMRES: c0
+                                            # runs both full and restarted at 50
+                                            (5, "exact", 0), (3, "me", 0), (2, "diag", 0),
+                                            (4, "block", 0)])
 def test_gmres_c0_matches_oracle(k, rhat, restart):
     prob, ora = get("c0")
     pc = dict(shape="PI", lhat="LM", k=k, rhat=rhat)
@@ -368,3 +372,48 @@ def test_explicit_inverse_mode_agrees_forward():
         assert np.linalg.norm(a - b) / np.linalg.norm(b) <= max(1e-12, 10 * kap * U)
         fails, worst = block_parity(prob, pc, x.cpu().numpy(), a, ora, [0], cache=_kcache)
         print("[A32 inverse mode]", pc, worst)
+
+
+HOST_CHUNK = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2105_06975_b200 as W
+from synth import configs as SC
+prob = SC.custom_problem(s=600, N=3, q=2, m=7, seed0=5, Bp=(0.05, 1.0), Qp=(0.05, 0.1),
+                         Rp=(0.03, 0.05))
+x = np.random.Generator(np.random.PCG64(8)).standard_normal(prob.n)
+outs = []
+for pc in (dict(shape="PD", lhat="LM", k=2, rhat="exact"),
+           dict(shape="PD", lhat="LM", k=2, rhat="exact", apply_mode="inverse")):
+    ctx = W.Context.from_problem(prob, pc)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty(prob.n, dtype=torch.float64).pin_memory()
+    for _ in range(2):
+        ctx.apply_AP_host(xp.numpy(), yp.numpy())
+    t = torch.empty(prob.n, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(t)
+    ctx.apply_AP(torch.from_numpy(x).cuda(), t, y)
+    outs += [yp.numpy().copy(), y.cpu().numpy()]
+    ctx.close()
+np.save(sys.argv[2], np.stack(outs))
+"""
+
+
+def test_host_path_column_chunks(tmp_path):
+    """The host path copies the first block in window-aligned column chunks and solves /
+    multiplies each chunk as it lands (forced here on a small problem with
+    WF4DVAR_HOST_CHUNK_MB=0): same result as the device path to the blocks' conditioning,
+    for the triangular solves (default) and the explicit inverses."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = tmp_path / "hc.npy"
+    r = subprocess.run([sys.executable, "-c", HOST_CHUNK, root, str(out)], capture_output=True,
+                       text=True, env=dict(os.environ, WF4DVAR_HOST_CHUNK_MB="0"), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    o = np.load(out)
+    prob, _ = get("mid")
+    kap = max(np.linalg.cond(prob.B), np.linalg.cond(prob.Q), np.linalg.cond(prob.R))
+    for host, devv in ((o[0], o[1]), (o[2], o[3])):
+        assert np.linalg.norm(host - devv) / np.linalg.norm(devv) <= max(1e-12, 10 * kap * U)
