@@ -7,6 +7,9 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "dmma.cuh"
 #include "internal.h"
 
@@ -323,6 +326,128 @@ __global__ void __launch_bounds__(C::NT) k_gemm_bulk(const GemmLaunch L) {
   tile_epilogue<C>(Pb, m0, n0, acc);
 }
 
+// ------------------------------------------------------------------ 2-D TMA staging
+// The same 64x128 / 4-warp DMMA tile with each operand tile staged by ONE 2-D tensor
+// copy per stage (cp.async.bulk.tensor, SASS UTMALDG) instead of 12 bounds-checked
+// cp.async per thread: the SASS of the cp.async main loop spends ~6 integer
+// instructions per DMMA on addresses and bounds (r02 count: 2400 IMAD/LEA/IADD3/ISETP
+// per 384 DMMA), which is what keeps the DMMA pipe below cuBLAS's.  The padded,
+// conflict-free fragment layout is kept without swizzling: the A box is BK + 4 = 20
+// columns wide and the X box BN + 4 = 132, so the shared row strides are exactly LDA /
+// LDB (the 4 extra columns are real data of the neighbouring k / n tile, never read by
+// the DMMAs; past the matrix edge the TMA unit zero-fills, which also covers ragged M,
+// N and K without a single bounds check in the kernel).  Stage s is armed by thread 0
+// (expect_tx = both boxes' bytes) and refilled by it once every warp has released it
+// (one "empty" arrival per warp).
+struct TmaMaps {
+  CUtensorMap a[2], x[2];   // per group: A (M x K) and X (K x N), row-major doubles
+};
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"((unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT) k_gemm_tma(const GemmLaunch L,
+                                                   const __grid_constant__ TmaMaps T) {
+  extern __shared__ __align__(1024) double smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::SMEM_DOUBLES);
+  uint64_t *empty = full + C::STAGES;
+  int gi, m0, n0;
+  tile_coords<C>(L, blockIdx.x, gi, m0, n0);
+  const GemmProb &P = L.p[gi];
+  const CUtensorMap *ma = &T.a[gi], *mx = &T.x[gi];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int nk = (P.K + C::BK - 1) / C::BK;
+  constexpr unsigned kBytes = (unsigned)(C::STAGE * sizeof(double));
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], C::NWARP);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int kt) {   // thread 0
+    const int s = kt % C::STAGES;
+    double *sA = smem + s * C::STAGE, *sB = sA + C::A_STAGE;
+    mbar_arrive_expect_tx(&full[s], kBytes);
+    tma_load_2d(sA, ma, kt * C::BK, m0, &full[s]);
+    tma_load_2d(sB, mx, n0, kt * C::BK, &full[s]);
+  };
+  if (tid == 0)
+    for (int kt = 0; kt < C::STAGES - 1 && kt < nk; ++kt) issue(kt);
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kt = 0; kt < nk; ++kt) {
+    if (tid == 0 && kt + C::STAGES - 1 < nk) {
+      const int kn = kt + C::STAGES - 1;
+      if (kn >= C::STAGES) mbar_wait(&empty[kn % C::STAGES], ((kn / C::STAGES) - 1) & 1);
+      issue(kn);
+    }
+    const int s = kt % C::STAGES;
+    mbar_wait(&full[s], (kt / C::STAGES) & 1);
+    const double *st = smem + s * C::STAGE;
+    mma_stage<C>(st, st + C::A_STAGE, acc, wm, wn, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+  tile_epilogue<C>(P, m0, n0, acc);
+}
+
+// host: encode the 2-D tensor maps of one problem (row-major, 16-byte aligned rows)
+static bool encode_tma(CUtensorMap *map, const double *base, int64_t rows, int64_t cols,
+                       int64_t ld, unsigned box_cols, unsigned box_rows) {
+  static PFN_cuTensorMapEncodeTiled fn = []() -> PFN_cuTensorMapEncodeTiled {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(f);
+  }();
+  if (!fn || ((uintptr_t)base & 15) || (ld & 1) || rows < 1 || cols < 1) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+// Y = A X (+ Z) for the tiles [0, tiles) of L through k_gemm_tma; false (nothing
+// launched) when a problem does not meet the TMA alignment rules or is banded/batched
+template <class C>
+static bool run_tma(Ctx &c, const GemmLaunch &L, int nprob, int tiles) {
+  static const int env = env_int("WF4DVAR_GEMM_TMA", 1);
+  if (!env || tiles <= 0) return false;
+  TmaMaps T{};
+  for (int i = 0; i < nprob; ++i) {
+    const GemmProb &p = L.p[i];
+    if (p.kr) return false;
+    if (!encode_tma(&T.a[i], p.A, p.M, p.K, p.lda, C::BK + 4, C::BM)) return false;
+    if (!encode_tma(&T.x[i], p.X, p.K, p.N, p.ldx, C::BN + 4, C::BK)) return false;
+  }
+  const size_t smem = C::SMEM_DOUBLES * sizeof(double) + 2 * C::STAGES * sizeof(uint64_t);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_gemm_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  WF_CUDA(attr);
+  k_gemm_tma<C><<<tiles, C::NT, smem, c.st>>>(L, T);
+  WF_CUDA(cudaGetLastError());
+  return true;
+}
+
 // Large problems: 64x128 CTA tile, 4 warps of 32x64 (32 independent DMMA
 // accumulator tiles per warp per k-step), BK = 16, 3-stage cp.async ring,
 // 81 KB smem -> 2 CTAs (8 warps) per SM.  Chosen by measurement (tools/kbench.py,
@@ -428,10 +553,12 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
     WF_CUDA(attr);
     S.dp_begin = 0;
     if (sk_env != 2 && S.dp_tiles > 0) {
-      static const cudaError_t attr_dp = cudaFuncSetAttribute(k_gemm<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      WF_CUDA(attr_dp);
-      k_gemm<C, true><<<dim3(S.dp_tiles, 1, 1), C::NT, smem, c.st>>>(L);   // tiles [0, dp_tiles)
-      WF_CUDA(cudaGetLastError());
+      if (!run_tma<C>(c, L, nprob, S.dp_tiles)) {
+        static const cudaError_t attr_dp = cudaFuncSetAttribute(k_gemm<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        WF_CUDA(attr_dp);
+        k_gemm<C, true><<<dim3(S.dp_tiles, 1, 1), C::NT, smem, c.st>>>(L);   // tiles [0, dp_tiles)
+        WF_CUDA(cudaGetLastError());
+      }
       c.launches++;
       S.dp_begin = S.dp_tiles;
     }
@@ -457,6 +584,9 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
       WF_CUDA(cudaGetLastError());
       return;
     }
+  }
+  if constexpr (C::BM == 64 && C::BN == 128 && C::BK == 16 && C::STAGES == 3) {
+    if (batch == 1 && !banded && run_tma<C>(c, L, nprob, tiles)) return;
   }
   dim3 grid(tiles, 1, batch);
   if (v16) {

@@ -186,16 +186,27 @@ def gpu_column_ops(ctx, prob, col=0):
     apply is column-wise, so the other columns do not touch it).  Feeding these into
     the oracle's Krylov recurrence (oracle/krylov.py) isolates the recurrence from the
     operators' rounding: the oracle's count with the GPU's applies must equal the
-    GPU solver's count to +-1 (reading A33)."""
+    GPU solver's count to +-1 (reading A33).  The column's library-layout
+    positions are scattered / gathered on the device (no full-batch transposes)."""
     import torch
     s, p, W, m = prob.s, prob.p, prob.W, prob.m
+    # library index of each paper-order entry of column `col` (pure index permutation:
+    # paper order is window-major per segment, the library's [len][W][m])
+    segs = []
+    off = 0
+    for ln in (s, p, s):
+        i, w = np.meshgrid(np.arange(ln), np.arange(W), indexing="ij")
+        segs.append((off + (i * W + w) * m + col).T.reshape(-1))
+        off += ln * W * m
+    lib_of = np.concatenate(segs)
+    ti = torch.from_numpy(lib_of).cuda()
+    xd = torch.zeros(prob.n, dtype=torch.float64, device="cuda")
+    yd = torch.empty_like(xd)
 
     def run(fn, v):
-        mat = np.zeros((m, v.size))
-        mat[col] = v
-        xd = torch.from_numpy(from_paper_order(mat, s, p, W)).cuda()
-        y = torch.empty_like(xd)
-        fn(xd, y)
+        xd.zero_()
+        xd[ti] = torch.from_numpy(np.ascontiguousarray(v)).cuda()
+        fn(xd, yd)
         torch.cuda.synchronize()
-        return to_paper_order(y.cpu().numpy(), s, p, W, m)[col]
+        return yd[ti].cpu().numpy()
     return (lambda v: run(ctx.apply_A, v)), (lambda v: run(ctx.apply_P, v))

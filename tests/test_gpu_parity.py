@@ -308,7 +308,7 @@ def test_minres_c0_matches_oracle(k, rhat):
                                             (4, "block", 0)])
 def test_gmres_c0_matches_oracle(k, rhat, restart):
     prob, ora = get("c0")
-    pc = dict(shape="PI", lhat="LM", k=k, rhat=rhat)
+    pc = dict(shape="PI", lhat="LM", k=k, rhat=rhat, block=5 if rhat == "block" else 0)
     ctx = W4().Context.from_problem(prob, pc)
     b = dev(prob.rhs)
     x = torch.empty_like(b)

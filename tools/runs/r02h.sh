@@ -6,6 +6,7 @@ TAG=r02h
 mkdir -p gpurun_out
 export WF4DVAR_PROBLEM_CACHE=/tmp/wfpc_$TAG
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_dist.py tests/test_gpu_nccl1.py tests/test_gpu_paper_heat.py tests/test_gpu_parity.py -q -rf -k "dist or sharded or nccl or host or apply_A or AP" > gpurun_out/pytest_dist_$TAG.log 2>&1; echo "pytest_dist=$?" >> gpurun_out/status_$TAG
 for cfg in 0 1 2 5; do
 timeout 900 python bench.py --config $cfg > gpurun_out/bench_c${cfg}_$TAG.log 2>&1; echo "c$cfg=$?" >> gpurun_out/status_$TAG
 done
