@@ -1,12 +1,14 @@
 #!/bin/bash
-# r02h: bench lines for every config, shard projections (one shard's windows of
+# r02h (after the TMA GEMM): full-GMRES diagnosis on c0, c3 time-to-1e-8 for both apply
+# modes, bench lines for every config, shard projections (one shard's windows of
 # configs[3] at N+1 = 64/32/16), the reference arm, ncu launch list + GEMM capture
 # (roofline.traffic) + heat-scan capture of the default c3 step.
 TAG=r02h
 mkdir -p gpurun_out
 export WF4DVAR_PROBLEM_CACHE=/tmp/wfpc_$TAG
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
-timeout 1200 python -m pytest tests/test_gpu_dist.py tests/test_gpu_nccl1.py tests/test_gpu_paper_heat.py tests/test_gpu_parity.py -q -rf -k "dist or sharded or nccl or host or apply_A or AP" > gpurun_out/pytest_dist_$TAG.log 2>&1; echo "pytest_dist=$?" >> gpurun_out/status_$TAG
+timeout 900 python tools/gmres_full_diag.py > gpurun_out/gmres_full_diag_$TAG.log 2>&1; echo "diag=$?" >> gpurun_out/status_$TAG
+timeout 1500 python tools/tts.py --config 3 --maxit 3000 --out gpurun_out/tts_c3_$TAG.json > gpurun_out/tts_c3_$TAG.log 2>&1; echo "tts=$?" >> gpurun_out/status_$TAG
 for cfg in 0 1 2 5; do
 timeout 900 python bench.py --config $cfg > gpurun_out/bench_c${cfg}_$TAG.log 2>&1; echo "c$cfg=$?" >> gpurun_out/status_$TAG
 done
