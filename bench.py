@@ -385,6 +385,24 @@ def main():
     prof = ctx.profile_read()
     ctx.profile_enable(False)
 
+    # the two operator applies alone (device buffers, CUDA events on the library stream):
+    # where a step's time goes between A and P (the rest is the Krylov vector work)
+    phases = {}
+    if ws == 1:
+        xa = torch.from_numpy(np.random.Generator(np.random.PCG64(6)).standard_normal(n_local)).to(dev)
+        ya = torch.empty_like(xa)
+        for name, fn in (("apply_A", ctx.apply_A), ("apply_P", ctx.apply_P)):
+            with torch.cuda.stream(stream):
+                fn(xa, ya)
+                q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                q0.record(stream)
+                for _ in range(5):
+                    fn(xa, ya)
+                q1.record(stream)
+            torch.cuda.synchronize(dev)
+            phases[name + "_ms"] = q0.elapsed_time(q1) / 5
+        del xa, ya
+
     # end-to-end: the public API with HOST buffers (H2D + A+P + D2H every step)
     xh = torch.from_numpy(np.random.Generator(np.random.PCG64(5)).standard_normal(n_local)).pin_memory()
     yh = torch.empty(n_local, dtype=torch.float64).pin_memory()
@@ -492,6 +510,7 @@ def main():
                          d2h_bytes_per_step=n_local * 8 * ws,
                          how="wf4dvar_apply_AP_host: pinned host x -> device, A+P, y -> host"),
                 gpu_launches=launches, clocks=clk.summary(), time_to_1e8=tts, kernels=kernels,
+                phases=phases,
                 counters=dict(n_apply_A=rep["n_apply_A"], n_apply_P=rep["n_apply_P"]))
     print(json.dumps(line), flush=True)
 

@@ -130,6 +130,12 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       WF_CUDA(cudaEventCreateWithFlags(&c.ev_join[i], cudaEventDisableTiming));
     }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming));
+    {
+      int lo_pri = 0, hi_pri = 0;
+      WF_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
+      WF_CUDA(cudaStreamCreateWithPriority(&c.aux2, cudaStreamNonBlocking, c.aux_priority ? hi_pri : 0));
+      for (auto &e : c.ev_split) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_halo, cudaEventDisableTiming));
     WF_CUDA(cudaStreamCreateWithFlags(&c.cpy, cudaStreamNonBlocking));
     for (auto &e : c.ev_in) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -240,6 +246,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (c.ev_join[i]) cudaEventDestroy(c.ev_join[i]);
   }
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
+  if (c.aux2) { cudaStreamSynchronize(c.aux2); cudaStreamDestroy(c.aux2); }
+  for (auto &e : c.ev_split) if (e) cudaEventDestroy(e);
   if (c.ev_halo) cudaEventDestroy(c.ev_halo);
   if (c.cpy) { cudaStreamSynchronize(c.cpy); cudaStreamDestroy(c.cpy); }
   for (auto &e : c.ev_in) if (e) cudaEventDestroy(e);

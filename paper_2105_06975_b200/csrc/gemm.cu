@@ -585,7 +585,7 @@ static void run(Ctx &c, const GemmProb *probs, int nprob, int batch, bool v16) {
       return;
     }
   }
-  if constexpr (C::BM == 64 && C::BN == 128 && C::BK == 16 && C::STAGES == 3) {
+  if constexpr (C::BK == 16) {   // every BK = 16 tile shape (64x128, 128x64, 64x32)
     if (batch == 1 && !banded && run_tma<C>(c, L, nprob, tiles)) return;
   }
   dim3 grid(tiles, 1, batch);

@@ -215,6 +215,8 @@ struct Ctx {
   cudaStream_t st = nullptr;
   // fork/join streams: the three independent blocks of A and of P_D run concurrently
   cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaStream_t aux2 = nullptr;     // second column half of D_hat^{-1} (see dhat_inv)
+  cudaEvent_t ev_split[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   cudaEvent_t ev_halo = nullptr;   // apply_A's halo exchange done (aux[1] -> main)
   cudaStream_t cpy = nullptr;          // host path: block-wise H2D of apply_P's input

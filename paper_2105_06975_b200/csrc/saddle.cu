@@ -59,20 +59,27 @@ static void d_product(Ctx &c, const double *X, double *Y, const double *Z, doubl
 // Host path: the segment's columns in kHostChunks window-aligned chunks, so the first
 // block's copies and products pipeline (chunk k's product runs while chunk k+1 is on
 // the link).
-constexpr int kHostChunks = 4;
+constexpr int kHostChunks = 4;   // maximum; apply_P's D_hat^{-1} input uses host_nchunks()
+static int host_nchunks() {
+  // r02j (configs[3] e2e, applies/s): 4 chunks 26.09, 2 chunks 26.94, 1 chunk 26.65;
+  // sending x3 before x1: 23.96 -- halves keep the triangular solves wide
+  static const int v = std::max(1, std::min(kHostChunks, env_int("WF4DVAR_HOST_CHUNKS", 2)));
+  return v;
+}
 // only worth it when a block's copy is long against the per-chunk launch latencies
 // (configs[3]: 268 MB per block, 4.9 ms over PCIe; configs[1]: 2.7 MB)
 static bool host_chunking(const Ctx &c) {
   static const int mb = env_int("WF4DVAR_HOST_CHUNK_MB", 64);   // tests force it on small blocks
   return (double)c.s * c.ncol * 8 >= mb * 1e6;
 }
-static void host_chunks(const Ctx &c, int64_t *bounds) {
+static void host_chunks(const Ctx &c, int64_t *bounds, int n = kHostChunks) {
   const int64_t ld = c.ncol, m = c.m;
   for (int k = 0; k <= kHostChunks; ++k) {
-    int64_t b = (ld * k / kHostChunks + m - 1) / m * m;   // window-aligned
-    bounds[k] = std::min(ld, b);
+    int64_t b = (ld * std::min(k, n) / n + m - 1) / m * m;   // window-aligned
+    bounds[k] = std::min(ld, b);                              // chunks >= n are empty
   }
-  bounds[kHostChunks] = ld;
+  bounds[n] = ld;
+  for (int k = n; k <= kHostChunks; ++k) bounds[k] = ld;
 }
 
 // D_hat^{-1} on the segment columns [c0, c1) (B_hat on this rank's window-0 columns,
@@ -118,7 +125,26 @@ void dhat_inv(Ctx &c, const double *x1, double *y1) {
     c.n_Dhat_inv += c.WG;
     return;
   }
-  dhat_inv_cols(c, x1, y1, 0, ld);
+  // wide right-hand sides: the two column halves' triangular-solve pairs on two streams
+  // (columns are independent), so one half's latency-bound panels and short-K coupling
+  // GEMMs overlap the other half's work instead of leaving SMs idle
+  // opt-in: r02j measured the configs[3] step 29.92 -> 30.64 ms with the split (the
+  // halves' narrower panels cost more than the overlap gains)
+  static const int split_env = env_int("WF4DVAR_DHAT_SPLIT", 0);
+  if (split_env && !c.IQ && ld >= 4096 && !c.prof.on && c.fork_on) {
+    const int64_t half = (ld / 2 + m - 1) / m * m;   // window-aligned
+    WF_CUDA(cudaEventRecord(c.ev_split[0], c.st));
+    WF_CUDA(cudaStreamWaitEvent(c.aux2, c.ev_split[0], 0));
+    dhat_inv_cols(c, x1, y1, 0, half);
+    {
+      OnStream os(c, c.aux2);
+      dhat_inv_cols(c, x1, y1, half, ld);
+      WF_CUDA(cudaEventRecord(c.ev_split[1], c.st));
+    }
+    WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_split[1], 0));
+  } else {
+    dhat_inv_cols(c, x1, y1, 0, ld);
+  }
   c.n_Dhat_inv += c.WG;
 }
 
@@ -287,13 +313,18 @@ void apply_P(Ctx &c, const double *x, double *y, const double *host_x) {
   const bool chunked = host_x && c.pc.shape == WF4DVAR_PD &&
                        c.pc.factor == WF4DVAR_FACTOR_CHOL && host_chunking(c);
   int64_t cb[kHostChunks + 1];
-  if (chunked) host_chunks(c, cb);
+  if (chunked) host_chunks(c, cb, host_nchunks());
   if (host_x) {
     WF_CUDA(cudaEventRecord(c.ev_in[3], c.st));
     WF_CUDA(cudaStreamWaitEvent(c.cpy, c.ev_in[3], 0));
     const int64_t off[3] = {0, (int64_t)(s + p) * ld, (int64_t)s * ld};
     const int64_t len[3] = {(int64_t)s * ld, (int64_t)s * ld, (int64_t)p * ld};
-    for (int b = 0; b < 3; ++b) {
+    // copy order: x1 (D_hat^{-1}), x3 (S_hat^{-1} / L_hat chain), x2; env
+    // WF4DVAR_HOST_X3_FIRST=1 sends x3 first (tuning)
+    static const int x3_first = env_int("WF4DVAR_HOST_X3_FIRST", 0);
+    const int order[3] = {x3_first ? 1 : 0, x3_first ? 0 : 1, 2};
+    for (int bi = 0; bi < 3; ++bi) {
+      const int b = order[bi];
       if (b == 0 && chunked) {
         for (int k = 0; k < kHostChunks; ++k) {
           if (cb[k + 1] > cb[k])
