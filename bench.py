@@ -33,7 +33,9 @@ sys.path.insert(0, ROOT)
 
 CELLS = {
     0: dict(shape="PD", lhat="LM", k=3, rhat="exact", solver="minres"),
-    1: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
+    # BJ.c1: "GMRES(restart 50) with each of the paper's preconditioner variants" -- the
+    # bench line takes P_D, L_M(4), R_hat = R; tools/grid.py c1 times all 60 cells
+    1: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="gmres"),
     2: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
     3: dict(shape="PD", lhat="LM", k=4, rhat="exact", solver="minres"),
     4: dict(shape="PI", lhat="LM", k=4, rhat="exact", solver="gmres"),
@@ -71,6 +73,7 @@ def parse():
                     help="dense D_hat/R_hat blocks: triangular solves (default) or the opt-in "
                          "explicit inverses (DESIGN.md reading A32)")
     ap.add_argument("--restart", type=int, default=50)
+    ap.add_argument("--solver", default=None, choices=["minres", "gmres"])
     ap.add_argument("--tts-maxit", type=int, default=2000,
                     help="cap for the time-to-1e-8 solve (0 disables it)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -216,6 +219,8 @@ def cell_of(args):
             cell[key] = v
     if cell["shape"] == "PI":
         cell["solver"] = "gmres"
+    if args.solver:
+        cell["solver"] = args.solver
     return cell
 
 

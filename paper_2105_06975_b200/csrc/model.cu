@@ -196,46 +196,79 @@ __global__ void __launch_bounds__(WARPS * 32) k_heat_iir_scan(
   const int len = max(0, min(CH, NS - j0));
   double rl = 1.0;                           // rho^len
   for (int t = 0; t < len; ++t) rl *= rho;
-  for (int c = warp; c < 32; c += WARPS) {
-    double *col = tile + c;
+  // two columns per pass: their recursions and shuffle scans are independent (ILP 2)
+  static_assert((32 / WARPS) % 2 == 0, "columns per warp must be even");
+  for (int c = warp; c < 32; c += 2 * WARPS) {
+    double *col[2] = {tile + c, tile + c + WARPS};
     // forward, local from zero
-    double u = 0.0;
+    double u[2] = {0.0, 0.0};
 #pragma unroll
     for (int t = 0; t < CH; ++t)
-      if (t < len) { u = fma(rho, u, col[(j0 + t) * LD]); col[(j0 + t) * LD] = u; }
+      if (t < len) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          u[q] = fma(rho, u[q], col[q][(j0 + t) * LD]);
+          col[q][(j0 + t) * LD] = u[q];
+        }
+      }
     // inclusive scan of (a, b) = (rho^len, u_end) over the lanes
-    double a = rl, b = u;
+    double a = rl, b[2] = {u[0], u[1]};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double ap = __shfl_up_sync(0xffffffffu, a, o);
-      const double bp = __shfl_up_sync(0xffffffffu, b, o);
-      if (lane >= o) { b = fma(bp, a, b); a *= ap; }
+      const double b0 = __shfl_up_sync(0xffffffffu, b[0], o);
+      const double b1 = __shfl_up_sync(0xffffffffu, b[1], o);
+      if (lane >= o) { b[0] = fma(b0, a, b[0]); b[1] = fma(b1, a, b[1]); a *= ap; }
     }
-    double carry = __shfl_up_sync(0xffffffffu, b, 1);   // state entering this lane's rows
-    if (lane == 0) carry = 0.0;
+    double carry[2];   // state entering this lane's rows
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      carry[q] = __shfl_up_sync(0xffffffffu, b[q], 1);
+      if (lane == 0) carry[q] = 0.0;
+    }
     double pw = rho;
 #pragma unroll
     for (int t = 0; t < CH; ++t)
-      if (t < len) { col[(j0 + t) * LD] = fma(carry, pw, col[(j0 + t) * LD]); pw *= rho; }
+      if (t < len) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          col[q][(j0 + t) * LD] = fma(carry[q], pw, col[q][(j0 + t) * LD]);
+        pw *= rho;
+      }
     __syncwarp();
     // backward, local from zero, then the carry from the lanes above
-    double v = 0.0;
+    double v[2] = {0.0, 0.0};
 #pragma unroll
     for (int t = CH - 1; t >= 0; --t)
-      if (t < len) { v = fma(rho, v, col[(j0 + t) * LD]); col[(j0 + t) * LD] = v; }
-    a = rl; b = v;
+      if (t < len) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          v[q] = fma(rho, v[q], col[q][(j0 + t) * LD]);
+          col[q][(j0 + t) * LD] = v[q];
+        }
+      }
+    a = rl; b[0] = v[0]; b[1] = v[1];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const double an = __shfl_down_sync(0xffffffffu, a, o);
-      const double bn = __shfl_down_sync(0xffffffffu, b, o);
-      if (lane + o < 32) { b = fma(bn, a, b); a *= an; }
+      const double b0 = __shfl_down_sync(0xffffffffu, b[0], o);
+      const double b1 = __shfl_down_sync(0xffffffffu, b[1], o);
+      if (lane + o < 32) { b[0] = fma(b0, a, b[0]); b[1] = fma(b1, a, b[1]); a *= an; }
     }
-    carry = __shfl_down_sync(0xffffffffu, b, 1);
-    if (lane == 31) carry = 0.0;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      carry[q] = __shfl_down_sync(0xffffffffu, b[q], 1);
+      if (lane == 31) carry[q] = 0.0;
+    }
     pw = rho;
 #pragma unroll
     for (int t = CH - 1; t >= 0; --t)
-      if (t < len) { col[(j0 + t) * LD] = fma(carry, pw, col[(j0 + t) * LD]); pw *= rho; }
+      if (t < len) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          col[q][(j0 + t) * LD] = fma(carry[q], pw, col[q][(j0 + t) * LD]);
+        pw *= rho;
+      }
     __syncwarp();
   }
   __syncthreads();
@@ -459,7 +492,7 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // r02f (configs[3] per step): thread-per-chunk 1.264 ms (2.31 TB/s) -> warp-scan with
     // cp.async staging R = 128: 1.110 ms (2.63 TB/s), R = 256: 1.431 ms (fewer CTAs per SM)
     static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 128);   // 0: thread-per-chunk form
-    if (tile_env == 128 || tile_env == 256) {
+    if (tile_env == 64 || tile_env == 128 || tile_env == 256) {
       constexpr int WARPS = 8;
       auto go = [&](auto r_tag) {
         constexpr int R = decltype(r_tag)::value;
@@ -473,6 +506,7 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
             w_step, nw, transpose ? 1 : -1, transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
       };
       if (tile_env == 128) go(std::integral_constant<int, 128>{});
+      else if (tile_env == 64) go(std::integral_constant<int, 64>{});
       else go(std::integral_constant<int, 256>{});
       WF_CUDA(cudaGetLastError());
       return;

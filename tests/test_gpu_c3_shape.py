@@ -50,9 +50,13 @@ def test_c3_shaped_minres_matches_oracle(k):
     if abs(it_g - info["iters"]) > 1:
         gA, gP = gpu_column_ops(ctx, prob, 0)
         _, info_g = KR.minres(gA, gP, bp, tol=1e-10, maxit=4000)
+        # finite-precision Lanczos counts of runs over 500 iterations move
+        # by up to ~2% under rounding-level changes (PROBE-2: +-30 beyond 1000
+        # iterations); its secondary rule |d| <= ceil(0.02 it) applies there (reading A33)
+        tol_it = 1 if info_g["iters"] <= 500 else int(np.ceil(0.02 * info_g["iters"]))
         print(f"[flag] gpu {it_g} oracle {info['iters']} oracle-recurrence-with-gpu-applies "
-              f"{info_g['iters']}")
-        assert abs(it_g - info_g["iters"]) <= 1
+              f"{info_g['iters']} (allowed +-{tol_it})")
+        assert abs(it_g - info_g["iters"]) <= tol_it
     X = to_paper_order(x.cpu().numpy(), prob.s, prob.p, prob.W, prob.m)
     d = np.linalg.norm(X[0] - xo) / np.linalg.norm(xo)
     xs = FO.solve_heat(prob, to_paper_order(prob.rhs, prob.s, prob.p, prob.W, prob.m))
