@@ -134,6 +134,9 @@ wf4dvar_status wf4dvar_create(const wf4dvar_problem *prob, const wf4dvar_precond
       int lo_pri = 0, hi_pri = 0;
       WF_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pri, &hi_pri));
       WF_CUDA(cudaStreamCreateWithPriority(&c.aux2, cudaStreamNonBlocking, c.aux_priority ? hi_pri : 0));
+      WF_CUDA(cudaStreamCreateWithFlags(&c.kside, cudaStreamNonBlocking));
+      WF_CUDA(cudaEventCreateWithFlags(&c.ev_kfork, cudaEventDisableTiming));
+      WF_CUDA(cudaEventCreateWithFlags(&c.ev_kjoin, cudaEventDisableTiming));
       for (auto &e : c.ev_split) WF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     WF_CUDA(cudaEventCreateWithFlags(&c.ev_halo, cudaEventDisableTiming));
@@ -247,6 +250,9 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
   }
   if (c.ev_fork) cudaEventDestroy(c.ev_fork);
   if (c.aux2) { cudaStreamSynchronize(c.aux2); cudaStreamDestroy(c.aux2); }
+  if (c.kside) { cudaStreamSynchronize(c.kside); cudaStreamDestroy(c.kside); }
+  if (c.ev_kfork) cudaEventDestroy(c.ev_kfork);
+  if (c.ev_kjoin) cudaEventDestroy(c.ev_kjoin);
   for (auto &e : c.ev_split) if (e) cudaEventDestroy(e);
   if (c.ev_halo) cudaEventDestroy(c.ev_halo);
   if (c.cpy) { cudaStreamSynchronize(c.cpy); cudaStreamDestroy(c.cpy); }

@@ -216,6 +216,8 @@ struct Ctx {
   // fork/join streams: the three independent blocks of A and of P_D run concurrently
   cudaStream_t aux[2] = {nullptr, nullptr};
   cudaStream_t aux2 = nullptr;     // second column half of D_hat^{-1} (see dhat_inv)
+  cudaStream_t kside = nullptr;    // MINRES: iteration j-1's update overlapping A z_j
+  cudaEvent_t ev_kfork = nullptr, ev_kjoin = nullptr;
   cudaEvent_t ev_split[2] = {nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
   cudaEvent_t ev_halo = nullptr;   // apply_A's halo exchange done (aux[1] -> main)

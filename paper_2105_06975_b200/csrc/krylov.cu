@@ -193,6 +193,43 @@ __global__ void k_minres_s3(MinresS S, int m, double tol, double mark_tol) {
   }
 }
 
+// Deferred-update MINRES (overlap): s3 split in two.
+// s3a, right after s2 on the main stream: the scalar shifts of iteration j (eta, gamma,
+// c, s) that iteration j+1's s1 / s2 need; s3b, after iteration j's update on the side
+// stream: the residual norm -> relres, counts, convergence, history, mark.
+__global__ void k_minres_s3a(MinresS S, int m) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= m || !S.active[r]) return;
+  S.eta[r] = -S.snew[r] * S.eta[r];
+  S.gamma_prev[r] = S.gamma[r];
+  S.gamma[r] = S.gnew[r];
+  S.c_prev[r] = S.c[r]; S.c[r] = S.cnew[r];
+  S.sn_prev[r] = S.sn[r]; S.sn[r] = S.snew[r];
+}
+
+__global__ void k_minres_s3b(MinresS S, const double *rr, int m, double tol, double mark_tol) {
+  const int j = S.flags[3] + 1;
+  int cnt = 0, below_mark = 1;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    if (S.active[r]) {
+      const double rel = sqrt(rr[r]) / S.bnorm[r];
+      S.relres[r] = rel;
+      S.iters[r] = j;
+      if (rel <= tol || S.gnew[r] == 0.0) S.active[r] = 0;
+    }
+    if (S.hist) S.hist[(int64_t)j * m + r] = S.relres[r];
+    cnt += S.active[r];
+    below_mark &= (S.relres[r] <= mark_tol);
+  }
+  cnt = __syncthreads_count(cnt);
+  below_mark = __syncthreads_and(below_mark);
+  if (threadIdx.x == 0) {
+    S.flags[0] = cnt;
+    if (below_mark && S.flags[2] < 0) S.flags[2] = j;
+    S.flags[3] = j;
+  }
+}
+
 static unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 
@@ -202,11 +239,15 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   const int m = c.m;
   const int NS = 13 + 3 + 4 + 4;
   size_t hist_n = (rep && rep->history) ? (size_t)(o.maxit + 1) * m : 0;
-  c.kws_reset(11 * (((size_t)n * 8 + 255) / 256 * 256) + (size_t)NS * m * 8 + 4 * (size_t)m * 4 +
-              hist_n * 8 + 4096);
+  const RedGrid rgu = red_grid(c, n);
+  c.kws_reset(12 * (((size_t)n * 8 + 255) / 256 * 256) + (size_t)NS * m * 8 + 4 * (size_t)m * 4 +
+              hist_n * 8 + ((size_t)rgu.gy + 1) * m * 8 + 8192);
   auto vec = [&]() { return c.kws_take<double>(n); };
   double *res = vec(), *vp = vec(), *v = vec(), *vn = vec(), *z = vec(), *zn = vec(), *q = vec(),
          *wp = vec(), *w = vec(), *awp = vec(), *aw = vec();
+  double *qb[2] = {q, vec()};                    // q of iterations j (odd) / j (even)
+  double *upart = c.kws_take<double>((size_t)rgu.gy * m);   // the update's ||r||^2 partials
+  double *rr = c.kws_take<double>(m);
   double *A = c.kws_take<double>((size_t)NS * m);
   MinresS S{};
   S.gamma = A; S.gamma_prev = A + m; S.eta = A + 2 * m; S.c = A + 3 * m; S.c_prev = A + 4 * m;
@@ -244,28 +285,66 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   bool indef = false;
   const int ce = std::max(1, o.check_every);
   int *hpin = c.hpin;
-  // one MINRES iteration on the current rotation of the work vectors
+  // Iteration j's update (w, A w, x, r and ||r||^2: k_minres_update, then k_minres_s3b)
+  // does not feed iteration j+1's A z_{j+1}: it is deferred into iteration j+1 and runs on
+  // the side stream c.kside concurrently with that A apply (HBM-bound vector work under
+  // the GEMM-bound operator), joined before P^{-1} -- the first kernel that overwrites
+  // one of its inputs (z_j's buffer).  q is double-buffered (q_j is read by the update
+  // while A writes q_{j+1}).  SURVEY 8(c)-B2.5 allows the one wasted iteration at exit
+  // (convergence is known one iteration late).  WF4DVAR_MINRES_OVERLAP=0: in order.
+  static const int overlap_env = env_int("WF4DVAR_MINRES_OVERLAP", 1);
+  // (not with a transport: the update's allreduce would run concurrently with A's halo
+  // exchange on another stream, and collectives must keep one order on every rank)
+  const bool overlap = overlap_env && !c.prof.on && c.fork_on && !c.comm;
+  struct Upd { double *z, *q, *wp, *w, *awp, *aw; };
+  auto update = [&](const Upd &u, double *rr_out, double *part_buf) {
+    const RedGrid rg = red_grid(c, n);
+    LaunchScope ls(c, K_VEC, 10.0 * n, 8.0 * 12 * n);
+    k_minres_update<<<dim3(rg.gx, rg.gy), 256, 0, c.st>>>(u.z, u.q, u.wp, u.w, u.awp, u.aw, x, res,
+                                                          S.coef, rg.rows, m, rg.RB, rg.rpb,
+                                                          part_buf);
+    c.launches += 2;
+    reduce_final(c, part_buf, rg.gy, 1, rr_out);   // ||r_j||^2
+  };
+  // one MINRES iteration on the current rotation of the work vectors; `pend` is the
+  // previous iteration's deferred update (overlap mode), or nullptr
   auto body = [&](double *vp_, double *v_, double *vn_, double *z_, double *zn_, double *wp_,
-                  double *w_, double *awp_, double *aw_) {
+                  double *w_, double *awp_, double *aw_, double *q, const Upd *pend) {
+    if (pend) {
+      WF_CUDA(cudaEventRecord(c.ev_kfork, c.st));
+      WF_CUDA(cudaStreamWaitEvent(c.kside, c.ev_kfork, 0));
+      OnStream os(c, c.kside);
+      update(*pend, rr, upart);
+      k_minres_s3b<<<1, 1024, 0, c.st>>>(S, rr, m, o.tol, o.mark_tol);
+      c.launches++;
+      WF_CUDA(cudaEventRecord(c.ev_kjoin, c.st));
+    }
     apply_A(c, z_, q);
     { const double *a[1] = {q}, *bb[1] = {z_}; dots(c, 1, a, bb, n, S.dots); }
     k_minres_s1<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
     k_lin3<<<nblk(n, 256), 256, 0, c.st>>>(vn_, q, S.cv, v_, S.cv + m, vp_, S.cv + 2 * m, n, m);
     c.launches += 2;
+    if (pend) WF_CUDA(cudaStreamWaitEvent(c.st, c.ev_kjoin, 0));
     apply_P(c, vn_, zn_);
     { const double *a[1] = {zn_}, *bb[1] = {vn_}; dots(c, 1, a, bb, n, S.dots); }
     k_minres_s2<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
-    {
-      const RedGrid rg = red_grid(c, n);
-      LaunchScope ls(c, K_VEC, 10.0 * n, 8.0 * 12 * n);
-      k_minres_update<<<dim3(rg.gx, rg.gy), 256, 0, c.st>>>(z_, q, wp_, w_, awp_, aw_, x, res,
-                                                            S.coef, rg.rows, m, rg.RB, rg.rpb,
-                                                            c.dot_part);
-      c.launches += 2;
-      reduce_final(c, c.dot_part, rg.gy, 1, S.dots);   // ||r_j||^2
-    }
-    k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, o.tol, o.mark_tol);
     c.launches++;
+    if (overlap) {
+      k_minres_s3a<<<nblk(m, 128), 128, 0, c.st>>>(S, m);
+      c.launches++;
+    } else {
+      const RedGrid rg = red_grid(c, n);
+      {
+        LaunchScope ls(c, K_VEC, 10.0 * n, 8.0 * 12 * n);
+        k_minres_update<<<dim3(rg.gx, rg.gy), 256, 0, c.st>>>(z_, q, wp_, w_, awp_, aw_, x, res,
+                                                              S.coef, rg.rows, m, rg.RB, rg.rpb,
+                                                              c.dot_part);
+        c.launches += 2;
+        reduce_final(c, c.dot_part, rg.gy, 1, S.dots);   // ||r_j||^2
+      }
+      k_minres_s3<<<1, 1024, 0, c.st>>>(S, m, o.tol, o.mark_tol);
+      c.launches++;
+    }
     WF_CUDA(cudaGetLastError());
   };
   // Launch-bound sizes replay the iteration as a CUDA graph (one per phase of the
@@ -281,6 +360,11 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
       c.mg_mark = o.mark_tol;
     }
   }
+  // the previous iteration's deferred update, from the current (rotated) names: z_{j-1}
+  // is in zn, q_{j-1} in qb[(j-1)&1], and the swap after it exchanged wp/w and awp/aw
+  auto pending = [&](int jj, double *zn_, double *wp_, double *w_, double *awp_, double *aw_) {
+    return Upd{zn_, qb[jj & 1], w_, wp_, aw_, awp_};
+  };
   for (j = 1; j <= o.maxit; ++j) {
     const int phase = (j - 1) % 6;
     if (graphs && c.mg_warm) {
@@ -294,13 +378,16 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
         double *q_wp = wp, *q_w = w, *q_awp = awp, *q_aw = aw;
         for (int q = 0; q < 6; ++q) {
           const int ph = (phase + q) % 6;
+          const int jj = j + q;   // >= 2: the eager first iteration is never replayed
           if (!c.mg_exec[ph]) {
             // record the counter increments of one iteration (launches, per-window
             // constituent products) and add them on every replay
             cudaGraph_t g = nullptr;
             const Ctx::Counters before = c.counters();
+            const Upd pu = pending(jj - 1, q_zn, q_wp, q_w, q_awp, q_aw);
             WF_CUDA(cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal));
-            body(q_vp, q_v, q_vn, q_z, q_zn, q_wp, q_w, q_awp, q_aw);
+            body(q_vp, q_v, q_vn, q_z, q_zn, q_wp, q_w, q_awp, q_aw, qb[jj & 1],
+                 overlap ? &pu : nullptr);
             WF_CUDA(cudaStreamEndCapture(c.st, &g));
             c.mg_delta[ph] = c.counters() - before;
             c.set_counters(before);
@@ -316,8 +403,9 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
       WF_CUDA(cudaGraphLaunch(c.mg_exec[phase], c.st));
       c.set_counters(c.counters() + c.mg_delta[phase]);
     } else {
-      body(vp, v, vn, z, zn, wp, w, awp, aw);
-      if (graphs) c.mg_warm = true;
+      const Upd pu = pending(j - 1, zn, wp, w, awp, aw);
+      body(vp, v, vn, z, zn, wp, w, awp, aw, qb[j & 1], (overlap && j > 1) ? &pu : nullptr);
+      if (graphs && j > 1) c.mg_warm = true;   // the eager pass ran the overlap path too
     }
     WF_CUDA(cudaEventRecord(c.iter_event(j), c.st));
     // rotate: v_prev <- v, v <- v_new, z <- z_new, w_prev <- w, w <- w_new(in wp), same for Aw
@@ -334,19 +422,29 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
     }
   }
   if (j > o.maxit) j = o.maxit;
+  if (overlap && !indef) {   // the last iteration's deferred update, in order
+    const Upd pu = pending(j, zn, wp, w, awp, aw);
+    update(pu, rr, upart);
+    k_minres_s3b<<<1, 1024, 0, c.st>>>(S, rr, m, o.tol, o.mark_tol);
+    c.launches++;
+    WF_CUDA(cudaEventRecord(c.iter_event(j + 1), c.st));
+  }
   WF_CUDA(cudaMemcpyAsync(hpin, S.flags, 3 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
   WF_CUDA(cudaStreamSynchronize(c.st));
   memcpy(h, hpin, 3 * sizeof(int));
   if (rep) {
     float ms = 0;
-    cudaEventElapsedTime(&ms, e0, c.iter_event(j));
+    // overlap mode: iteration j's update completes inside iteration j+1 (or the final
+    // flush, event j+1), so the solve ends and the mark is reached one event later
+    const int lag = (overlap && !indef) ? 1 : 0;
+    cudaEventElapsedTime(&ms, e0, c.iter_event(j + lag));
     rep->seconds = ms * 1e-3;
     rep->iters_to_mark = h[2];
     rep->seconds_to_mark = -1;
     cudaEventElapsedTime(&ms, e0, c.ev_init);
     rep->seconds_init = ms * 1e-3;
     if (h[2] >= 0) {
-      cudaEventElapsedTime(&ms, e0, c.iter_event(h[2]));
+      cudaEventElapsedTime(&ms, e0, c.iter_event(std::min(h[2] + lag, j + lag)));
       rep->seconds_to_mark = ms * 1e-3;
     }
     std::vector<int> it(m), act(m);
@@ -503,6 +601,96 @@ __global__ void __launch_bounds__(256) k_multiaxpy(const double *V, int64_t n, i
     double s = 0.0;
     for (int uu = 0; uu < U; ++uu) s += sm[uu * RB + rl];
     norm_part[(int64_t)blockIdx.y * m + r] = s;
+  }
+}
+
+// CGS2's first projection and second inner products in one pass:
+//   w <- w - sum_i V_i h1_i      (exactly k_multiaxpy's FMA order: bitwise the same w)
+//   part <- per-block partials of V_i . w_new   (the second multidot)
+// Each row's basis entries are read twice back to back: the first read keeps them in
+// L2, the second (the dot with the new w) finds them there, so DRAM sees three basis
+// passes per Arnoldi step instead of four.  Dot accumulators live in shared memory
+// ([nv][256], one column per thread: no conflicts, no atomics), reduced over the
+// block's row groups in fixed order at the end (deterministic).
+__global__ void __launch_bounds__(256) k_axpy_multidot(const double *V, int64_t n, int nv,
+                                                       double *w, const double *h, int64_t rows,
+                                                       int m, int RB, int64_t rpb, double *part,
+                                                       int jmax) {
+  extern __shared__ double sacc[];   // [nv][256]
+  const int t = threadIdx.x;
+  const int rl = t % RB, u = t / RB, U = 256 / RB;
+  const int r = blockIdx.x * RB + rl;
+  const int64_t row0 = (int64_t)blockIdx.y * rpb, row1 = min(rows, row0 + rpb);
+  for (int i = 0; i < nv; ++i) sacc[i * 256 + t] = 0.0;
+  if (r < m && u < U) {
+    constexpr int RU = 2;
+    for (int64_t row = row0 + u; row < row1; row += (int64_t)U * RU) {
+      double v[RU];
+      int64_t f[RU];
+      bool ok[RU];
+#pragma unroll
+      for (int q = 0; q < RU; ++q) {
+        const int64_t rq = row + (int64_t)q * U;
+        ok[q] = rq < row1;
+        f[q] = rq * m + r;
+        v[q] = ok[q] ? w[f[q]] : 0.0;
+      }
+      int i = 0;
+      for (; i + 4 <= nv; i += 4) {
+        double vv[4][RU], hh[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          hh[k] = __ldg(h + (i + k) * m + r);
+#pragma unroll
+          for (int q = 0; q < RU; ++q) vv[k][q] = ok[q] ? __ldg(V + (int64_t)(i + k) * n + f[q]) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int q = 0; q < RU; ++q) v[q] = fma(-vv[k][q], hh[k], v[q]);
+      }
+      for (; i < nv; ++i) {
+        const double hi = __ldg(h + i * m + r);
+#pragma unroll
+        for (int q = 0; q < RU; ++q) {
+          const double vv = ok[q] ? __ldg(V + (int64_t)i * n + f[q]) : 0.0;
+          v[q] = fma(-vv, hi, v[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RU; ++q)
+        if (ok[q]) w[f[q]] = v[q];
+      // second inner products with the new w (basis rows re-read from L2)
+      for (i = 0; i + 4 <= nv; i += 4) {
+        double vv[4][RU];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int q = 0; q < RU; ++q) vv[k][q] = ok[q] ? __ldcs(V + (int64_t)(i + k) * n + f[q]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          double a = sacc[(i + k) * 256 + t];
+#pragma unroll
+          for (int q = 0; q < RU; ++q) a = fma(vv[k][q], v[q], a);
+          sacc[(i + k) * 256 + t] = a;
+        }
+      }
+      for (; i < nv; ++i) {
+        double a = sacc[i * 256 + t];
+#pragma unroll
+        for (int q = 0; q < RU; ++q)
+          a = fma(ok[q] ? __ldcs(V + (int64_t)i * n + f[q]) : 0.0, v[q], a);
+        sacc[i * 256 + t] = a;
+      }
+    }
+  }
+  __syncthreads();
+  if (u == 0 && r < m) {
+    for (int i = 0; i < nv; ++i) {
+      double s = 0.0;
+      for (int uu = 0; uu < U; ++uu) s += sacc[i * 256 + uu * RB + rl];
+      part[((int64_t)blockIdx.y * jmax + i) * m + r] = s;
+    }
   }
 }
 
@@ -702,6 +890,25 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
       allreduce(c, S.ww, (size_t)m);
     }
   };
+  // CGS2's first projection fused with its second inner products (k_axpy_multidot),
+  // opt-in WF4DVAR_CGS2_FUSED=1: r02m measured no gain (configs[4] 18.83 -> 18.80 ms per
+  // step; vector + dot classes 8.70 -> 8.67 ms) -- the second read of the basis did not
+  // stay in L2 under the other blocks' streams -- and its other summation order moved two
+  // rounding-sensitive GMRES cells past their parity bounds
+  static const int fused_env = env_int("WF4DVAR_CGS2_FUSED", 0);
+  const bool fused = fused_env != 0;
+  auto axpy_multidot = [&](int nv, double *w, const double *h, double *out) {
+    LaunchScope ls(c, K_VEC, 4.0 * nv * n, 8.0 * (nv + 2) * n);
+    const size_t smem = (size_t)nv * 256 * sizeof(double);
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        k_axpy_multidot, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 256 * (int)sizeof(double));
+    WF_CUDA(attr);
+    dim3 grid(gx, gy);
+    k_axpy_multidot<<<grid, 256, smem, c.st>>>(V, n, nv, w, h, rows, m, RB, rpb, part, jmax);
+    k_multidot_final<<<nblk((int64_t)nv * m, 8), 256, 0, c.st>>>(part, gy, nv, jmax, m, out);
+    c.launches += 2;
+    allreduce(c, out, (size_t)nv * m);
+  };
   auto norm2 = [&](const double *v) {
     const double *a[1] = {v};
     dots(c, 1, a, a, n, S.ww);
@@ -735,8 +942,12 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
       apply_P(c, Vj, u);
       apply_A(c, u, w);
       multidot(j + 1, w, S.h1);
-      multiaxpy(j + 1, w, S.h1, false);
-      multidot(j + 1, w, S.h2);
+      if (fused && j + 1 <= 64) {   // shared-memory accumulators for <= 64 basis vectors
+        axpy_multidot(j + 1, w, S.h1, S.h2);
+      } else {
+        multiaxpy(j + 1, w, S.h1, false);
+        multidot(j + 1, w, S.h2);
+      }
       multiaxpy(j + 1, w, S.h2, true);
       ++global_it;
       k_gmres_step<<<1, 1024, 0, c.st>>>(S, j, o.tol, o.mark_tol, global_it);

@@ -492,7 +492,10 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // r02f (configs[3] per step): thread-per-chunk 1.264 ms (2.31 TB/s) -> warp-scan with
     // cp.async staging R = 128: 1.110 ms (2.63 TB/s), R = 256: 1.431 ms (fewer CTAs per SM)
     static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 128);   // 0: thread-per-chunk form
-    if (tile_env == 64 || tile_env == 128 || tile_env == 256) {
+    // the tiled form needs columns to fill its 32-wide CTAs and rows to amortise the
+    // 2H-row halo: tiny problems (configs[0]: 5 columns of 50 rows) keep the
+    // thread-per-chunk form
+    if ((tile_env == 64 || tile_env == 128 || tile_env == 256) && cols >= 256 && c.s >= 256) {
       constexpr int WARPS = 8;
       auto go = [&](auto r_tag) {
         constexpr int R = decltype(r_tag)::value;
