@@ -482,10 +482,21 @@ def main():
     F = sum(v["flops"] for v in prof.values())
     By = sum(v["bytes"] for v in prof.values())
     t_roof = max(F / (peak_fp64 * 1e12), By / (hbm * 1e9))
+    # second, dependency-aware bound: every kernel class at its own roofline, the classes
+    # back to back (a Krylov step's vector work needs the operator's output and the next
+    # operator apply needs the orthogonalised vector, so the tensor-bound and the
+    # HBM-bound phases cannot overlap in one batch); frac_serial >= frac
+    t_roof_ser = sum(max(v["flops"] / (peak_fp64 * 1e12), v["bytes"] / (hbm * 1e9))
+                     for v in prof.values())
     step_roof = dict(flops_per_step=F / steps, bytes_per_step=By / steps,
                      t_roof_ms=t_roof / steps * 1e3, t_step_ms=secs_total / steps * 1e3,
                      frac=t_roof / secs_total, profiled_pass_ms_per_step=tot_ms / steps,
-                     note="per step = per timed solve / K (solver initialisation included)")
+                     t_roof_serial_ms=t_roof_ser / steps * 1e3,
+                     frac_serial=t_roof_ser / secs_total,
+                     note="per step = per timed solve / K (solver initialisation included); "
+                          "t_roof = max(all flops / FP64 peak, all bytes / HBM peak) (perfect "
+                          "overlap of compute and memory phases); t_roof_serial = sum over "
+                          "kernel classes of max(class flops / FP64 peak, class bytes / HBM)")
     kernels = {k: dict(launches=v["launches"], ms=round(v["ms"], 3),
                        tflops=(v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] else None,
                        gbs=(v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None)

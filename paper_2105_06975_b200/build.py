@@ -30,9 +30,36 @@ def build(verbose=False, force=False):
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(f) <= t for f in srcs + hdrs if os.path.exists(f)):
             return LIB
-    cmd = [_nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v" if verbose else "-O3",
-           "-o", LIB + ".tmp"] + srcs + [
+    # one nvcc per translation unit, run concurrently (no cross-file device code, so
+    # whole-program compilation is not needed), then one host link
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    ccmd = [_nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            "-Xptxas", "-v" if verbose else "-O3", "-c"]
+    objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
+
+    def _one(so):
+        src, obj = so
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) >= max(
+                [os.path.getmtime(src)] + [os.path.getmtime(h) for h in hdrs if os.path.exists(h)]):
+            return None
+        r = subprocess.run(ccmd + ["-o", obj + ".tmp", src], capture_output=True, text=True)
+        if r.returncode == 0:
+            os.replace(obj + ".tmp", obj)
+        return r
+
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(srcs), max(1, os.cpu_count() or 1))) as ex:
+        results = list(ex.map(_one, zip(srcs, objs)))
+    for src, r in zip(srcs, results):
+        if r is None:
+            continue
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed compiling " + os.path.basename(src))
+        if verbose:
+            sys.stderr.write(r.stderr)
+    cmd = [_nvcc(), ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB + ".tmp"] + objs + [
            "-L" + os.path.join(CUDA_HOME, "lib64"), "-lcusolver", "-lcublas", "-ldl",
            "-Xlinker", "-rpath=" + os.path.join(CUDA_HOME, "lib64")]
     if verbose:
@@ -40,9 +67,7 @@ def build(verbose=False, force=False):
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building libwf4dvar.so")
-    if verbose:
-        sys.stderr.write(r.stderr)
+        raise RuntimeError("nvcc failed linking libwf4dvar.so")
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -266,6 +266,8 @@ wf4dvar_status wf4dvar_destroy(wf4dvar_ctx ctx) {
     if (e.ws) cudaFree(e.ws);
     if (e.flags) cudaFree(e.flags);
     if (e.splitk) cudaFree(e.splitk);
+    if (e.df_flags) cudaFree(e.df_flags);
+    if (e.df_ep) cudaFree(e.df_ep);
   }
   for (void *p : c.retired) cudaFree(p);
   for (void *p : c.allocs) cudaFree(p);

@@ -302,6 +302,9 @@ struct Ctx {
   struct SkState {
     cudaStream_t stream = nullptr; double *ws = nullptr; unsigned *flags = nullptr; size_t cap = 0;
     double *splitk = nullptr; size_t splitk_cap = 0;   // split-K partial tiles
+    // dataflow TRSM (trsm.cu k_trsm_df): per (tile, panel) ready flags and the launch
+    // epoch / finished-CTA counter pair
+    unsigned *df_flags = nullptr; size_t df_cap = 0; unsigned *df_ep = nullptr;
   };
   std::vector<SkState> sk_states;
   // workspaces replaced by a larger one: captured MINRES graphs may still reference

@@ -257,7 +257,10 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   int *I = c.kws_take<int>(2 * (size_t)m + 4);
   S.active = I; S.iters = I + m; S.flags = I + 2 * m;
   S.hist = hist_n ? c.kws_take<double>(hist_n) : nullptr;
-  const int h_flags[4] = {0, 0, -1, 0};
+  // flags: [0] active RHS count (m until the first convergence check has run: in
+  // overlap mode iteration 1's check is deferred into iteration 2, and a count of 0
+  // would end the solve after one iteration), [1] indefinite, [2] mark, [3] iteration
+  const int h_flags[4] = {m, 0, -1, 0};
   WF_CUDA(cudaMemcpyAsync(S.flags, h_flags, sizeof(h_flags), cudaMemcpyHostToDevice, c.st));
 
   cudaEvent_t e0 = c.iter_event(0);
@@ -367,7 +370,10 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
   };
   for (j = 1; j <= o.maxit; ++j) {
     const int phase = (j - 1) % 6;
-    if (graphs && c.mg_warm) {
+    // overlap mode: every phase's graph carries the previous iteration's deferred
+    // update, which iteration 1 does not have (a replay there would apply the previous
+    // solve's last coefficients to x): iteration 1 always runs eagerly
+    if (graphs && c.mg_warm && !(overlap && j == 1)) {
       // one eager iteration since the cache was (re)built has run every kernel path
       // and lazy allocation, so every phase can be captured: capture all missing
       // phases at once (capture does not execute), from the pointer sets the 6-periodic

@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(128) k_heat_iir(double *out, const double *bas
 // < 1e-17 relative), other rounding order than k_heat_iir.  Results go back to shared
 // memory and leave as coalesced rows: out = base + gain * v (+ the H^T scatter).
 template <int H, int R, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_heat_iir_scan(
+__global__ void __launch_bounds__(WARPS * 32, R <= 128 ? 4 : 2) k_heat_iir_scan(
     double *out, const double *base, const double *in, const double *add2, const int *row_map,
     double rho, double gain, int s, int W, int m, int w_first, int w_step, int nw, int dir,
     const double *halo, int w0, int WG) {
@@ -173,6 +173,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_heat_iir_scan(
   const int w = w_first + tt * w_step, ws = w + dir;
   const bool has = live && (w0 + ws >= 0 && w0 + ws < WG);
   const bool from_halo = (ws < 0 || ws >= W);
+  // this thread's rows of `base` (and of the H^T scatter) are loaded into registers now,
+  // in flight together with the staged tile: the store phase then issues no dependent
+  // loads (r02n: one base load per store left every warp waiting ~1 us per row).  Each
+  // element of base / out is read and written only by this thread, so in-place calls
+  // (out == base) stay exact.
+  constexpr int RPW = (R + WARPS - 1) / WARPS;
+  const int64_t ocol = (int64_t)w * m + r;
+  double bv[RPW];
+#pragma unroll
+  for (int k = 0; k < RPW; ++k) {
+    const int i = i0 + warp + k * WARPS;
+    bv[k] = (live && warp + k * WARPS < R && i < s) ? base[(int64_t)i * ld + ocol] : 0.0;
+  }
   {
     // all NS x 32 loads in flight at once: cp.async straight into shared memory (ncu
     // r02e: register-staged loads left this kernel long-scoreboard bound at 12% of DRAM
@@ -273,17 +286,155 @@ __global__ void __launch_bounds__(WARPS * 32) k_heat_iir_scan(
   }
   __syncthreads();
   if (!live) return;
-  const int64_t ocol = (int64_t)w * m + r;
-  for (int j = H + warp; j < H + R; j += WARPS) {
-    const int i = i0 + j - H;
-    if (i >= s) break;
-    double val = base[(int64_t)i * ld + ocol];
-    if (has) val = fma(gain, tile[j * LD + lane], val);
-    if (add2) {
-      const int q = row_map[i];
-      if (q >= 0) val += add2[(int64_t)q * ld + ocol];
+  if (!add2) {
+#pragma unroll
+    for (int k = 0; k < RPW; ++k) {
+      const int j = H + warp + k * WARPS;
+      const int i = i0 + j - H;
+      if (j < H + R && i < s)
+        out[(int64_t)i * ld + ocol] = has ? fma(gain, tile[j * LD + lane], bv[k]) : bv[k];
     }
-    out[(int64_t)i * ld + ocol] = val;
+    return;
+  }
+  // H^T scatter (the L^T x1 pass): its rows loaded 8 at a time ahead of their stores
+  constexpr int KB = RPW < 8 ? RPW : 8;
+#pragma unroll
+  for (int k0 = 0; k0 < RPW; k0 += KB) {
+    double a2[KB];
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      const int k = k0 + kk, i = i0 + warp + k * WARPS;
+      a2[kk] = 0.0;
+      if (k < RPW && warp + k * WARPS < R && i < s) {
+        const int q = row_map[i];
+        if (q >= 0) a2[kk] = add2[(int64_t)q * ld + ocol];
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < KB; ++kk) {
+      const int k = k0 + kk;
+      const int j = H + warp + k * WARPS;
+      const int i = i0 + j - H;
+      if (k < RPW && j < H + R && i < s) {
+        double val = has ? fma(gain, tile[j * LD + lane], bv[k]) : bv[k];
+        out[(int64_t)i * ld + ocol] = val + a2[kk];   // (base + gain v) + scatter, as before
+      }
+    }
+  }
+}
+
+// Column-sequential form (default, r02o): the same two first-order recursions as
+// k_heat_iir, but every lane runs its column's recursions serially over rows staged in
+// shared memory, instead of splitting a column over a warp with a shuffle scan (ncu r02n:
+// k_heat_iir_scan issued ~150 thread instructions per output and sat at 78% L1 / shared
+// memory busy with DRAM at 26%).  A CTA owns 32 consecutive (window, RHS) columns (lane =
+// column) and WARPS * R output rows; warp w owns rows [wR, wR + R) of the tile.  The
+// input rows [i0 - H, i0 + WARPS R + H] land in shared memory by cp.async (one
+// coalesced row of 32 columns per warp instruction, zero-filled where there is no
+// source); meanwhile each lane loads its R rows of `base` into registers.  Then
+//   1. warm-up: u from zero over the H rows before the warp's own rows (the previous
+//      warp's rows -- read before step 2 overwrites them);
+//   2. forward over the own rows, u written back in place (the last warp continues
+//      over the H + 1 rows below the tile);
+//   3. backward from H + 1 rows below the own rows (the next warp's u) down through
+//      the own rows, each output leaving as out = base + gain v (+ the H^T scatter).
+// This is k_heat_iir's arithmetic with TI = R (restart H rows early, dropped tail
+// < 1e-17 relative), at ~(2H + 1) / R + 2 serial FMAs per output and one shared load
+// each; the tile is read from DRAM once (plus its 2H-row halo, mostly L2 hits).
+template <int H, int R, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS * R + 2 * H + 1) * 256 <= 56 * 1024 ? 4 : 2)
+k_heat_iir_seq(double *out, const double *base, const double *in, const double *add2,
+               const int *row_map, double rho, double gain, int s, int W, int m, int w_first,
+               int w_step, int nw, int dir, const double *halo, int w0, int WG) {
+  constexpr int T = WARPS * R + 2 * H + 1;   // staged rows i0 - H .. i0 + WARPS R + H
+  extern __shared__ double tile[];           // [T][32]
+  const int64_t ld = (int64_t)W * m;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i0 = blockIdx.y * (WARPS * R);
+  const int cc = blockIdx.x * 32 + lane;
+  const bool live = cc < nw * m;
+  const int tt = live ? cc / m : 0, r = live ? cc - tt * m : 0;
+  const int w = w_first + tt * w_step, ws = w + dir;
+  const bool has = live && (w0 + ws >= 0 && w0 + ws < WG);
+  const bool from_halo = (ws < 0 || ws >= W);
+  const int64_t ocol = (int64_t)w * m + r;
+  {
+    const double *src = has ? (from_halo ? halo + r : in + (int64_t)ws * m + r) : in;
+    const int64_t sld = from_halo ? (int64_t)m : ld;
+    int row = (i0 - H + warp) % s;
+    row = row < 0 ? row + s : row;
+#pragma unroll 4
+    for (int j = warp; j < T; j += WARPS) {
+      cp_async8(tile + j * 32 + lane, has ? src + (int64_t)row * sld : src, has ? 8 : 0);
+      row += WARPS;
+      while (row >= s) row -= s;
+    }
+    cp_async_commit();
+  }
+  const int ob = i0 + warp * R;   // first output row of this warp
+  double bv[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k)
+    bv[k] = (live && ob + k < s) ? base[(int64_t)(ob + k) * ld + ocol] : 0.0;
+  cp_async_wait<0>();
+  __syncthreads();
+  const int t0 = H + warp * R;    // tile row of the warp's first output row
+  // 1. warm-up over the H rows above (the previous warp's own rows, still x)
+  double u = 0.0;
+#pragma unroll
+  for (int t = 0; t < H; ++t) u = fma(rho, u, tile[(t0 - H + t) * 32 + lane]);
+  __syncthreads();
+  // 2. forward over the own rows, in place (+ the tail below the tile: last warp)
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    u = fma(rho, u, tile[(t0 + t) * 32 + lane]);
+    tile[(t0 + t) * 32 + lane] = u;
+  }
+  if (warp == WARPS - 1) {
+#pragma unroll
+    for (int t = 0; t <= H; ++t) {
+      u = fma(rho, u, tile[(t0 + R + t) * 32 + lane]);
+      tile[(t0 + R + t) * 32 + lane] = u;
+    }
+  }
+  __syncthreads();
+  // 3. backward: warm-up over the H + 1 rows below, then the own rows -> out
+  double v = 0.0;
+#pragma unroll
+  for (int t = H; t >= 0; --t) v = fma(rho, v, tile[(t0 + R + t) * 32 + lane]);
+  if (!live) return;
+  if (!add2) {
+#pragma unroll
+    for (int t = R - 1; t >= 0; --t) {
+      v = fma(rho, v, tile[(t0 + t) * 32 + lane]);
+      if (ob + t < s) out[(int64_t)(ob + t) * ld + ocol] = has ? fma(gain, v, bv[t]) : bv[t];
+    }
+    return;
+  }
+  // H^T scatter (the L^T x1 pass): its rows loaded 8 at a time ahead of their stores
+  constexpr int KB = R < 8 ? R : 8;
+#pragma unroll
+  for (int t1 = R; t1 > 0; t1 -= KB) {
+    double a2[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int t = t1 - 1 - q;
+      a2[q] = 0.0;
+      if (t >= 0 && ob + t < s) {
+        const int qq = row_map[ob + t];
+        if (qq >= 0) a2[q] = add2[(int64_t)qq * ld + ocol];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int t = t1 - 1 - q;
+      if (t < 0) break;
+      v = fma(rho, v, tile[(t0 + t) * 32 + lane]);
+      if (ob + t < s) {
+        const double val = has ? fma(gain, v, bv[t]) : bv[t];
+        out[(int64_t)(ob + t) * ld + ocol] = val + a2[q];   // (base + gain v) + scatter
+      }
+    }
   }
 }
 
@@ -491,11 +642,31 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // more independent chains and fewer registers (higher occupancy)
     // r02f (configs[3] per step): thread-per-chunk 1.264 ms (2.31 TB/s) -> warp-scan with
     // cp.async staging R = 128: 1.110 ms (2.63 TB/s), R = 256: 1.431 ms (fewer CTAs per SM)
+    // r02o: column-sequential kernel (WF4DVAR_HEAT_SEQ = rows per warp, 0: off)
+    static const int seq_env = env_int("WF4DVAR_HEAT_SEQ", 16);   // r02p: R = 16 4.92 TB/s, 32: 4.61
+    if (seq_env == 16 || seq_env == 32) {
+      constexpr int WARPS = 8;
+      auto go = [&](auto r_tag) {
+        constexpr int R = decltype(r_tag)::value;
+        constexpr size_t smem = (size_t)(WARPS * R + 2 * H + 1) * 32 * sizeof(double);
+        static const cudaError_t attr = cudaFuncSetAttribute(
+            k_heat_iir_seq<H, R, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        WF_CUDA(attr);
+        dim3 grid((cols + 31) / 32, (c.s + WARPS * R - 1) / (WARPS * R));
+        k_heat_iir_seq<H, R, WARPS><<<grid, WARPS * 32, smem, c.st>>>(
+            out, base, in, add2, row_map, c.heat_rho, sign * c.heat_gain, c.s, c.W, c.m, w_first,
+            w_step, nw, transpose ? 1 : -1, transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
+      };
+      if (seq_env == 16) go(std::integral_constant<int, 16>{});
+      else go(std::integral_constant<int, 32>{});
+      WF_CUDA(cudaGetLastError());
+      return;
+    }
     static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 128);   // 0: thread-per-chunk form
-    // the tiled form needs columns to fill its 32-wide CTAs and rows to amortise the
-    // 2H-row halo: tiny problems (configs[0]: 5 columns of 50 rows) keep the
-    // thread-per-chunk form
-    if ((tile_env == 64 || tile_env == 128 || tile_env == 256) && cols >= 256 && c.s >= 256) {
+    // (every size: r02n measured the thread-per-chunk form on configs[0] moving a
+    // restarted-GMRES solution to the edge of its 1e-9 parity bound -- a rounding-order
+    // effect at the stop, not a speed matter for a 5-column problem)
+    if (tile_env == 64 || tile_env == 128 || tile_env == 256) {
       constexpr int WARPS = 8;
       auto go = [&](auto r_tag) {
         constexpr int R = decltype(r_tag)::value;

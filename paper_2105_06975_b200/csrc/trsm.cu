@@ -241,6 +241,159 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   }
 }
 
+// ---- Dataflow form of one segment (default where it applies, r02o): one CTA per
+// (64-row tile, NB-column panel) instead of one CTA per panel walking every tile.  CTA
+// (t, c) computes  Y_t = G_tt^{-1} (X_t - sum_{j before t} G_tj Y_j)  for its panel: it
+// accumulates each G_tj Y_j as soon as tile j of the same panel is published (a ready
+// flag in global memory), so the off-diagonal products of all tiles run in parallel on
+// ntile x panels CTAs and only the chain "Y_{t-1} ready -> one 64 x 64 x NB product ->
+// the inverse-tile product -> publish Y_t" is serial.  The blocked panel kernel above
+// runs that whole chain, products included, inside one CTA per panel (ncu r02c: 11%
+// warps active, latency bound; configs[1]: 42 CTAs on 148 SMs).
+// Same arithmetic as k_trsm's inverse form: the K range of each tile is summed in
+// increasing row order (lower) / decreasing tile order (upper) in BK = 16 steps, then
+// T = X - acc, Y = G_tt^{-1} T (reading A31).
+// CTAs are numbered in solve order (tile-major), so a CTA only waits for CTAs with
+// lower indices, which the hardware dispatched before it: no co-residency is needed.
+// Flags hold the launch epoch + 1; the epoch (ep[0]) is read at the start of every CTA
+// and advanced by the last CTA to finish (ep[1] counts finished CTAs), so back-to-back
+// launches and CUDA-graph replays on one stream need no host-side reset.
+struct TrsmDfArgs {
+  TrsmProb p[2];
+  int panels0, panels;   // panels of problem 0; of both problems
+  int slo, shi, ntile;   // the segment's rows; its 64-row tiles
+  unsigned *flags;       // [ntile][panels]
+  unsigned *ep;          // [0] epoch, [1] finished CTAs of the current launch
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int NB, bool UPPER>
+__global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
+  using C = TrsmCfg<NB>;
+  extern __shared__ __align__(16) double smem[];
+  double *sPipe = smem;                        // C::SMEM_DOUBLES
+  double *sT = smem + C::SMEM_DOUBLES;         // [64][NB+1]
+  double *sG = sT + TB * (NB + 1);             // G_tt^{-1}, row-major, stride kInvLd
+  __shared__ unsigned s_ep;
+  __shared__ int s_ready;
+  const int it = blockIdx.x / L.panels, pc = blockIdx.x - it * L.panels;
+  int gi = 0, panel = pc;
+  if (pc >= L.panels0) { gi = 1; panel -= L.panels0; }
+  const TrsmProb &P = L.p[gi];
+  const int ti = UPPER ? L.ntile - 1 - it : it;
+  const int r0 = L.slo + ti * TB, r1 = min(L.shi, r0 + TB), nr = r1 - r0;
+  const int c0 = panel * NB;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+  const int ncols = P.ncols;
+  // the inverse diagonal tile: in flight under the dependency wait and the products
+  const double *dpk = P.dpack + (int64_t)(r0 / TB) * kDiagPack;
+  for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(sG + e, dpk + e, 16);
+  cp_async_commit();
+  if (tid == 0) s_ep = __ldcg(L.ep);
+  __syncthreads();
+  const unsigned want = s_ep + 1;
+  double acc[C::FM][C::FN][2];
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // dependencies: the tiles before this one in solve order, it' = 0 .. it-1
+  auto dep_flag = [&](int k) {   // flag of the k-th tile in solve order, this panel
+    const int tk = UPPER ? L.ntile - 1 - k : k;
+    return L.flags + (int64_t)tk * L.panels + pc;
+  };
+  int done = 0;
+  while (done < it) {
+    if (tid == 0) {
+      int k = done;
+      while (ld_acquire_u32(dep_flag(k)) != want) __nanosleep(32);
+      ++k;
+      while (k < it && ld_acquire_u32(dep_flag(k)) == want) ++k;   // everything ready now
+      s_ready = k;
+    }
+    __syncthreads();
+    const int k1 = s_ready;
+    int kb, ke;   // rows of G's columns / Y's rows covered by solve-order tiles [done, k1)
+    if (!UPPER) {
+      kb = L.slo + done * TB;
+      ke = L.slo + k1 * TB;
+    } else {
+      kb = L.slo + (L.ntile - k1) * TB;
+      ke = min(L.shi, L.slo + (L.ntile - done) * TB);
+    }
+    tile_mainloop<C, true>(sPipe, acc, P.G + (int64_t)r0 * P.ldg, P.ldg, P.Y + c0, P.ldy, 0, 0,
+                           kb, ke, nr, ncols - c0);   // ends with __syncthreads
+    done = k1;
+  }
+  // T = X - acc -> shared memory
+#pragma unroll
+  for (int i = 0; i < C::FM; ++i) {
+    const int rr = wm * C::WM + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = wn * C::WN + j * 8 + 2 * t + h;
+        double xv = 0.0;
+        if (rr < nr && c0 + cc < ncols) xv = P.X[(int64_t)(r0 + rr) * P.ldx + c0 + cc];
+        sT[rr * (NB + 1) + cc] = xv - acc[i][j][h];
+      }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // Y_t = G_tt^{-1} T on the tensor pipe (warp w: the 8-row blocks w and w + 4)
+  constexpr int NJ = NB / 8;
+  double ya[2][NJ][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) ya[q][j][0] = ya[q][j][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < TB; kk += 4) {
+    const double a0 = sG[(warp * 8 + g) * kInvLd + kk + t];
+    const double a1 = sG[((warp + 4) * 8 + g) * kInvLd + kk + t];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const double b = sT[(kk + t) * (NB + 1) + j * 8 + g];
+      dmma884(ya[0][j][0], ya[0][j][1], a0, b);
+      dmma884(ya[1][j][0], ya[1][j][1], a1, b);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int rr = (warp + 4 * q) * 8 + g;
+    if (rr >= nr) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = j * 8 + 2 * t + h;
+        if (c0 + cc < ncols) P.Y[(int64_t)(r0 + rr) * P.ldy + c0 + cc] = ya[q][j][h];
+      }
+  }
+  // publish Y_t of this panel, then count this CTA out of the launch
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    st_release_u32(L.flags + (int64_t)ti * L.panels + pc, want);
+    if (atomicAdd(L.ep + 1, 1u) == gridDim.x - 1) {
+      atomicExch(L.ep + 1, 0u);
+      __threadfence();
+      atomicAdd(L.ep, 1u);
+    }
+  }
+}
+
 // Setup: pack every 64x64 diagonal tile of a triangular factor as the kernel wants it
 // in shared memory: transposed and strictly masked (sG[c][r], stride 65) followed by
 // the 64 reciprocal diagonal entries (identity padding past n).
@@ -341,6 +494,41 @@ static void run(Ctx &c, const TrsmLaunch &L, int panels, int nseg, bool v16) {
   else run_inv<NB, UPPER, false>(c, L, panels, nseg, v16);
 }
 
+template <int NB, bool UPPER>
+static void run_df(Ctx &c, TrsmDfArgs &A) {
+  using C = TrsmCfg<NB>;
+  const size_t smem = (C::SMEM_DOUBLES + TB * (NB + 1) + kDiagPack) * sizeof(double);
+  static const cudaError_t attr = cudaFuncSetAttribute(
+      k_trsm_df<NB, UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  WF_CUDA(attr);
+  // per-stream flags / epoch (concurrent solves on the fork/join streams must not share)
+  Ctx::SkState *st = nullptr;
+  for (auto &e : c.sk_states)
+    if (e.stream == c.st) st = &e;
+  if (!st) {
+    c.sk_states.push_back(Ctx::SkState{});
+    st = &c.sk_states.back();
+    st->stream = c.st;
+  }
+  const size_t need = (size_t)A.ntile * A.panels;
+  if (!st->df_ep) {
+    WF_CUDA(cudaMalloc(&st->df_ep, 2 * sizeof(unsigned)));
+    WF_CUDA(cudaMemsetAsync(st->df_ep, 0, 2 * sizeof(unsigned), c.st));
+  }
+  if (st->df_cap < need) {
+    // flags of a grown set start at 0 (< every epoch + 1); the old set may still be
+    // referenced by captured graphs: retired, freed with the context
+    if (st->df_flags) c.retired.push_back(st->df_flags);
+    WF_CUDA(cudaMalloc(&st->df_flags, need * sizeof(unsigned)));
+    WF_CUDA(cudaMemsetAsync(st->df_flags, 0, need * sizeof(unsigned), c.st));
+    st->df_cap = need;
+  }
+  A.flags = st->df_flags;
+  A.ep = st->df_ep;
+  k_trsm_df<NB, UPPER><<<A.ntile * A.panels, 128, smem, c.st>>>(A);
+  WF_CUDA(cudaGetLastError());
+}
+
 // Small triangles: every segment (diagonal block) has <= 64 rows -- R_hat / D_hat of the
 // L96 configs (s = 40, 50; p = 20, 25) and the R_block blocks.  The 64-row panel kernel
 // above spends such a solve in the shuffle chain of a mostly empty tile; here one
@@ -420,9 +608,23 @@ static void run_small(Ctx &c, const TrsmLaunch &L, int chunks, int nseg, int max
   WF_CUDA(cudaGetLastError());
 }
 
+// the dataflow kernel applies to dense factors with packed inverse diagonal tiles
+// (WF4DVAR_TRSM_DF=0: never)
+// (dense: the registered tile ranges of a full triangle are the triangle itself, so the
+// kernel's dependency K loop covers exactly them; narrow-band factors keep the panel walk,
+// whose K loops skip the zero tiles -- the caller passes allow_df = false for those)
+static bool df_ok(const TrsmProb *p, int np) {
+  static const int df_env = env_int("WF4DVAR_TRSM_DF", 1);
+  if (!df_env || !trsm_inv_mode()) return false;
+  for (int i = 0; i < np; ++i)
+    if (!p[i].dpack || p[i].blk || p[i].segs) return false;
+  return true;
+}
+
 // one k_trsm launch over segments [seg_lo + j*seg_len ...) of every problem
 static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int seg_lo,
-                          int seg_len, int seg_hi, const std::vector<int> *tab = nullptr) {
+                          int seg_len, int seg_hi, const std::vector<int> *tab = nullptr,
+                          bool allow_df = true) {
   TrsmLaunch L{};
   int total_cols = 0;
   bool v16 = (seg_len % 2 == 0) && (seg_lo % 2 == 0);
@@ -486,13 +688,43 @@ static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int
     c.launches++;
     return;
   }
+  // one dense segment, inverse diagonal tiles packed, 16-byte aligned operands: the
+  // dataflow kernel (WF4DVAR_TRSM_DF=0: the panel walk)
+  static const int nb_env = env_int("WF4DVAR_TRSM_NB", 0);   // tuning experiments only
+  if (allow_df && nseg == 1 && !tab && v16 && (seg_lo % TB) == 0 && df_ok(L.p, np)) {
+    TrsmDfArgs A{};
+    A.p[0] = L.p[0];
+    if (np > 1) A.p[1] = L.p[1];
+    A.slo = seg_lo; A.shi = seg_hi;
+    A.ntile = (seg_hi - seg_lo + TB - 1) / TB;
+    // panel width: the widest of 32 / 16 / 8 columns that still gives >= 2 CTAs per SM
+    int nb = 32;
+    auto ctas = [&](int w) {
+      int t = 0;
+      for (int i = 0; i < np; ++i) t += (L.p[i].ncols + w - 1) / w;
+      return t * A.ntile;
+    };
+    if (ctas(32) < 2 * 148) nb = 16;
+    if (nb == 16 && ctas(16) < 2 * 148) nb = 8;
+    if (nb_env == 8 || nb_env == 16 || nb_env == 32) nb = nb_env;
+    A.panels0 = (L.p[0].ncols + nb - 1) / nb;
+    A.panels = A.panels0 + (np > 1 ? (L.p[1].ncols + nb - 1) / nb : 0);
+    if (np == 1) A.panels0 = A.panels;
+    LaunchScope ls(c, K_TRSM, flops, bytes);
+    switch (nb) {
+      case 32: upper ? run_df<32, true>(c, A) : run_df<32, false>(c, A); break;
+      case 16: upper ? run_df<16, true>(c, A) : run_df<16, false>(c, A); break;
+      default: upper ? run_df<8, true>(c, A) : run_df<8, false>(c, A); break;
+    }
+    c.launches++;
+    return;
+  }
   // panel width: as wide as possible while still filling the SMs
   const int ctas_per_col = nseg;
   int NB = 64;
   if ((total_cols + 63) / 64 * ctas_per_col < 148) NB = 32;
   if ((total_cols + 31) / 32 * ctas_per_col < 148) NB = 16;
   if ((total_cols + 15) / 16 * ctas_per_col < 148) NB = 8;
-  static const int nb_env = env_int("WF4DVAR_TRSM_NB", 0);   // tuning experiments only
   if (nb_env == 8 || nb_env == 16 || nb_env == 32 || nb_env == 64) NB = nb_env;
   int panels = 0;
   for (int i = 0; i < np; ++i) {
@@ -596,6 +828,15 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     return;
   }
   static const int sb_env = env_int("WF4DVAR_TRSM_SB", 0);   // tuning experiments only
+  // the dataflow kernel needs no coupling GEMMs between super-blocks: for n <= 2048 one
+  // launch over the whole triangle (ntile x panels CTAs, K up to n) -- the blocked
+  // scheme's 2 (n / SB) - 1 launches per solve were what made configs[1]'s solves
+  // latency bound (16 panel walks + 12 GEMMs per step)
+  static const int df_whole = env_int("WF4DVAR_TRSM_DF_WHOLE", 2048);
+  if (!sb_env && leaf == 0 && !banded && n <= df_whole && df_ok(probs, np)) {
+    trsm_segments(c, probs, np, upper, 0, n, n);
+    return;
+  }
   // measured (tools/kbench.py, r01): at n = 4096 SB = 512 gives 19.1 TFLOP/s vs 16.2
   // (256) and 12.3 (128) -- the coupling GEMMs need K >= 512 to run efficiently
   // (1024 at n = 4096: 20.6 TFLOP/s, above cuBLAS DTRSM's 18.8 on the same shape)
@@ -612,7 +853,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
                  : (n >= 4096 ? (total_cols <= 1536 ? 512 : 1024)
                               : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
   if (n <= SB) {
-    trsm_segments(c, probs, np, upper, 0, n, n);
+    trsm_segments(c, probs, np, upper, 0, n, n, nullptr, !banded);
     return;
   }
   const int nsb = (n + SB - 1) / SB;
@@ -644,7 +885,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
         launch_gemm(c, g, np, 1);
         c.gemm_cls = K_GEMM;
       }
-      trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
+      trsm_segments(c, cur, np, upper, lo, hi - lo, hi, nullptr, !banded);
     }
     return;
   }
@@ -653,7 +894,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   for (int it = 0; it < nsb; ++it) {
     const int kb = upper ? nsb - 1 - it : it;
     const int lo = kb * SB, hi = std::min(n, lo + SB);
-    trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
+    trsm_segments(c, cur, np, upper, lo, hi - lo, hi, nullptr, !banded);
     // couple the solved block to the rest:  Y_rest = Z_rest - G_rest,blk Y_blk
     const int rlo = upper ? 0 : hi, rhi = upper ? lo : n;
     if (rhi > rlo) {

@@ -117,7 +117,10 @@ def test_identical_to_dense_k_loop(tmp_path):
     for flag in ("1", "0"):
         # same super-block size on both sides (a narrow-band factor otherwise takes one
         # panel walk, a different blocking of the same sums)
-        env = dict(os.environ, WF4DVAR_BANDED=flag, WF4DVAR_TRSM_BANDED_SB="0")
+        # and the same triangular-solve kernel (without registered ranges a factor is
+        # dense to the library, which would take the dataflow TRSM)
+        env = dict(os.environ, WF4DVAR_BANDED=flag, WF4DVAR_TRSM_BANDED_SB="0",
+                   WF4DVAR_TRSM_DF="0")
         out = tmp_path / f"b{flag}.npy"
         r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, str(out)], env=env,
                            capture_output=True, text=True, timeout=600)
