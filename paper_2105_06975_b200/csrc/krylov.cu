@@ -474,7 +474,11 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
 }
 
 // ------------------------------------------------------------------ GMRES
-// partial dots of w with basis vectors V_i, i in [i0, i0+8) ∩ [0, nv): grid.z = group
+// partial dots of w with basis vectors V_i, i in [i0, i0+8) ∩ [0, nv): grid.z = group.
+// (r02r tried the groups of one row block back to back, blockIdx.x = group, so that w's
+// rows would be re-read from L2 rather than DRAM: configs[4]'s dot class went 4.4 -> 3.4
+// TB/s -- eight basis vectors per block at 7 row offsets at once spread the DRAM
+// streams -- and was reverted)
 __global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64_t n, int nv,
                                                           const double *w, int64_t rows, int m,
                                                           int RB, int64_t rpb, double *part,

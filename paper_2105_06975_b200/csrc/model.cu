@@ -341,8 +341,17 @@ __global__ void __launch_bounds__(WARPS * 32, R <= 128 ? 4 : 2) k_heat_iir_scan(
 // This is k_heat_iir's arithmetic with TI = R (restart H rows early, dropped tail
 // < 1e-17 relative), at ~(2H + 1) / R + 2 serial FMAs per output and one shared load
 // each; the tile is read from DRAM once (plus its 2H-row halo, mostly L2 hits).
+// resident CTAs per SM: as many as shared memory allows (228 KB, 1 KB reserved per CTA),
+// but never fewer than 64 registers per thread (R = 16's 16 staged base rows)
 template <int H, int R, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS * R + 2 * H + 1) * 256 <= 56 * 1024 ? 4 : 2)
+constexpr int heat_seq_ctas() {
+  constexpr int by_smem = (228 * 1024) / ((WARPS * R + 2 * H + 1) * 256 + 1024);
+  constexpr int by_reg = 1024 / (WARPS * 32);   // keep >= 64 registers per thread
+  return by_smem < by_reg ? by_smem : by_reg;
+}
+
+template <int H, int R, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, heat_seq_ctas<H, R, WARPS>())
 k_heat_iir_seq(double *out, const double *base, const double *in, const double *add2,
                const int *row_map, double rho, double gain, int s, int W, int m, int w_first,
                int w_step, int nw, int dir, const double *halo, int w0, int WG) {
@@ -644,10 +653,11 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // cp.async staging R = 128: 1.110 ms (2.63 TB/s), R = 256: 1.431 ms (fewer CTAs per SM)
     // r02o: column-sequential kernel (WF4DVAR_HEAT_SEQ = rows per warp, 0: off)
     static const int seq_env = env_int("WF4DVAR_HEAT_SEQ", 16);   // r02p: R = 16 4.92 TB/s, 32: 4.61
+    static const int seqw_env = env_int("WF4DVAR_HEAT_SEQW", 8);   // warps per CTA (4 / 8 / 16)
     if (seq_env == 16 || seq_env == 32) {
-      constexpr int WARPS = 8;
-      auto go = [&](auto r_tag) {
+      auto go2 = [&](auto r_tag, auto w_tag) {
         constexpr int R = decltype(r_tag)::value;
+        constexpr int WARPS = decltype(w_tag)::value;
         constexpr size_t smem = (size_t)(WARPS * R + 2 * H + 1) * 32 * sizeof(double);
         static const cudaError_t attr = cudaFuncSetAttribute(
             k_heat_iir_seq<H, R, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -657,8 +667,11 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
             out, base, in, add2, row_map, c.heat_rho, sign * c.heat_gain, c.s, c.W, c.m, w_first,
             w_step, nw, transpose ? 1 : -1, transpose ? c.halo_hi : c.halo_lo, c.w0, c.WG);
       };
-      if (seq_env == 16) go(std::integral_constant<int, 16>{});
-      else go(std::integral_constant<int, 32>{});
+      using I16 = std::integral_constant<int, 16>;
+      if (seq_env == 32) go2(std::integral_constant<int, 32>{}, std::integral_constant<int, 8>{});
+      else if (seqw_env == 4) go2(I16{}, std::integral_constant<int, 4>{});
+      else if (seqw_env == 16) go2(I16{}, std::integral_constant<int, 16>{});
+      else go2(I16{}, std::integral_constant<int, 8>{});
       WF_CUDA(cudaGetLastError());
       return;
     }

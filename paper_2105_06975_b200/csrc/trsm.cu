@@ -318,7 +318,12 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
       int k = done;
       while (ld_acquire_u32(dep_flag(k)) != want) __nanosleep(32);
       ++k;
-      while (k < it && ld_acquire_u32(dep_flag(k)) == want) ++k;   // everything ready now
+      // lower: every tile ready now, one increasing-k sweep (the chunking does not change
+      // the summation order).  Upper: one tile per sweep -- its tiles arrive in decreasing
+      // order, and a multi-tile sweep would sum them in increasing order, so the result
+      // would depend on the arrival timing (deterministic results are tested bitwise)
+      if (!UPPER)
+        while (k < it && ld_acquire_u32(dep_flag(k)) == want) ++k;
       s_ready = k;
     }
     __syncthreads();
@@ -624,7 +629,7 @@ static bool df_ok(const TrsmProb *p, int np) {
 // one k_trsm launch over segments [seg_lo + j*seg_len ...) of every problem
 static void trsm_segments(Ctx &c, const TrsmProb *probs, int np, bool upper, int seg_lo,
                           int seg_len, int seg_hi, const std::vector<int> *tab = nullptr,
-                          bool allow_df = true) {
+                          bool allow_df = false) {
   TrsmLaunch L{};
   int total_cols = 0;
   bool v16 = (seg_len % 2 == 0) && (seg_lo % 2 == 0);
@@ -828,13 +833,18 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     return;
   }
   static const int sb_env = env_int("WF4DVAR_TRSM_SB", 0);   // tuning experiments only
-  // the dataflow kernel needs no coupling GEMMs between super-blocks: for n <= 2048 one
-  // launch over the whole triangle (ntile x panels CTAs, K up to n) -- the blocked
-  // scheme's 2 (n / SB) - 1 launches per solve were what made configs[1]'s solves
-  // latency bound (16 panel walks + 12 GEMMs per step)
+  // the dataflow kernel needs no coupling GEMMs between super-blocks: one launch over the
+  // whole triangle (ntile x panels CTAs, K up to n) where the blocked scheme's
+  // 2 (n / SB) - 1 launches per solve leave the GPU latency bound: narrow right-hand
+  // sides.  r02q per step: configs[1] (n = 1000 / 500, 336 columns) GMRES 0.592 -> 0.548
+  // ms, MINRES 0.426 -> 0.364 ms; but wide ones lose -- configs[4] (n = 2048, 8192
+  // columns) 18.68 -> 19.07 ms, configs[3] with the dataflow kernel at the 512-row leaves
+  // 29.46 -> 30.06 ms, over the whole triangle 32.5 ms (its 64 x NB tiles run the long K
+  // loops at ~21 TFLOP/s against the coupling GEMMs' 28)
   static const int df_whole = env_int("WF4DVAR_TRSM_DF_WHOLE", 2048);
-  if (!sb_env && leaf == 0 && !banded && n <= df_whole && df_ok(probs, np)) {
-    trsm_segments(c, probs, np, upper, 0, n, n);
+  static const int df_cols = env_int("WF4DVAR_TRSM_DF_COLS", 1024);
+  if (!sb_env && !banded && n <= df_whole && total_cols0 <= df_cols && df_ok(probs, np)) {
+    trsm_segments(c, probs, np, upper, 0, n, n, nullptr, true);
     return;
   }
   // measured (tools/kbench.py, r01): at n = 4096 SB = 512 gives 19.1 TFLOP/s vs 16.2
@@ -853,7 +863,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
                  : (n >= 4096 ? (total_cols <= 1536 ? 512 : 1024)
                               : (n >= 2048 ? 512 : (n >= 512 ? 256 : 128)));
   if (n <= SB) {
-    trsm_segments(c, probs, np, upper, 0, n, n, nullptr, !banded);
+    trsm_segments(c, probs, np, upper, 0, n, n);
     return;
   }
   const int nsb = (n + SB - 1) / SB;
@@ -885,7 +895,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
         launch_gemm(c, g, np, 1);
         c.gemm_cls = K_GEMM;
       }
-      trsm_segments(c, cur, np, upper, lo, hi - lo, hi, nullptr, !banded);
+      trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
     }
     return;
   }
@@ -894,7 +904,7 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
   for (int it = 0; it < nsb; ++it) {
     const int kb = upper ? nsb - 1 - it : it;
     const int lo = kb * SB, hi = std::min(n, lo + SB);
-    trsm_segments(c, cur, np, upper, lo, hi - lo, hi, nullptr, !banded);
+    trsm_segments(c, cur, np, upper, lo, hi - lo, hi);
     // couple the solved block to the rest:  Y_rest = Z_rest - G_rest,blk Y_blk
     const int rlo = upper ? 0 : hi, rhi = upper ? lo : n;
     if (rhi > rlo) {

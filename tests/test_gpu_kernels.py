@@ -94,6 +94,28 @@ def test_trsm_vs_float64_reference(n, ncols, blk, upper):
     assert fwd <= 1e-12, fwd
 
 
+@pytest.mark.parametrize("upper", [False, True])
+def test_trsm_dataflow_bitwise_reproducible(upper):
+    """n = 1000, 336 columns takes the dataflow TRSM (k_trsm_df): its CTAs consume their
+    dependency tiles as they are published, so arrival order varies run to run; the
+    summation order must not (lower: increasing-k sweeps; upper: one tile per sweep)."""
+    n, ncols = 1000, 336
+    g = torch.Generator().manual_seed(11)
+    M = torch.randn(n, n, generator=g, dtype=torch.float64)
+    S = M @ M.T / n + torch.eye(n, dtype=torch.float64)
+    F = torch.linalg.cholesky(S)
+    F = (F.T if upper else F).contiguous().cuda()
+    X = torch.randn(n, ncols, generator=g, dtype=torch.float64).cuda()
+    outs = []
+    for _ in range(6):
+        Y = torch.empty(n, ncols, dtype=torch.float64, device="cuda")
+        L().test_trsm(F, X, Y, upper=upper)
+        outs.append(Y)
+    torch.cuda.synchronize()
+    for Y in outs[1:]:
+        assert torch.equal(Y, outs[0])
+
+
 def test_trsm_in_place():
     n, ncols = 700, 50
     S = torch.randn(n, n, dtype=torch.float64)

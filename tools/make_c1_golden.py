@@ -44,6 +44,12 @@ def main():
                          "relative noise on every P^{-1} output (3 seeds, first --sens-its "
                          "iterations), max over seeds of |h_noisy / h - 1| per iteration")
     ap.add_argument("--sens-its", type=int, default=100)
+    ap.add_argument("--noise", default="output", choices=["output", "input"],
+                    help="--sens: where the 1e-15 relative noise enters P^{-1}.  'input' is the "
+                         "backward-error model of a backward-stable solve, (C + E)^{-1} x = "
+                         "C^{-1} (x - E y): its output moves by up to kappa(C) 1e-15 -- the size of "
+                         "the differences two correct implementations' triangular solves have "
+                         "(reading A34); 'output' (the round-1 model) moves it by 1e-15 only")
     ap.add_argument("--seeds", type=int, default=3)
     ap.add_argument("--config", type=int, default=1, choices=[1, 4])
     a = ap.parse_args()
@@ -55,11 +61,15 @@ def main():
         res = []
         for f in sorted(glob.glob(OUT + ".part*")):
             res += json.load(open(f))
-        sens = {}
-        for f in sorted(glob.glob(OUT + ".sens*")):
+        sens, sens_in = {}, {}
+        for f in sorted(glob.glob(OUT + ".sens[0-9]*")):
             sens.update({d["index"]: d["sens"] for d in json.load(open(f))})
+        for f in sorted(glob.glob(OUT + ".sensin[0-9]*")):
+            sens_in.update({d["index"]: d["sens"] for d in json.load(open(f))})
         for d in res:
             d["sens"] = sens.get(d["index"])
+            if d["index"] in sens_in:
+                d["sens_in"] = sens_in[d["index"]]
         res.sort(key=lambda d: d["index"])
         json.dump(dict(source="tools/make_c1_golden.py (oracle/ only): oracle.saddle blockwise A, "
                               "P_D / P_I (P:L629-667) and oracle.krylov.gmres (CGS2, restart 50)",
@@ -83,8 +93,14 @@ def main():
             if j % n != i:
                 continue
             pc = Precond(c[0], c[1], c[2], c[3], block=blk)
-            run = lambda nz: np.array(KR.gmres(sad.apply_A, lambda v: nz(sad.apply_Pinv(pc, v)), bp,
-                                               tol=1e-10, restart=50, maxit=a.sens_its)[1]["history"])
+            if a.noise == "input":
+                run = lambda nz: np.array(KR.gmres(sad.apply_A, lambda v: sad.apply_Pinv(pc, nz(v)),
+                                                   bp, tol=1e-10, restart=50,
+                                                   maxit=a.sens_its)[1]["history"])
+            else:
+                run = lambda nz: np.array(KR.gmres(sad.apply_A, lambda v: nz(sad.apply_Pinv(pc, v)),
+                                                   bp, tol=1e-10, restart=50,
+                                                   maxit=a.sens_its)[1]["history"])
             h0 = run(lambda v: v)
             worst = np.zeros(h0.size)
             for seed in range(1, a.seeds + 1):
@@ -94,7 +110,7 @@ def main():
                 worst[:k] = np.maximum(worst[:k], np.abs(h1[:k] / h0[:k] - 1))
             res.append(dict(index=j, sens=[float(v) for v in worst]))
             print(j, c, "sens max %.1e" % worst.max(), flush=True)
-            json.dump(res, open(OUT + f".sens{i}", "w"))
+            json.dump(res, open(OUT + (f".sens{i}" if a.noise == "output" else f".sensin{i}"), "w"))
         return
     for j, c in enumerate(cells(a.config)):
         if j % n != i:
