@@ -34,8 +34,10 @@ def build(verbose=False, force=False):
     # whole-program compilation is not needed), then one host link
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
+    # WF4DVAR_NVCC_FLAGS: extra flags for tuning experiments (e.g. -DL96_MINB_F=2); pass
+    # force=True when they change (object files are reused by modification time only)
     ccmd = [_nvcc(), ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-            "-Xptxas", "-v" if verbose else "-O3", "-c"]
+            "-Xptxas", "-v" if verbose else "-O3"] + os.environ.get("WF4DVAR_NVCC_FLAGS", "").split() + ["-c"]
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
 
     def _one(so):

@@ -176,7 +176,15 @@ __device__ __forceinline__ void rk4_stages(const double (&x)[IPT], double (&x2)[
 // adjoint are separate instantiations so each gets its own register allocation, and
 // the IPT = 5 (s <= 40) variants are held to 2 CTAs per SM (IPT = 8 would spill).
 template <int IPT, int NSUB_MAX, bool SH, bool ADJ>
-__global__ void __launch_bounds__(256, IPT <= 5 ? 2 : 1) k_l96_step(const L96Args a) {
+#ifndef L96_MINB_F
+#define L96_MINB_F 2   // r02w (configs[2] step): 2 CTAs per SM (96 registers) 0.519 ms,
+                       // 3 (80 registers, 48-byte spill) 0.522, 4 (64, 232-byte spill) 0.595
+#endif
+#ifndef L96_MINB_A
+#define L96_MINB_A 2   // adjoint: 3 CTAs spill 552 bytes (with forward 3: 0.538 ms)
+#endif
+__global__ void __launch_bounds__(256, IPT <= 5 ? (ADJ ? L96_MINB_A : L96_MINB_F) : 1)
+k_l96_step(const L96Args a) {
   extern __shared__ double xs_sm[];
   __shared__ double bx[SH ? 1 : L96Thread<IPT>::S_MAX * 32];
   __shared__ double bu[SH ? 1 : L96Thread<IPT>::S_MAX * 32];

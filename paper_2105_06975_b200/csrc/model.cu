@@ -654,7 +654,13 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
     // r02o: column-sequential kernel (WF4DVAR_HEAT_SEQ = rows per warp, 0: off)
     static const int seq_env = env_int("WF4DVAR_HEAT_SEQ", 16);   // r02p: R = 16 4.92 TB/s, 32: 4.61
     static const int seqw_env = env_int("WF4DVAR_HEAT_SEQW", 8);   // warps per CTA (4 / 8 / 16)
-    if (seq_env == 16 || seq_env == 32) {
+    // small launches (configs[1]'s chain steps: 80 columns x 1000 rows = 24 CTAs of 32 x 128)
+    // leave most SMs idle; WF4DVAR_HEAT_SEQ_MINCTA=K sends launches of fewer than K such
+    // CTAs to the thread-per-chunk form (8 rows per thread, 128 columns per CTA: 125 CTAs
+    // there).  r02w, configs[1] MINRES step: K = 148 0.340 ms, off (default) 0.336 ms
+    static const int seq_min = env_int("WF4DVAR_HEAT_SEQ_MINCTA", 0);
+    const int seq_ctas = ((cols + 31) / 32) * ((c.s + 8 * seq_env - 1) / (8 * std::max(seq_env, 1)));
+    if ((seq_env == 16 || seq_env == 32) && seq_ctas >= seq_min) {
       auto go2 = [&](auto r_tag, auto w_tag) {
         constexpr int R = decltype(r_tag)::value;
         constexpr int WARPS = decltype(w_tag)::value;
@@ -676,10 +682,10 @@ static void heat_iir_launch(Ctx &c, bool transpose, double sign, const double *i
       return;
     }
     static const int tile_env = env_int("WF4DVAR_HEAT_TILE", 128);   // 0: thread-per-chunk form
-    // (every size: r02n measured the thread-per-chunk form on configs[0] moving a
-    // restarted-GMRES solution to the edge of its 1e-9 parity bound -- a rounding-order
-    // effect at the stop, not a speed matter for a 5-column problem)
-    if (tile_env == 64 || tile_env == 128 || tile_env == 256) {
+    // (the warp-scan form: opt-in, WF4DVAR_HEAT_SEQ=0; launches too small for the
+    // column-sequential kernel take the thread-per-chunk form below)
+    const bool small = (seq_env == 16 || seq_env == 32);   // seq default, too few CTAs
+    if (!small && (tile_env == 64 || tile_env == 128 || tile_env == 256)) {
       constexpr int WARPS = 8;
       auto go = [&](auto r_tag) {
         constexpr int R = decltype(r_tag)::value;

@@ -295,9 +295,16 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
   const int ncols = P.ncols;
-  // the inverse diagonal tile: in flight under the dependency wait and the products
+  // the inverse diagonal tile and this tile's X rows: in flight under the dependency
+  // waits and the products (X_t is read only here; in place, only this CTA writes Y_t)
   const double *dpk = P.dpack + (int64_t)(r0 / TB) * kDiagPack;
   for (int e = 2 * tid; e < kDiagPack; e += 2 * 128) cp_async16(sG + e, dpk + e, 16);
+  for (int e = tid; e < TB * NB; e += 128) {
+    const int rr = e / NB, cc = e % NB;
+    const bool ok = rr < nr && c0 + cc < ncols;
+    cp_async8(sT + rr * (NB + 1) + cc, ok ? P.X + (int64_t)(r0 + rr) * P.ldx + c0 + cc : P.X,
+              ok ? 8 : 0);
+  }
   cp_async_commit();
   if (tid == 0) s_ep = __ldcg(L.ep);
   __syncthreads();
@@ -308,12 +315,15 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   // dependencies: the tiles before this one in solve order, it' = 0 .. it-1
-  auto dep_flag = [&](int k) {   // flag of the k-th tile in solve order, this panel
-    const int tk = UPPER ? L.ntile - 1 - k : k;
-    return L.flags + (int64_t)tk * L.panels + pc;
+  auto dep_tile = [&](int k) { return UPPER ? L.ntile - 1 - k : k; };
+  auto dep_flag = [&](int k) { return L.flags + (int64_t)dep_tile(k) * L.panels + pc; };
+  auto wait_dep = [&](int k) {
+    if (tid == 0)
+      while (ld_acquire_u32(dep_flag(k)) != want) __nanosleep(20);
   };
+  // all but the last dependency through the cp.async DMMA main loop, as they arrive
   int done = 0;
-  while (done < it) {
+  while (done < it - 1) {
     if (tid == 0) {
       int k = done;
       while (ld_acquire_u32(dep_flag(k)) != want) __nanosleep(32);
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
       // order, and a multi-tile sweep would sum them in increasing order, so the result
       // would depend on the arrival timing (deterministic results are tested bitwise)
       if (!UPPER)
-        while (k < it && ld_acquire_u32(dep_flag(k)) == want) ++k;
+        while (k < it - 1 && ld_acquire_u32(dep_flag(k)) == want) ++k;
       s_ready = k;
     }
     __syncthreads();
@@ -340,7 +350,50 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
                            kb, ke, nr, ncols - c0);   // ends with __syncthreads
     done = k1;
   }
-  // T = X - acc -> shared memory
+  // the last dependency (the previous tile, on the critical path): its 64 x 64 block of G
+  // is staged before its flag is awaited, so after the flag only Y_j (64 x NB, from L2)
+  // is loaded before the product
+  if (it >= 1) {
+    const int jt = dep_tile(it - 1);
+    const int jc0 = L.slo + jt * TB, jw = min(TB, L.shi - jc0);
+    double *sGl = sPipe;                       // [64][kInvLd]
+    double *sYl = sPipe + TB * kInvLd;         // [64][NB + 4]
+    constexpr int LDY = NB + 4;
+    static_assert(TB * kInvLd + TB * (NB + 4) <= C::SMEM_DOUBLES, "last-dependency staging");
+    for (int e = tid; e < TB * (TB / 2); e += 128) {
+      const int rr = e / (TB / 2), cp = (e % (TB / 2)) * 2;
+      const int bytes = rr < nr ? max(0, min(2, jw - cp)) * 8 : 0;
+      cp_async16(sGl + rr * kInvLd + cp, bytes ? P.G + (int64_t)(r0 + rr) * P.ldg + jc0 + cp : P.G,
+                 bytes);
+    }
+    cp_async_commit();
+    wait_dep(it - 1);
+    __syncthreads();
+    for (int e = tid; e < TB * (NB / 2); e += 128) {
+      const int rr = e / (NB / 2), cp = (e % (NB / 2)) * 2;
+      const int bytes = rr < jw ? max(0, min(2, ncols - c0 - cp)) * 8 : 0;
+      cp_async16(sYl + rr * LDY + cp, bytes ? P.Y + (int64_t)(jc0 + rr) * P.ldy + c0 + cp : P.Y,
+                 bytes);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < TB; kk += 4) {
+      double a[C::FM], b[C::FN];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i) a[i] = sGl[(wm * C::WM + i * 8 + g) * kInvLd + kk + t];
+#pragma unroll
+      for (int j = 0; j < C::FN; ++j) b[j] = sYl[(kk + t) * LDY + wn * C::WN + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < C::FM; ++i)
+#pragma unroll
+        for (int j = 0; j < C::FN; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  // T = X - acc (X staged in sT at the start)
+  cp_async_wait<0>();
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < C::FM; ++i) {
     const int rr = wm * C::WM + i * 8 + g;
@@ -349,9 +402,7 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int cc = wn * C::WN + j * 8 + 2 * t + h;
-        double xv = 0.0;
-        if (rr < nr && c0 + cc < ncols) xv = P.X[(int64_t)(r0 + rr) * P.ldx + c0 + cc];
-        sT[rr * (NB + 1) + cc] = xv - acc[i][j][h];
+        sT[rr * (NB + 1) + cc] -= acc[i][j][h];
       }
   }
   cp_async_wait<0>();
