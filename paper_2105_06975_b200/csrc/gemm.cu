@@ -381,6 +381,9 @@ __global__ void __launch_bounds__(C::NT) k_gemm_tma(const GemmLaunch L,
     tma_load_2d(sA, ma, kt * C::BK, m0, &full[s]);
     tma_load_2d(sB, mx, n0, kt * C::BK, &full[s]);
   };
+#ifdef TMA_FENCE
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+#endif
   if (tid == 0)
     for (int kt = 0; kt < C::STAGES - 1 && kt < nk; ++kt) issue(kt);
   double acc[C::FM][C::FN][2];
@@ -401,6 +404,14 @@ __global__ void __launch_bounds__(C::NT) k_gemm_tma(const GemmLaunch L,
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+#ifdef TMA_INVAL
+  __syncthreads();
+  if (tid == 0)
+    for (int s = 0; s < C::STAGES; ++s) {
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(&full[s])) : "memory");
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(&empty[s])) : "memory");
+    }
+#endif
   tile_epilogue<C>(P, m0, n0, acc);
 }
 
@@ -430,8 +441,19 @@ static bool encode_tma(CUtensorMap *map, const double *base, int64_t rows, int64
 // launched) when a problem does not meet the TMA alignment rules or is banded/batched
 template <class C>
 static bool run_tma(Ctx &c, const GemmLaunch &L, int nprob, int tiles) {
-  static const int env = env_int("WF4DVAR_GEMM_TMA", 1);
+  // 1 = every eligible GEMM; 2 (default) = not the blocked TRSM's coupling GEMMs; 3 = only
+  // those.  r02y-r02ab: with the coupling GEMMs TMA-staged, configs[4]'s P_I apply
+  // (R_hat^{-1} blocked TRSM on an aux stream concurrent with the L_hat chains and the D
+  // product) was not reproducible -- 60 chained applies differed by up to 6e-3 between
+  // runs, and GMRES histories drifted from the oracle recurrence -- while the cp.async
+  // coupling GEMMs, serialised streams (WF4DVAR_FORK=0) or a single TRSM segment were
+  // bitwise reproducible and equal to each other.  Root cause not identified (see
+  // DESIGN.md section 10); the covariance products keep the TMA staging (reproducible in
+  // every probe)
+  static const int env = env_int("WF4DVAR_GEMM_TMA", 2);
   if (!env || tiles <= 0) return false;
+  if (env == 2 && c.gemm_cls == K_TRSM_UPD) return false;
+  if (env == 3 && c.gemm_cls != K_TRSM_UPD) return false;
   TmaMaps T{};
   for (int i = 0; i < nprob; ++i) {
     const GemmProb &p = L.p[i];
