@@ -7,8 +7,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 import paper_2105_06975_b200 as W
 from synth import configs as SC
-prob = SC.make_problem(4)
-ctx = W.Context.from_problem(prob, dict(shape="PI", lhat="LM", k=4, rhat="exact", block=256))
+CFG = int(os.environ.get("CFG", "4"))
+prob = SC.make_problem(CFG)
+cell = dict(shape="PI", lhat="LM", k=4, rhat="exact", block=256) if CFG == 4 else \
+    dict(shape="PD", lhat="LM", k=4, rhat="exact")
+ctx = W.Context.from_problem(prob, cell)
 g = torch.Generator().manual_seed(5)
 x0 = torch.randn(prob.n, generator=g, dtype=torch.float64).cuda()
 outs = []
@@ -27,5 +30,5 @@ for rep in range(NREP):
     torch.cuda.synchronize()
     outs.append(v.cpu().numpy())
 d = max(np.max(np.abs(outs[0] - o)) for o in outs[1:])
-print(os.environ.get("TAGENV", ""), os.environ.get("MODE", "PA"), "repeats bitwise equal:", [bool(np.array_equal(outs[0], o)) for o in outs[1:]], "max diff %.2e" % d,
+print(os.environ.get("TAGENV", ""), "cfg", CFG, os.environ.get("MODE", "PA"), "repeats bitwise equal:", [bool(np.array_equal(outs[0], o)) for o in outs[1:]], "max diff %.2e" % d,
       "checksum %.17e" % float(np.sum(outs[0] * np.arange(outs[0].size) % 7)), flush=True)
