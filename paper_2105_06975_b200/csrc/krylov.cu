@@ -479,24 +479,24 @@ static void minres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts 
 // rows would be re-read from L2 rather than DRAM: configs[4]'s dot class went 4.4 -> 3.4
 // TB/s -- eight basis vectors per block at 7 row offsets at once spread the DRAM
 // streams -- and was reverted)
+template <int GV, int RU>
 __global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64_t n, int nv,
                                                           const double *w, int64_t rows, int m,
                                                           int RB, int64_t rpb, double *part,
                                                           int jmax) {
-  __shared__ double sm[8][256];
+  __shared__ double sm[GV][256];
   const int t = threadIdx.x;
   const int rl = t % RB, u = t / RB, U = 256 / RB;
   const int r = blockIdx.x * RB + rl;
-  const int i0 = blockIdx.z * 8;
+  const int i0 = blockIdx.z * GV;
   const int64_t row0 = (int64_t)blockIdx.y * rpb, row1 = min(rows, row0 + rpb);
-  double acc[8];
+  double acc[GV];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) acc[k] = 0.0;
+  for (int k = 0; k < GV; ++k) acc[k] = 0.0;
   if (r < m && u < U) {
-    // 4 rows per iteration: up to 32 independent basis loads in flight and 4 x 2 KB
+    // RU rows per iteration: up to GV x RU independent basis loads in flight and RU x 2 KB
     // contiguous runs per vector per block (ncu r01q: the 1-row loop reached 44% of
     // DRAM bandwidth, stalled on long-scoreboard)
-    constexpr int RU = 4;
     for (int64_t row = row0 + u; row < row1; row += (int64_t)U * RU) {
       double wv[RU];
       int64_t f[RU];
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64
         wv[q] = rq < row1 ? w[f[q]] : 0.0;
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < GV; ++k) {
         if (i0 + k < nv) {
           const double *Vk = V + (int64_t)(i0 + k) * n;
           double vv[RU];
@@ -520,10 +520,10 @@ __global__ void __launch_bounds__(256) k_multidot_partial(const double *V, int64
     }
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) sm[k][t] = acc[k];
+  for (int k = 0; k < GV; ++k) sm[k][t] = acc[k];
   __syncthreads();
   if (u == 0 && r < m) {
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < GV; ++k) {
       if (i0 + k >= nv) break;
       double v = 0.0;
       for (int uu = 0; uu < U; ++uu) v += sm[k][uu * RB + rl];
@@ -883,8 +883,17 @@ static void gmres(Ctx &c, const double *b, double *x, const wf4dvar_solve_opts &
 
   auto multidot = [&](int nv, const double *w, double *out) {
     LaunchScope ls(c, K_DOT, 2.0 * nv * n, 8.0 * (nv + 1) * n);
-    dim3 grid(gx, gy, (nv + 7) / 8);
-    k_multidot_partial<<<grid, 256, 0, c.st>>>(V, n, nv, w, rows, m, RB, rpb, part, jmax);
+    // basis vectors per block: 8 (4 rows in flight per thread) or 16 (2 rows): w is
+    // re-read once per group (WF4DVAR_MULTIDOT_G, tuning; r02ah: 16 slowed configs[4]'s
+    // dot class 4.39 -> 3.94 TB/s, step 18.84 -> 19.40 ms)
+    static const int gv_env = env_int("WF4DVAR_MULTIDOT_G", 8);
+    if (gv_env == 16) {
+      dim3 grid(gx, gy, (nv + 15) / 16);
+      k_multidot_partial<16, 2><<<grid, 256, 0, c.st>>>(V, n, nv, w, rows, m, RB, rpb, part, jmax);
+    } else {
+      dim3 grid(gx, gy, (nv + 7) / 8);
+      k_multidot_partial<8, 4><<<grid, 256, 0, c.st>>>(V, n, nv, w, rows, m, RB, rpb, part, jmax);
+    }
     k_multidot_final<<<nblk((int64_t)nv * m, 8), 256, 0, c.st>>>(part, gy, nv, jmax, m, out);
     c.launches += 2;
     allreduce(c, out, (size_t)nv * m);
