@@ -239,6 +239,11 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
     }
     __syncthreads();   // Y rows visible to the whole CTA (next tile's cp.async reads)
   }
+#ifdef TRSM_PROXY_FENCE
+  // probe: order this thread's generic Y stores before any later
+  // async-proxy (TMA) access
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+#endif
 }
 
 // ---- Dataflow form of one segment (default where it applies, r02o): one CTA per
