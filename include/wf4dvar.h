@@ -81,7 +81,9 @@ typedef enum {
   WF4DVAR_M_HEAT = 1,  /* M = (I - r Lap)^{-1}, Lap = periodic second difference
                           (BJ.c0-c4); applied as its exact circulant stencil        */
   WF4DVAR_M_L96 = 2,   /* tangent linear of l96_nsub RK4 steps of Lorenz-96
-                           along l96_traj, recomputed matrix-free      */
+                           along l96_traj, recomputed matrix-free
+                          (the create call stores the RK4 substep start states
+                          on the device: N * l96_nsub * s * m doubles)            */
   WF4DVAR_M_HEAT_EXPLICIT = 3 /* the paper's own heat model: M = M_dt^n,
                           M_dt = forward-Euler Dirichlet step (first/last rows zero,
                           interior (r, 1-2r, r)), n = heat_nsteps <= 8 per window,

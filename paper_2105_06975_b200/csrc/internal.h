@@ -239,6 +239,7 @@ struct Ctx {
   double *Mdense = nullptr;       // [N][s][s]
   double *MdenseT = nullptr;      // [N][s][s] transposes
   double *traj = nullptr;         // [N][s][m]
+  double *l96_sub = nullptr;      // [N][nsub][s][m] RK4 substep start states along traj
   double l96_F = 8, l96_dt = 0.025; int l96_nsub = 5;
   // heat stencil
   int heat_D = 0;                 // half width (0 => dense path)
@@ -413,6 +414,13 @@ void model_step(Ctx &c, bool transpose, double sign, const double *in, const dou
 void l96_step(Ctx &c, bool transpose, double sign, const double *in, const double *base,
               double *out, int w_first, int w_step, int nw, const double *add2,
               const int *row_map);
+
+// Lorenz-96 chain step over two window groups in one launch (in place on z, sign +1):
+// windows f0 + i s0 (i < n0) and f1 + i (i < n1).
+void l96_step2(Ctx &c, bool transpose, double *z, int f0, int s0, int n0, int f1, int n1);
+
+// Lorenz-96: recompute c.l96_sub from c.traj (after every trajectory change).
+void l96_substates(Ctx &c);
 
 // L-hat^{-1} (forward chains) / L-hat^{-T} (backward chains) in place on z.
 void lhat_solve(Ctx &c, bool transpose, double *z);

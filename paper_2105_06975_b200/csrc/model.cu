@@ -975,6 +975,13 @@ void lhat_solve(Ctx &c, bool transpose, double *z) {
       }
       c.comm->exchange(ops, c.st);
     }
+    if (c.model == WF4DVAR_M_L96 && st.nl == 2) {
+      // the full chains' windows and the ragged last chain's window in ONE launch (a
+      // one-window Lorenz-96 launch is pure latency: 11 us at configs[2], r02al)
+      l96_step2(c, transpose, z, st.first[0], st.stride[0], st.count[0], st.first[1],
+                st.count[1]);
+      continue;
+    }
     for (int l = 0; l < st.nl; ++l)
       model_step(c, transpose, 1.0, z, z, z, st.first[l], st.stride[l], st.count[l]);
   }
@@ -1050,8 +1057,11 @@ void setup_model(Ctx &c, const wf4dvar_problem &p) {
     WF_REQUIRE(p.l96_dt > 0, WF4DVAR_EINVAL, "L96 dt must be > 0");
     c.l96_F = p.l96_F; c.l96_dt = p.l96_dt; c.l96_nsub = p.l96_nsub;
     c.traj = c.alloc<double>((size_t)std::max(N, 1) * s * c.m);
-    if (N > 0)
+    c.l96_sub = c.alloc<double>((size_t)std::max(N, 1) * c.l96_nsub * s * c.m);
+    if (N > 0) {
       WF_CUDA(memcpy_sync(c, c.traj, p.l96_traj, (size_t)N * s * c.m * 8, cudaMemcpyHostToDevice));
+      l96_substates(c);
+    }
   } else {
     throw Error{WF4DVAR_EINVAL, "unknown model kind"};
   }

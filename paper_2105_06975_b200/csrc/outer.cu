@@ -111,6 +111,7 @@ void outer_loop(Ctx &c, const double *xb, const double *y, double *x, int n_oute
                                                c.W, m, c.w0, c.N);
         WF_CUDA(cudaGetLastError());
         c.launches++;
+        l96_substates(c);
       }
       l96_forecast(c, x, fc);
     } else {

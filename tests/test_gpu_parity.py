@@ -63,6 +63,14 @@ PROBS = {
     "c1": lambda: SC.make_problem(1),
     # Lorenz-96 TLM (configs[2] recipe), 8 problems, N = 12: per-column M_w
     "l96": lambda: SC.make_problem(2, m=8, N=12),
+    # the other L96 kernel variants: shared-memory exchange with 5 and 8 states per
+    # thread (s = 24, 56), register shuffles with 8 (s = 64), and nsub != 5
+    "l96s24": lambda: SC.custom_problem(s=24, N=6, q=2, m=37, model="l96", F=8.0, dt=0.025,
+                                        nsub=3, spinup=200, seed0=7, Rp=(1.5, 0.1)),
+    "l96s56": lambda: SC.custom_problem(s=56, N=5, q=2, m=9, model="l96", F=8.0, dt=0.02,
+                                        nsub=8, spinup=200, seed0=8, Rp=(1.5, 0.1)),
+    "l96s64": lambda: SC.custom_problem(s=64, N=5, q=2, m=33, model="l96", F=8.0, dt=0.025,
+                                        nsub=1, spinup=200, seed0=9, Rp=(1.5, 0.1)),
 }
 
 
@@ -91,7 +99,8 @@ CELLS = [dict(shape=s, lhat=l, k=k, rhat=r, block=b, ridge=rd)
 CELLS.append(dict(shape="PD", lhat="LM", k=2, rhat="exact", ridge=0.01))
 
 
-@pytest.mark.parametrize("name", ["dense", "heat", "c0", "mid", "c1", "l96"])
+@pytest.mark.parametrize("name", ["dense", "heat", "c0", "mid", "c1", "l96", "l96s24", "l96s56",
+                                  "l96s64"])
 def test_apply_A(name):
     prob, ora = get(name)
     ctx = W4().Context.from_problem(prob, dict(shape="PD", lhat="LM", k=2, rhat="exact"))
@@ -163,9 +172,10 @@ L96_CELLS = [dict(shape="PD", lhat="LM", k=3, rhat="exact"),
              dict(shape="PI", lhat="LI", k=1, rhat="diag")]
 
 
+@pytest.mark.parametrize("name", ["l96", "l96s24", "l96s56", "l96s64"])
 @pytest.mark.parametrize("pc", L96_CELLS, ids=lambda p: f"{p['shape']}-{p['lhat']}{p['k']}-{p['rhat']}")
-def test_apply_P_l96(pc):
-    prob, ora = get("l96")
+def test_apply_P_l96(name, pc):
+    prob, ora = get(name)
     ctx = W4().Context.from_problem(prob, pc)
     # exact L^{-1} chains of the L96 TLM amplify rounding (||L^{-1}|| ~ 3e5 at N=50,
     # SURVEY PROBE-4, 8(c)-D2 "solve parts ... the exact-L chain"): 1e-10 there
