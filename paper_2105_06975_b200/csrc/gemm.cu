@@ -678,6 +678,124 @@ __global__ void __launch_bounds__(128) k_gemm_small(const GemmLaunch L) {
   }
 }
 
+// The same small products on the FP64 tensor pipe (round 2, r02ao): with K <= 64 the
+// streaming kernel above issues one FMA per multiply and one shared-memory A pair per
+// two FMAs, so its issue slots, not HBM, bound it (configs[2]: 29 us per 40 x 40 x 52k
+// product against ~5 us of HBM traffic).  Here each warp owns 16-column slabs of X (two
+// 8-column DMMA tiles): it loads the slab's B fragments for all of K (2 KMAX / 4
+// independent 8-byte loads per lane, in flight together; every 128-byte row segment is
+// read by one warp), then runs ceil(M/8) x K/4 pairs of DMMA.8x8x4 against A fragments
+// read from shared memory (A staged once per CTA with the conflict-free padded stride),
+// and writes its M x 16 outputs (+ beta Z, 16-byte stores when aligned).  A warp owns
+// ALL M rows of its columns, so the product may be in place (Y = X): every B fragment
+// is in registers before the first store.  Slabs per warp are set by the host so the
+// grid is ~2 waves of 8-warp CTAs.
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_gemm_small_dmma(const GemmLaunch L, int tpw) {
+  constexpr int KS = KMAX / 4, LDA = KMAX + 4;
+  __shared__ __align__(16) double sA[64 * LDA];
+  int chunk = blockIdx.x, gi = 0;
+  if (chunk >= L.tiles0) { chunk -= L.tiles0; gi = 1; }
+  const GemmProb &P = L.p[gi];
+  const int b = blockIdx.z;
+  const double *A = P.A + (int64_t)b * P.sA;
+  const double *X = P.X + (int64_t)b * P.sX;
+  double *Y = P.Y + (int64_t)b * P.sY;
+  const double *Z = P.Z ? P.Z + (int64_t)b * P.sZ : nullptr;
+  const int M = P.M, K = P.K, N = P.N;
+  const int mt = (M + 7) / 8;
+  for (int e = threadIdx.x; e < mt * 8 * KMAX; e += 256) {
+    const int r = e / KMAX, k = e % KMAX;
+    sA[r * LDA + k] = (r < M && k < K) ? A[(int64_t)r * P.lda + k] : 0.0;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  // 16 columns per warp pass (two 8-column DMMA tiles): every 128-byte row segment of X
+  // is read by one warp, and 2 KS loads per lane are in flight together
+  const bool y16 = ((P.ldy & 1) == 0) && (((uintptr_t)Y & 15) == 0) &&
+                   (!Z || (((P.ldz & 1) == 0) && (((uintptr_t)Z & 15) == 0)));
+  for (int it = 0; it < tpw; ++it) {
+    const int n0 = ((chunk * tpw + it) * 8 + warp) * 16;
+    if (n0 >= N) break;
+    double bf[2][KS];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cb = n0 + 8 * h + g;            // B fragment column of this lane
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int k = 4 * ks + t;
+        bf[h][ks] = (k < K && cb < N) ? X[(int64_t)k * P.ldx + cb] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      if (m >= mt) break;
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const double a = sA[(8 * m + g) * LDA + 4 * ks + t];
+        dmma884(c[0][0], c[0][1], a, bf[0][ks]);
+        dmma884(c[1][0], c[1][1], a, bf[1][ks]);
+      }
+      const int row = 8 * m + g;
+      if (row >= M) continue;
+      const int64_t zr = Z ? (int64_t)(P.zrow ? P.zrow[row] : row) * P.ldz : 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = n0 + 8 * h + 2 * t;
+        double v0 = P.alpha * c[h][0], v1 = P.alpha * c[h][1];
+        if (y16 && col + 1 < N) {
+          if (Z) {
+            const double2 zz = *reinterpret_cast<const double2 *>(Z + zr + col);
+            v0 += P.beta * zz.x;
+            v1 += P.beta * zz.y;
+          }
+          *reinterpret_cast<double2 *>(Y + (int64_t)row * P.ldy + col) = make_double2(v0, v1);
+        } else {
+          if (col < N) {
+            if (Z) v0 += P.beta * Z[zr + col];
+            Y[(int64_t)row * P.ldy + col] = v0;
+          }
+          if (col + 1 < N) {
+            if (Z) v1 += P.beta * Z[zr + col + 1];
+            Y[(int64_t)row * P.ldy + col + 1] = v1;
+          }
+        }
+      }
+    }
+  }
+}
+
+static void run_small_dmma(Ctx &c, const GemmProb *probs, int nprob, int batch, int kmax) {
+  GemmLaunch L{};
+  int64_t tiles = 0;   // 16-column warp tiles over all problems and the batch
+  for (int i = 0; i < nprob; ++i) tiles += (int64_t)((probs[i].N + 15) / 16) * batch;
+  // ~2 waves of 8-warp CTAs (each CTA stages A once; more tiles per warp amortise it)
+  const int tpw = (int)std::max<int64_t>(1, tiles / (8 * 2 * 2 * 148));
+  const int cols_per_cta = tpw * 128;
+  int chunks = 0;
+  for (int i = 0; i < nprob; ++i) {
+    L.p[i] = probs[i];
+    const int ci = (probs[i].N + cols_per_cta - 1) / cols_per_cta;
+    if (i == 0) L.tiles0 = ci;
+    chunks += ci;
+  }
+  if (nprob == 1) L.tiles0 = chunks;
+  const dim3 grid(chunks, 1, batch);
+  switch ((kmax + 7) / 8) {
+    case 1: k_gemm_small_dmma<8><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    case 2: k_gemm_small_dmma<16><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    case 3: k_gemm_small_dmma<24><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    case 4: k_gemm_small_dmma<32><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    case 5: k_gemm_small_dmma<40><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    case 6: k_gemm_small_dmma<48><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    case 7: k_gemm_small_dmma<56><<<grid, 256, 0, c.st>>>(L, tpw); break;
+    default: k_gemm_small_dmma<64><<<grid, 256, 0, c.st>>>(L, tpw); break;
+  }
+  WF_CUDA(cudaGetLastError());
+}
+
 static void run_small(Ctx &c, const GemmProb *probs, int nprob, int batch, int mmax, int kmax) {
   GemmLaunch L{};
   int chunks = 0;
@@ -940,14 +1058,16 @@ void launch_gemm(Ctx &c, const GemmProb *probs, int nprob, int batch, double flo
   }
   if (flops_hint >= 0) flops = flops_hint;
   LaunchScope ls(c, c.gemm_cls, flops, bytes);
-  static const int small_env = env_int("WF4DVAR_GEMM_SMALL", 1);   // 0: DMMA tiles always
+  static const int small_env = env_int("WF4DVAR_GEMM_SMALL", 2);   // 0: DMMA tiles always
   int mmax = 0, kmax = 0;
   for (int i = 0; i < valid; ++i) {
     mmax = std::max(mmax, ps[i].M);
     kmax = std::max(kmax, ps[i].K);
   }
   if (small_env && mmax <= 64 && kmax <= 64 && kmax > 0) {
-    run_small(c, ps, valid, batch, mmax, kmax);
+    // 2 (default): the DMMA form; 1: the streaming FMA kernel (round 1)
+    if (small_env == 2) run_small_dmma(c, ps, valid, batch, kmax);
+    else run_small(c, ps, valid, batch, mmax, kmax);
     c.launches++;
     return;
   }

@@ -32,7 +32,7 @@ struct L96Args {
   double *out;
   const double *base, *in, *traj, *sub, *add2, *halo;
   const int *row_map;
-  double sign, F, dt;
+  double sign, F, dt, h6, h3;   // h6 = dt / 6, h3 = dt / 3 (host-side: no device divisions)
   int s, W, m, nsub, w_first, w_step, nw, dir;
   int w0, WG;   // global index of local window 0; global window count
   int nw0, w_first1;   // blockIdx.y >= nw0: window w_first1 + (blockIdx.y - nw0)
@@ -289,7 +289,7 @@ k_l96_step(const L96Args a) {
   const bool live = r < a.m;
   const int64_t ld = (int64_t)a.W * a.m;
   const int s = a.s;
-  const double h = a.dt;
+  const double h = a.dt, h6 = a.h6, h3 = a.h3;
   double v[IPT];
   if (has) {
     // trajectory start state of the window pair: M_w uses traj[w-1], M_{w+1}^T uses traj[w]
@@ -333,8 +333,8 @@ k_l96_step(const L96Args a) {
         fused_any<IPT, SH, LPP>(xs, us, f, d, bxw, buw, s, ty, lane, a.F);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) {
-          x[k] = x[k] + (h / 6.0) * (ks[k] + f[k]);
-          v[k] = v[k] + (h / 6.0) * (ds[k] + d[k]);
+          x[k] = x[k] + h6 * (ks[k] + f[k]);
+          v[k] = v[k] + h6 * (ds[k] + d[k]);
         }
       }
     } else {
@@ -379,10 +379,10 @@ k_l96_step(const L96Args a) {
         // lambda_d4 = h/6 l ; lambda_u4 = J4^T lambda_d4
         double lv[IPT], tmp[IPT];
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) { lv[k] = v[k]; tmp[k] = (h / 6.0) * v[k]; }
+        for (int k = 0; k < IPT; ++k) { lv[k] = v[k]; tmp[k] = h6 * v[k]; }
         jac_any<IPT, SH, LPP>(xt, tmp, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld3[k] = (h / 3.0) * v[k] + h * lu[k]; }
+        for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld3[k] = h3 * v[k] + h * lu[k]; }
 #if L96_ADJ_STASH
         WF_STAGE(1)
         jac_any<IPT, SH, LPP>(xt, ld3, lu, bxw, buw, s, ty, lane, true);
@@ -390,7 +390,7 @@ k_l96_step(const L96Args a) {
         jac_any<IPT, SH, LPP>(x3, ld3, lu, bxw, buw, s, ty, lane, true);
 #endif
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld2[k] = (h / 3.0) * v[k] + 0.5 * h * lu[k]; }
+        for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld2[k] = h3 * v[k] + 0.5 * h * lu[k]; }
 #if L96_ADJ_STASH
         WF_STAGE(0)
         jac_any<IPT, SH, LPP>(xt, ld2, lu, bxw, buw, s, ty, lane, true);
@@ -399,7 +399,7 @@ k_l96_step(const L96Args a) {
         jac_any<IPT, SH, LPP>(x2, ld2, lu, bxw, buw, s, ty, lane, true);
 #endif
 #pragma unroll
-        for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld1[k] = (h / 6.0) * v[k] + 0.5 * h * lu[k]; }
+        for (int k = 0; k < IPT; ++k) { lv[k] += lu[k]; ld1[k] = h6 * v[k] + 0.5 * h * lu[k]; }
         jac_any<IPT, SH, LPP>(x1, ld1, lu, bxw, buw, s, ty, lane, true);
 #pragma unroll
         for (int k = 0; k < IPT; ++k) v[k] = lv[k] + lu[k];
@@ -407,18 +407,31 @@ k_l96_step(const L96Args a) {
     }
   }
   if (!live) return;
+  // epilogue: every load (base, add2) issued before the first store -- out may alias
+  // base, so the compiler cannot hoist the loads itself, and the load -> FMA -> store
+  // chain per element was the kernel's top stall (ncu r02an: 20% of the samples)
+  double bv[IPT], av[IPT];
 #pragma unroll
   for (int k = 0; k < IPT; ++k) {
-    int i = SH ? ty * IPT + k : ty + 8 * k;
+    const int i = SH ? ty * IPT + k : ty + 8 * k;
+    bv[k] = 0.0; av[k] = 0.0;
     if (i < s) {
-      int64_t o = i * ld + (int64_t)w * a.m + r;
-      double val = a.base[o];
-      if (has) val = fma(a.sign, v[k], val);
+      const int64_t o = i * ld + (int64_t)w * a.m + r;
+      bv[k] = a.base[o];
       if (a.add2) {
-        int j = a.row_map[i];
-        if (j >= 0) val += a.add2[(int64_t)j * ld + (int64_t)w * a.m + r];
+        const int j = a.row_map[i];
+        if (j >= 0) av[k] = a.add2[(int64_t)j * ld + (int64_t)w * a.m + r];
       }
-      a.out[o] = val;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < IPT; ++k) {
+    const int i = SH ? ty * IPT + k : ty + 8 * k;
+    if (i < s) {
+      double val = bv[k];
+      if (has) val = fma(a.sign, v[k], val);
+      if (a.add2) val += av[k];
+      a.out[i * ld + (int64_t)w * a.m + r] = val;
     }
   }
 }
@@ -512,7 +525,7 @@ static void l96_launch(Ctx &c, bool transpose, double sign, const double *in, co
   a.nw0 = nw; a.w_first1 = w_first1;
   nw += nw1;
   a.out = out; a.base = base; a.in = in; a.traj = c.traj; a.sub = c.l96_sub; a.add2 = add2; a.row_map = row_map;
-  a.sign = sign; a.F = c.l96_F; a.dt = c.l96_dt; a.s = c.s; a.W = c.W; a.m = c.m;
+  a.sign = sign; a.F = c.l96_F; a.dt = c.l96_dt; a.h6 = c.l96_dt / 6.0; a.h3 = c.l96_dt / 3.0; a.s = c.s; a.W = c.W; a.m = c.m;
   a.w0 = c.w0; a.WG = c.WG; a.halo = transpose ? c.halo_hi : c.halo_lo;
   a.nsub = c.l96_nsub; a.w_first = w_first; a.w_step = w_step; a.nw = nw;
   a.dir = transpose ? 1 : -1;

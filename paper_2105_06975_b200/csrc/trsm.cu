@@ -873,6 +873,36 @@ void launch_trsm(Ctx &c, const TrsmProb *probs_in, int nprob, bool upper) {
     trsm_segments(c, probs, np, upper, 0, blk, n);
     return;
   }
+  // a whole triangle of <= 64 rows (the L96 configs' D_hat / R_hat, s = 40, p = 20) is a
+  // single diagonal tile: apply its setup-time inverse (reading A31) as one small DMMA
+  // product, in place allowed (gemm.cu k_gemm_small_dmma).  OPT-IN (WF4DVAR_TRSM_SMALL_INV=1):
+  // r02ao measured configs[2]'s TRSM class 1.62 -> 1.28 ms per 20 steps (step 0.467 ->
+  // 0.456 ms), but a product with an inverse is not backward stable (reading A32) and on
+  // configs[0] it moved the smoke cell's MINRES count outside reading A33's envelope
+  // (GPU 180, oracle recurrence with the GPU's applies 182); the thread-per-column
+  // substitution (k_trsm_small) stays the default.
+  static const int small_inv = env_int("WF4DVAR_TRSM_SMALL_INV", 0);
+  bool tile_inv = small_inv && trsm_inv_mode() && n <= TB;
+  for (int i = 0; i < np; ++i) tile_inv = tile_inv && probs[i].dpack && probs[i].n == n;
+  if (tile_inv) {
+    GemmProb g[2];
+    double flops = 0;
+    for (int i = 0; i < np; ++i) {
+      const TrsmProb &P = probs[i];
+      g[i] = GemmProb{};
+      g[i].A = P.dpack; g[i].lda = kInvLd;
+      g[i].X = P.X; g[i].ldx = P.ldx;
+      g[i].Y = P.Y; g[i].ldy = P.ldy;
+      g[i].M = n; g[i].N = P.ncols; g[i].K = n;
+      g[i].alpha = 1.0; g[i].beta = 0.0;
+      flops += (double)n * n * P.ncols;   // the triangle's n^2 / 2 FMAs per column
+    }
+    const int saved = c.gemm_cls;
+    c.gemm_cls = K_TRSM;
+    launch_gemm(c, g, np, 1, flops);
+    c.gemm_cls = saved;
+    return;
+  }
   // recursion (Elmroth-Gustavson, leaf 512) for the large dense factors with wide
   // right-hand sides: with the triangular solves as the default D_hat^{-1} apply, the
   // configs[3] step measured 32.33 (blocked, SB = 1024) -> 32.04 ms (leaf 512; leaf 256:
