@@ -341,10 +341,25 @@ __global__ void __launch_bounds__(C::NT) k_gemm_bulk(const GemmLaunch L) {
 // (one "empty" arrival per warp).
 struct TmaMaps {
   CUtensorMap a[2], x[2];   // per group: A (M x K) and X (K x N), row-major doubles
+  // L2 eviction policies of the two operand streams (0 = none).  One raster group of gm
+  // A row panels is re-read by every wave of the group, each X column panel only by the
+  // CTAs of one wave (in k lock-step): A evict_last, X evict_first keeps the group's A
+  // panels resident instead of letting the X stream push them out (ncu r02ae: 1.47 GB of
+  // DRAM traffic per configs[3] covariance product against 0.70 GB algorithmic).
+  int hint;   // 1: A evict_last, X evict_first
 };
 
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
-                                            uint64_t *bar) {
+                                            uint64_t *bar, unsigned long long pol) {
+  if (pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(
+            (unsigned)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(pol)
+        : "memory");
+    return;
+  }
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%2, %3}], [%4];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
@@ -374,12 +389,17 @@ __global__ void __launch_bounds__(C::NT) k_gemm_tma(const GemmLaunch L,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  unsigned long long pol_a = 0, pol_x = 0;
+  if (tid == 0 && T.hint) {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_a));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_x));
+  }
   auto issue = [&](int kt) {   // thread 0
     const int s = kt % C::STAGES;
     double *sA = smem + s * C::STAGE, *sB = sA + C::A_STAGE;
     mbar_arrive_expect_tx(&full[s], kBytes);
-    tma_load_2d(sA, ma, kt * C::BK, m0, &full[s]);
-    tma_load_2d(sB, mx, n0, kt * C::BK, &full[s]);
+    tma_load_2d(sA, ma, kt * C::BK, m0, &full[s], pol_a);
+    tma_load_2d(sB, mx, n0, kt * C::BK, &full[s], pol_x);
   };
 #ifdef TMA_FENCE
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
@@ -461,6 +481,10 @@ static bool run_tma(Ctx &c, const GemmLaunch &L, int nprob, int tiles) {
     if (!encode_tma(&T.a[i], p.A, p.M, p.K, p.lda, C::BK + 4, C::BM)) return false;
     if (!encode_tma(&T.x[i], p.X, p.K, p.N, p.ldx, C::BN + 4, C::BK)) return false;
   }
+  // only where a raster group spans several waves (otherwise there is nothing to keep).
+  // WF4DVAR_GEMM_L2HINT=0 disables, 2 = every TMA GEMM
+  static const int hint_env = env_int("WF4DVAR_GEMM_L2HINT", 1);
+  T.hint = hint_env == 2 || (hint_env == 1 && tiles > 4 * 148 && c.gemm_cls != K_TRSM_UPD);
   const size_t smem = C::SMEM_DOUBLES * sizeof(double) + 2 * C::STAGES * sizeof(uint64_t);
   static const cudaError_t attr =
       cudaFuncSetAttribute(k_gemm_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
