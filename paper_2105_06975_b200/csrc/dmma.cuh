@@ -23,6 +23,24 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
                : "d"(a), "d"(b));
 }
 
+// Outputs of a DMMA accumulator pair (columns 2t, 2t + 1 of one row) as ONE 16-byte store
+// when the row is 16-byte aligned: the four lanes of a quad then write two whole 32-byte
+// sectors per instruction.  Two 8-byte stores per pair leave every sector half written by
+// each instruction (round 2, r02at: see DESIGN.md section 10, the TMA-staged coupling GEMMs
+// read rows written this way).  `col` is the (even) column of v0, N the column count.
+__device__ __forceinline__ bool pair_aligned(const double *base, int64_t ld) {
+  return ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((ld & 1) == 0);
+}
+__device__ __forceinline__ void store_pair(double *dst, int col, int N, double v0, double v1,
+                                           bool aligned) {
+  if (aligned && col + 1 < N) {
+    *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
+  } else {
+    if (col < N) dst[0] = v0;
+    if (col + 1 < N) dst[1] = v1;
+  }
+}
+
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, int src_bytes) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));

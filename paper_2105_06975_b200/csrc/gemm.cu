@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
+  const bool y16 = pair_aligned(Y, P.ldy);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i) {
     int row = m0 + wm * C::WM + i * 8 + g;
@@ -71,14 +72,14 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
     int zr = Z ? (P.zrow ? P.zrow[row] : row) : 0;
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) {
+      const int col = n0 + wn * C::WN + j * 8 + 2 * t;
+      double v[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int col = n0 + wn * C::WN + j * 8 + 2 * t + h;
-        if (col >= P.N) continue;
-        double v = P.alpha * acc[i][j][h];
-        if (Z) v += P.beta * Z[(int64_t)zr * P.ldz + col];
-        Y[(int64_t)row * P.ldy + col] = v;
+        v[h] = P.alpha * acc[i][j][h];
+        if (Z && col + h < P.N) v[h] += P.beta * Z[(int64_t)zr * P.ldz + col + h];
       }
+      store_pair(Y + (int64_t)row * P.ldy + col, col, P.N, v[0], v[1], y16);
     }
   }
 }
@@ -125,6 +126,7 @@ __device__ __forceinline__ void tile_epilogue(const GemmProb &P, int m0, int n0,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
+  const bool y16 = pair_aligned(P.Y, P.ldy);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i) {
     int row = m0 + wm * C::WM + i * 8 + g;
@@ -132,14 +134,14 @@ __device__ __forceinline__ void tile_epilogue(const GemmProb &P, int m0, int n0,
     int zr = P.Z ? (P.zrow ? P.zrow[row] : row) : 0;
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) {
+      const int col = n0 + wn * C::WN + j * 8 + 2 * t;
+      double v[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int col = n0 + wn * C::WN + j * 8 + 2 * t + h;
-        if (col >= P.N) continue;
-        double v = P.alpha * acc[i][j][h];
-        if (P.Z) v += P.beta * P.Z[(int64_t)zr * P.ldz + col];
-        P.Y[(int64_t)row * P.ldy + col] = v;
+        v[h] = P.alpha * acc[i][j][h];
+        if (P.Z && col + h < P.N) v[h] += P.beta * P.Z[(int64_t)zr * P.ldz + col + h];
       }
+      store_pair(P.Y + (int64_t)row * P.ldy + col, col, P.N, v[0], v[1], y16);
     }
   }
 }
@@ -341,11 +343,11 @@ __global__ void __launch_bounds__(C::NT) k_gemm_bulk(const GemmLaunch L) {
 // (one "empty" arrival per warp).
 struct TmaMaps {
   CUtensorMap a[2], x[2];   // per group: A (M x K) and X (K x N), row-major doubles
-  // L2 eviction policies of the two operand streams (0 = none).  One raster group of gm
-  // A row panels is re-read by every wave of the group, each X column panel only by the
-  // CTAs of one wave (in k lock-step): A evict_last, X evict_first keeps the group's A
-  // panels resident instead of letting the X stream push them out (ncu r02ae: 1.47 GB of
-  // DRAM traffic per configs[3] covariance product against 0.70 GB algorithmic).
+  // L2 eviction hints on the two operand streams (opt-in experiment, r02ar).  One raster
+  // group of gm A row panels is re-read by every wave of the group, each X column panel
+  // only by the CTAs of one wave (in k lock-step): A evict_last / X evict_first was meant to
+  // keep the group's A panels resident (ncu r02ae: 1.47 GB of DRAM traffic per configs[3]
+  // covariance product against 0.70 GB algorithmic); measured without effect.
   int hint;   // 1: A evict_last, X evict_first
 };
 
@@ -451,9 +453,15 @@ static bool encode_tma(CUtensorMap *map, const double *base, int64_t rows, int64
   const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t estr[2] = {1, 1};
+  // probes only (r02as): 0 = no L2 promotion, 1 = 64 B, 2 = 128 B, 3 (default) = 256 B
+  static const int promo_env = env_int("WF4DVAR_TMA_L2PROMO", 3);
+  const CUtensorMapL2promotion promo =
+      promo_env == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+      : promo_env == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+      : promo_env == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides,
             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
          CUDA_SUCCESS;
 }
 
@@ -482,8 +490,11 @@ static bool run_tma(Ctx &c, const GemmLaunch &L, int nprob, int tiles) {
     if (!encode_tma(&T.x[i], p.X, p.K, p.N, p.ldx, C::BN + 4, C::BK)) return false;
   }
   // only where a raster group spans several waves (otherwise there is nothing to keep).
-  // WF4DVAR_GEMM_L2HINT=0 disables, 2 = every TMA GEMM
-  static const int hint_env = env_int("WF4DVAR_GEMM_L2HINT", 1);
+  // OPT-IN (WF4DVAR_GEMM_L2HINT=1; 2 = every TMA GEMM): r02ar measured no gain on
+  // configs[3] -- DRAM reads per covariance product 1.6-1.9 GB without and 1.8-2.2 GB
+  // with the hints (raster groups of 16 / 24 / 32 row panels alike), step 30.56 ms in
+  // every setting
+  static const int hint_env = env_int("WF4DVAR_GEMM_L2HINT", 0);
   T.hint = hint_env == 2 || (hint_env == 1 && tiles > 4 * 148 && c.gemm_cls != K_TRSM_UPD);
   const size_t smem = C::SMEM_DOUBLES * sizeof(double) + 2 * C::STAGES * sizeof(uint64_t);
   static const cudaError_t attr =

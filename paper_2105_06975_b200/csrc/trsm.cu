@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   double *Y = P.Y;
   const double *X = P.X;
   const int ncols = P.ncols;
+  const bool y16 = pair_aligned(Y, P.ldy);
 
   for (int it = 0; it < ntile; ++it) {
     const int ti = UPPER ? (ntile - 1 - it) : it;
@@ -161,12 +162,10 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
         const int rr = (warp + 4 * q) * 8 + g;
         if (rr >= nr) continue;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int cc = j * 8 + 2 * t + h;
-            if (c0 + cc < ncols) Y[(int64_t)(r0 + rr) * P.ldy + c0 + cc] = ya[q][j][h];
-          }
+        for (int j = 0; j < NJ; ++j) {
+          const int cc = c0 + j * 8 + 2 * t;
+          store_pair(Y + (int64_t)(r0 + rr) * P.ldy + cc, cc, ncols, ya[q][j][0], ya[q][j][1], y16);
+        }
       }
       __syncthreads();   // Y rows visible to the CTA; sG / sT free for the next tile
       continue;
@@ -299,6 +298,7 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
+  const bool y16 = pair_aligned(P.Y, P.ldy);
   const int ncols = P.ncols;
   // the inverse diagonal tile and this tile's X rows: in flight under the dependency
   // waits and the products (X_t is read only here; in place, only this CTA writes Y_t)
@@ -435,12 +435,10 @@ __global__ void __launch_bounds__(128) k_trsm_df(const TrsmDfArgs L) {
     const int rr = (warp + 4 * q) * 8 + g;
     if (rr >= nr) continue;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int cc = j * 8 + 2 * t + h;
-        if (c0 + cc < ncols) P.Y[(int64_t)(r0 + rr) * P.ldy + c0 + cc] = ya[q][j][h];
-      }
+    for (int j = 0; j < NJ; ++j) {
+      const int cc = c0 + j * 8 + 2 * t;
+      store_pair(P.Y + (int64_t)(r0 + rr) * P.ldy + cc, cc, ncols, ya[q][j][0], ya[q][j][1], y16);
+    }
   }
   // publish Y_t of this panel, then count this CTA out of the launch
   __threadfence();
