@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
   const bool y16 = pair_aligned(Y, P.ldy);
+  const bool z16 = Z && pair_aligned(Z, P.ldz);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i) {
     int row = m0 + wm * C::WM + i * 8 + g;
@@ -73,11 +74,17 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) {
       const int col = n0 + wn * C::WN + j * 8 + 2 * t;
-      double v[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        v[h] = P.alpha * acc[i][j][h];
-        if (Z && col + h < P.N) v[h] += P.beta * Z[(int64_t)zr * P.ldz + col + h];
+      double v[2] = {P.alpha * acc[i][j][0], P.alpha * acc[i][j][1]};
+      if (Z) {
+        const double *zp = Z + (int64_t)zr * P.ldz + col;
+        if (z16 && col + 1 < P.N) {
+          const double2 z = *reinterpret_cast<const double2 *>(zp);
+          v[0] += P.beta * z.x;
+          v[1] += P.beta * z.y;
+        } else {
+          if (col < P.N) v[0] += P.beta * zp[0];
+          if (col + 1 < P.N) v[1] += P.beta * zp[1];
+        }
       }
       store_pair(Y + (int64_t)row * P.ldy + col, col, P.N, v[0], v[1], y16);
     }
@@ -127,6 +134,7 @@ __device__ __forceinline__ void tile_epilogue(const GemmProb &P, int m0, int n0,
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
   const bool y16 = pair_aligned(P.Y, P.ldy);
+  const bool z16 = P.Z && pair_aligned(P.Z, P.ldz);
 #pragma unroll
   for (int i = 0; i < C::FM; ++i) {
     int row = m0 + wm * C::WM + i * 8 + g;
@@ -135,11 +143,17 @@ __device__ __forceinline__ void tile_epilogue(const GemmProb &P, int m0, int n0,
 #pragma unroll
     for (int j = 0; j < C::FN; ++j) {
       const int col = n0 + wn * C::WN + j * 8 + 2 * t;
-      double v[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        v[h] = P.alpha * acc[i][j][h];
-        if (P.Z && col + h < P.N) v[h] += P.beta * P.Z[(int64_t)zr * P.ldz + col + h];
+      double v[2] = {P.alpha * acc[i][j][0], P.alpha * acc[i][j][1]};
+      if (P.Z) {
+        const double *zp = P.Z + (int64_t)zr * P.ldz + col;
+        if (z16 && col + 1 < P.N) {
+          const double2 z = *reinterpret_cast<const double2 *>(zp);
+          v[0] += P.beta * z.x;
+          v[1] += P.beta * z.y;
+        } else {
+          if (col < P.N) v[0] += P.beta * zp[0];
+          if (col + 1 < P.N) v[1] += P.beta * zp[1];
+        }
       }
       store_pair(P.Y + (int64_t)row * P.ldy + col, col, P.N, v[0], v[1], y16);
     }
@@ -371,14 +385,16 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
 
 template <class C>
 __global__ void __launch_bounds__(C::NT) k_gemm_tma(const GemmLaunch L,
-                                                   const __grid_constant__ TmaMaps T) {
+                                                   const __grid_constant__ TmaMaps T,
+                                                   const TmaMaps *Tg) {
   extern __shared__ __align__(1024) double smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + C::SMEM_DOUBLES);
   uint64_t *empty = full + C::STAGES;
   int gi, m0, n0;
   tile_coords<C>(L, blockIdx.x, gi, m0, n0);
   const GemmProb &P = L.p[gi];
-  const CUtensorMap *ma = &T.a[gi], *mx = &T.x[gi];
+  // Tg (probe r02au, WF4DVAR_TMA_DESC_GLOBAL=1): the same maps in global memory
+  const CUtensorMap *ma = Tg ? &Tg->a[gi] : &T.a[gi], *mx = Tg ? &Tg->x[gi] : &T.x[gi];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int nk = (P.K + C::BK - 1) / C::BK;
@@ -496,11 +512,41 @@ static bool run_tma(Ctx &c, const GemmLaunch &L, int nprob, int tiles) {
   // every setting
   static const int hint_env = env_int("WF4DVAR_GEMM_L2HINT", 0);
   T.hint = hint_env == 2 || (hint_env == 1 && tiles > 4 * 148 && c.gemm_cls != K_TRSM_UPD);
-  const size_t smem = C::SMEM_DOUBLES * sizeof(double) + 2 * C::STAGES * sizeof(uint64_t);
+  // WF4DVAR_TMA_SMEM_PAD (probe r02au): extra dynamic shared memory, e.g. 40000 -> one
+  // k_gemm_tma CTA per SM
+  static const int pad_env = env_int("WF4DVAR_TMA_SMEM_PAD", 0);
+  const size_t smem =
+      C::SMEM_DOUBLES * sizeof(double) + 2 * C::STAGES * sizeof(uint64_t) + (size_t)pad_env;
   static const cudaError_t attr =
       cudaFuncSetAttribute(k_gemm_tma<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   WF_CUDA(attr);
-  k_gemm_tma<C><<<tiles, C::NT, smem, c.st>>>(L, T);
+  // WF4DVAR_TMA_CARVEOUT (probe r02aw): preferred shared-memory carve-out of the kernel in
+  // percent (100 = the maximum, so the SM's L1 / shared split never changes under it)
+  static const int carve_env = env_int("WF4DVAR_TMA_CARVEOUT", -1);
+  static const cudaError_t attr_carve =
+      carve_env >= 0 ? cudaFuncSetAttribute(k_gemm_tma<C>,
+                                            cudaFuncAttributePreferredSharedMemoryCarveout, carve_env)
+                     : cudaSuccess;
+  WF_CUDA(attr_carve);
+  // probe (r02au): descriptors read from a per-launch slot in global memory instead of the
+  // kernel parameter space (slot ring: pinned host copy -> device copy on the launch stream)
+  static const int desc_global = env_int("WF4DVAR_TMA_DESC_GLOBAL", 0);
+  const TmaMaps *Tg = nullptr;
+  if (desc_global) {
+    constexpr int kSlots = 4096;
+    static TmaMaps *hring = nullptr, *dring = nullptr;
+    static unsigned next = 0;
+    if (!hring) {
+      WF_CUDA(cudaMallocHost(&hring, sizeof(TmaMaps) * kSlots));
+      WF_CUDA(cudaMalloc(&dring, sizeof(TmaMaps) * kSlots));
+    }
+    const unsigned slot = next++ % kSlots;
+    hring[slot] = T;
+    WF_CUDA(cudaMemcpyAsync(dring + slot, hring + slot, sizeof(TmaMaps), cudaMemcpyHostToDevice,
+                            c.st));
+    Tg = dring + slot;
+  }
+  k_gemm_tma<C><<<tiles, C::NT, smem, c.st>>>(L, T, Tg);
   WF_CUDA(cudaGetLastError());
   return true;
 }
