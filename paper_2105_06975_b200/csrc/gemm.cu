@@ -22,6 +22,23 @@ struct GemmLaunch {
   int gm;           // raster group height (M-tiles sharing each X panel in L2)
 };
 
+// Z (the beta term) loads of the epilogues.  -DGEMM_Z_LDCG (probe r02az): L2-only loads,
+// so an in-place product (Z = Y) leaves no L1 lines of rows that a later kernel rewrites
+__device__ __forceinline__ double ld_z(const double *p) {
+#ifdef GEMM_Z_LDCG
+  return __ldcg(p);
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ double2 ld_z2(const double *p) {
+#ifdef GEMM_Z_LDCG
+  return __ldcg(reinterpret_cast<const double2 *>(p));
+#else
+  return *reinterpret_cast<const double2 *>(p);
+#endif
+}
+
 template <class C, bool V16>
 __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
   extern __shared__ __align__(16) double smem[];
@@ -78,12 +95,12 @@ __global__ void __launch_bounds__(C::NT) k_gemm(const GemmLaunch L) {
       if (Z) {
         const double *zp = Z + (int64_t)zr * P.ldz + col;
         if (z16 && col + 1 < P.N) {
-          const double2 z = *reinterpret_cast<const double2 *>(zp);
+          const double2 z = ld_z2(zp);
           v[0] += P.beta * z.x;
           v[1] += P.beta * z.y;
         } else {
-          if (col < P.N) v[0] += P.beta * zp[0];
-          if (col + 1 < P.N) v[1] += P.beta * zp[1];
+          if (col < P.N) v[0] += P.beta * ld_z(zp);
+          if (col + 1 < P.N) v[1] += P.beta * ld_z(zp + 1);
         }
       }
       store_pair(Y + (int64_t)row * P.ldy + col, col, P.N, v[0], v[1], y16);
@@ -147,12 +164,12 @@ __device__ __forceinline__ void tile_epilogue(const GemmProb &P, int m0, int n0,
       if (P.Z) {
         const double *zp = P.Z + (int64_t)zr * P.ldz + col;
         if (z16 && col + 1 < P.N) {
-          const double2 z = *reinterpret_cast<const double2 *>(zp);
+          const double2 z = ld_z2(zp);
           v[0] += P.beta * z.x;
           v[1] += P.beta * z.y;
         } else {
-          if (col < P.N) v[0] += P.beta * zp[0];
-          if (col + 1 < P.N) v[1] += P.beta * zp[1];
+          if (col < P.N) v[0] += P.beta * ld_z(zp);
+          if (col + 1 < P.N) v[1] += P.beta * ld_z(zp + 1);
         }
       }
       store_pair(P.Y + (int64_t)row * P.ldy + col, col, P.N, v[0], v[1], y16);

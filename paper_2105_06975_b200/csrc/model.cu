@@ -350,8 +350,15 @@ constexpr int heat_seq_ctas() {
   return by_smem < by_reg ? by_smem : by_reg;
 }
 
+// -DHEAT_SEQ_MAXNREG=n (probe r02ay): cap the kernel's registers below the 64 that, with
+// two 4-warp k_gemm_tma CTAs at 192, fill an SM's register file exactly
 template <int H, int R, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, heat_seq_ctas<H, R, WARPS>())
+__global__ void
+#ifdef HEAT_SEQ_MAXNREG
+__maxnreg__(HEAT_SEQ_MAXNREG)
+#else
+__launch_bounds__(WARPS * 32, heat_seq_ctas<H, R, WARPS>())
+#endif
 k_heat_iir_seq(double *out, const double *base, const double *in, const double *add2,
                const int *row_map, double rho, double gain, int s, int W, int m, int w_first,
                int w_step, int nw, int dir, const double *halo, int w0, int WG) {

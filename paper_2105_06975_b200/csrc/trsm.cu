@@ -87,7 +87,6 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   const double *X = P.X;
   const int ncols = P.ncols;
   const bool y16 = pair_aligned(Y, P.ldy);
-  const bool x16 = pair_aligned(X, P.ldx);
 
   for (int it = 0; it < ntile; ++it) {
     const int ti = UPPER ? (ntile - 1 - it) : it;
@@ -126,23 +125,14 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
     for (int i = 0; i < C::FM; ++i) {
       int rr = wm * C::WM + i * 8 + g;
 #pragma unroll
-      for (int j = 0; j < C::FN; ++j) {
-        const int cc = wn * C::WN + j * 8 + 2 * t;
-        double xv[2] = {0.0, 0.0};
-        if (rr < nr) {
-          const double *xp = X + (int64_t)(r0 + rr) * P.ldx + c0 + cc;
-          if (x16 && c0 + cc + 1 < ncols) {
-            const double2 x2 = *reinterpret_cast<const double2 *>(xp);
-            xv[0] = x2.x;
-            xv[1] = x2.y;
-          } else {
-            if (c0 + cc < ncols) xv[0] = xp[0];
-            if (c0 + cc + 1 < ncols) xv[1] = xp[1];
-          }
+      for (int j = 0; j < C::FN; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          int cc = wn * C::WN + j * 8 + 2 * t + h;
+          double xv = 0.0;
+          if (rr < nr && c0 + cc < ncols) xv = X[(int64_t)(r0 + rr) * P.ldx + c0 + cc];
+          sT[rr * (NB + 1) + cc] = xv - acc[i][j][h];
         }
-        sT[rr * (NB + 1) + cc] = xv[0] - acc[i][j][0];
-        sT[rr * (NB + 1) + cc + 1] = xv[1] - acc[i][j][1];
-      }
     }
     if (INV && dpk) {
       // ---- Y_i = G_ii^{-1} T_i on the tensor pipe (the setup-time inverse in sG,
