@@ -62,6 +62,47 @@ def test_gemm_strided_views_and_odd_ld():
     torch.testing.assert_close(Y, A @ X, rtol=1e-13, atol=1e-13)
 
 
+def test_gemm_pair_store_alignment_paths():
+    """The epilogues write each accumulator pair as one 16-byte store (and read the beta term
+    as one 16-byte load) only when base and leading dimension allow it: even ld with an
+    8-byte-offset base, and an odd last column, must take the 8-byte path."""
+    g = torch.Generator().manual_seed(11)
+    A = torch.randn(130, 96, generator=g, dtype=torch.float64).cuda()
+    X = torch.randn(96, 300, generator=g, dtype=torch.float64).cuda()
+    Zb = torch.randn(130, 302, generator=g, dtype=torch.float64).cuda()
+    Yb = torch.full((130, 302), 7.0, dtype=torch.float64, device="cuda")
+    ref = 2.0 * (A @ X)
+    for yo, zo, ncol in ((1, 1, 300), (0, 1, 300), (1, 0, 300), (0, 0, 299), (0, 0, 300)):
+        Yb.fill_(7.0)
+        Y, Z = Yb[:, yo:yo + ncol], Zb[:, zo:zo + ncol]
+        L().test_gemm(A, X[:, :ncol], Y, alpha=2.0, beta=-1.0, Z=Z)
+        torch.testing.assert_close(Y, ref[:, :ncol] - Z, rtol=1e-13, atol=1e-12)
+        # nothing written outside the view
+        assert (Yb[:, :yo] == 7.0).all() and (Yb[:, yo + ncol:] == 7.0).all()
+
+
+@pytest.mark.parametrize("upper", [False, True])
+def test_trsm_pair_store_misaligned_base(upper):
+    """Contiguous operands whose storage starts 8 bytes off a 16-byte boundary (even ld):
+    the panel / dataflow kernels must fall back to 8-byte stores."""
+    n, ncols = 600, 40
+    g = torch.Generator().manual_seed(3)
+    M = torch.randn(n, n, generator=g, dtype=torch.float64)
+    Gl = torch.linalg.cholesky(M @ M.T / n + torch.eye(n, dtype=torch.float64))
+    F = (Gl.T if upper else Gl).contiguous()
+    X = torch.randn(n, ncols, generator=g, dtype=torch.float64)
+    ref = torch.linalg.solve_triangular(F, X, upper=upper)
+    buf = torch.zeros(n * ncols + 2, dtype=torch.float64, device="cuda")
+    for off in (0, 1):
+        Y = buf[off:off + n * ncols].view(n, ncols)
+        assert Y.is_contiguous() and (Y.data_ptr() % 16 == 8 * off)
+        buf.zero_()
+        L().test_trsm(F.cuda(), X.cuda(), Y, upper=upper)
+        torch.cuda.synchronize()
+        assert ((Y.cpu() - ref).norm() / ref.norm()).item() <= 1e-12
+        assert buf[off + n * ncols:].abs().max().item() == 0.0 and buf[:off].abs().sum().item() == 0.0
+
+
 @pytest.mark.parametrize("n,ncols,blk", [(5, 3, 0), (64, 64, 0), (130, 17, 0), (600, 40, 0),
                                          (1000, 336, 0), (2048, 96, 0), (500, 21, 50),
                                          (256, 64, 64),
