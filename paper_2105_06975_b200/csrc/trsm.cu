@@ -243,6 +243,11 @@ __global__ void __launch_bounds__(128) k_trsm(const TrsmLaunch L) {
   // async-proxy (TMA) access
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 #endif
+#ifdef TRSM_END_FENCE
+  // probe r02bd: device-scope fence, then the proxy fence, after the last Y stores
+  __threadfence();
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+#endif
 }
 
 // ---- Dataflow form of one segment (default where it applies, r02o): one CTA per
